@@ -1,0 +1,173 @@
+"""Seeded synthetic particle sets for the BASELINE configurations.
+
+* ``uniform_box`` regenerates the reference's UniformBox stream bit-exactly
+  (splitmix64, workload.py:42-84 of the reference): draw t (0-based, three
+  per particle, x-y-z order) is ``mix(seed + (t+1)*GAMMA) >> 11`` scaled by
+  2^-53 and by the box side.  The sequential stream is a pure function of
+  the counter, so it vectorises.
+* ``nfw_halos`` is the clustered generator of BASELINE configs 2-5, which
+  the reference does not have.  Rules chosen and recorded here:
+  halo particle counts are drawn from dN/dM ~ M^-1.9 on [100, 50000] and
+  rescaled (largest remainder) to sum to round(f_halo * N); r_vir from an
+  overdensity of 200 times the mean particle density (so it scales with the
+  halo's particle count); radii by inverting the NFW enclosed mass
+  m(x) = ln(1+x) - x/(1+x) up to x = c; isotropic directions; periodic wrap
+  into [0, L); positions rounded to fp32 when ``fp32`` is set.  Velocities
+  are generated (sigma ~ M^(1/3)) but never read by the density pass.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+_MIX1 = np.uint64(0xBF58476D1CE4E5B9)
+_MIX2 = np.uint64(0x94D049BB133111EB)
+_TO_UNIT = 2.0 ** -53
+
+
+def _splitmix_values(seed: int, start: int, count: int) -> np.ndarray:
+    t = np.arange(start + 1, start + count + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        s = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + t * _GAMMA
+        z = (s ^ (s >> np.uint64(30))) * _MIX1
+        z = (z ^ (z >> np.uint64(27))) * _MIX2
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def uniform01(seed: int, count: int, start: int = 0) -> np.ndarray:
+    """The reference's splitmix64 uniform doubles in [0, 1)."""
+    return (_splitmix_values(seed, start, count) >> np.uint64(11)).astype(np.float64) * _TO_UNIT
+
+
+def uniform_box(n: int, seed: int, box: float = 1.0) -> np.ndarray:
+    """(n, 3) positions identical to the reference generate(UNIFORM_BOX)."""
+    u = uniform01(seed, 3 * n).reshape(n, 3)
+    v = u * box
+    over = v >= box
+    if over.any():
+        v[over] = np.nextafter(box, 0.0)
+    return v
+
+
+def nfw_enclosed(x):
+    return np.log1p(x) - x / (1.0 + x)
+
+
+def _nfw_radii(rng, count: int, c: float, r_vir: float, x_max: float) -> np.ndarray:
+    """Inverse-CDF sampling of the NFW profile truncated at x_max = r/r_s."""
+    u = rng.random(count) * nfw_enclosed(x_max)
+    lo = np.zeros(count)
+    hi = np.full(count, x_max)
+    for _ in range(60):  # bisection; m(x) is monotone
+        mid = 0.5 * (lo + hi)
+        below = nfw_enclosed(mid) < u
+        lo = np.where(below, mid, lo)
+        hi = np.where(below, hi, mid)
+    return 0.5 * (lo + hi) * (r_vir / c)
+
+
+def _directions(rng, count: int) -> np.ndarray:
+    v = rng.normal(size=(count, 3))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    return v
+
+
+def _largest_remainder(weights: np.ndarray, total: int) -> np.ndarray:
+    raw = weights / weights.sum() * total
+    base = np.floor(raw).astype(np.int64)
+    rem = total - int(base.sum())
+    if rem > 0:
+        order = np.argsort(-(raw - base), kind="stable")
+        base[order[:rem]] += 1
+    return base
+
+
+def nfw_halos(n: int, box: float, n_halos: int, seed: int, concentration: float = 10.0,
+              halo_fraction: float = 0.8, m_min: float = 100.0, m_max: float = 50000.0,
+              slope: float = -1.9, fp32: bool = True, truncate: float = 1.0):
+    """Clustered set: ``halo_fraction`` of N in NFW halos, rest uniform.
+
+    Returns (pos (n,3) float64, vel (n,3) float32, halo_counts).
+    """
+    rng = np.random.default_rng(seed)
+    n_halo_total = int(round(halo_fraction * n))
+    # dN/dM ~ M^slope on [m_min, m_max]: inverse CDF of a power law
+    a = slope + 1.0
+    u = rng.random(n_halos)
+    masses = (m_min ** a + u * (m_max ** a - m_min ** a)) ** (1.0 / a)
+    counts = _largest_remainder(masses, n_halo_total) if n_halos else np.zeros(0, np.int64)
+    mean_density = n / box ** 3
+    centres = rng.random((n_halos, 3)) * box
+    pos = np.empty((n, 3))
+    vel = np.empty((n, 3), dtype=np.float32)
+    off = 0
+    for hcount, c0 in zip(counts, centres):
+        if hcount == 0:
+            continue
+        r_vir = (3.0 * hcount / (4.0 * math.pi * 200.0 * mean_density)) ** (1.0 / 3.0)
+        r = _nfw_radii(rng, int(hcount), concentration, r_vir, concentration * truncate)
+        pos[off:off + hcount] = c0 + r[:, None] * _directions(rng, int(hcount))
+        sigma = float(hcount) ** (1.0 / 3.0) * 0.1
+        vel[off:off + hcount] = rng.normal(0.0, sigma, (hcount, 3))
+        off += int(hcount)
+    rest = n - off
+    pos[off:] = rng.random((rest, 3)) * box
+    vel[off:] = rng.normal(0.0, 1.0, (rest, 3))
+    pos = np.mod(pos, box)
+    if fp32:
+        pos = pos.astype(np.float32).astype(np.float64)
+        # fp32 rounding can land exactly on the box side
+        pos[pos >= box] = np.float64(np.nextafter(np.float32(box), np.float32(0.0)))
+    return pos, vel, counts
+
+
+def single_halo(n: int, box: float, seed: int, concentration: float = 20.0, r_vir: float = 1.0,
+                truncate: float = 2.0, background_fraction: float = 0.05, fp32: bool = True):
+    """BASELINE config 5: one NFW halo at the box centre plus a background."""
+    rng = np.random.default_rng(seed)
+    n_bg = int(round(background_fraction * n))
+    n_h = n - n_bg
+    r = _nfw_radii(rng, n_h, concentration, r_vir, concentration * truncate)
+    pos = np.empty((n, 3))
+    pos[:n_h] = 0.5 * box + r[:, None] * _directions(rng, n_h)
+    pos[n_h:] = rng.random((n_bg, 3)) * box
+    pos = np.mod(pos, box)
+    if fp32:
+        pos = pos.astype(np.float32).astype(np.float64)
+        pos[pos >= box] = np.float64(np.nextafter(np.float32(box), np.float32(0.0)))
+    vel = rng.normal(0.0, 1.0, (n, 3)).astype(np.float32)
+    return pos, vel
+
+
+def config(number: int, seed: int | None = None):
+    """Inputs of BASELINE.json config ``number`` (1-5) as a dict."""
+    seed = number if seed is None else seed
+    if number == 1:
+        n = 32768
+        pos = uniform_box(n, seed, 1.0)
+        vel = np.random.default_rng(seed).normal(0.0, 1.0, (n, 3)).astype(np.float32)
+        return dict(pos=pos, vel=vel, mass=np.full(n, 1.0 / n), h0=np.full(n, 2.0 * n ** (-1.0 / 3.0)),
+                    k=64, box=1.0, periodic=True, fp32=False, name="C1 uniform 32768 fp64")
+    if number in (2, 3, 4):
+        n, box, halos = {2: (1 << 20, 100.0, 200), 3: (1 << 24, 100.0 * 16 ** (1.0 / 3.0), 20000),
+                         4: (1 << 27, 400.0, 150000)}[number]
+        pos, vel, _ = nfw_halos(n, box, halos, seed)
+        h0 = _initial_h(box, n, 64)
+        return dict(pos=pos, vel=vel, mass=np.full(n, 1.0 / n), h0=np.full(n, h0), k=64, box=box,
+                    periodic=True, fp32=True, name=f"C{number} NFW {n} fp32")
+    if number == 5:
+        n, box = 1 << 23, 4.0
+        pos, vel = single_halo(n, box, seed)
+        h0 = _initial_h(box, n, 128)
+        return dict(pos=pos, vel=vel, mass=np.full(n, 1.0 / n), h0=np.full(n, h0), k=128, box=box,
+                    periodic=True, fp32=True, name="C5 single NFW halo 8388608 fp32")
+    raise ValueError(f"unknown config {number}")
+
+
+def _initial_h(box: float, n: int, k: int) -> float:
+    # density.py:136-140
+    return box * (3.0 * k / (4.0 * math.pi * n)) ** (1.0 / 3.0)
