@@ -1,0 +1,129 @@
+/*
+ * sph_b200.h -- C ABI of the B200-native SPH density / smoothing-length pass.
+ *
+ * One shared library (paper_1612_06090_b200/libsph_b200.so) behind the
+ * reference's operator API.  Every entry point takes plain pointers and sizes;
+ * no torch or CUDA types cross the boundary.  The reference is a Python
+ * package (`sphlab`), so the reference-side binding is a ctypes stub
+ * (INTEGRATION.md); the Python mirror in paper_1612_06090_b200/density.py is
+ * that stub.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/sphlab):
+ *   sph_density_pass      <- compute_density_pass(particles, config,
+ *                            thread_count, max_iterations)   density.py:286-413
+ *                            (smoothing_length / density / needs_recompute
+ *                            written back into the caller's records,
+ *                            PassStats todo trace in sph_stats)
+ *   sph_sort_perm         <- build_octree(...).particle_perm   octree.py:306-348
+ *   sph_neighbor_counts   <- range_query(tree, pos_i, h_i, exclude=i).size
+ *                                                              octree.py:351-379
+ *   sph_fnv1a64           <- snapshot.checksum64 / bench.density_checksum
+ *                                                              snapshot.py:70-82,
+ *                                                              bench.py:48-50
+ * Status codes map to the reference's exceptions (density.py:69-74, 375-379,
+ * 353-357; ValueError for invalid arguments, density.py:297-301).
+ */
+#ifndef SPH_B200_H
+#define SPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_OK 0
+#define SPH_NOT_CONVERGED 1 /* -> ConvergenceError(f"{unconverged} of {n} particles still flagged after {max_iterations} iterations") */
+#define SPH_DEGENERATE 2    /* -> DegenerateWorkloadError (K-th neighbour at zero distance; bad_index) */
+#define SPH_INVALID 3       /* -> ValueError */
+#define SPH_CUDA_ERROR 4    /* -> RuntimeError(sph_last_error(ctx)) */
+#define SPH_UNSUPPORTED 5   /* -> RuntimeError: input outside what this build handles (message in sph_last_error) */
+
+#define SPH_PRECISION_F64 0 /* positions are float64 */
+#define SPH_PRECISION_F32 1 /* positions are float32 (the fp32 configs); results stay bit-exact
+                               against the fp64 reference on the widened values */
+
+#define SPH_MAX_TODO 128
+
+typedef struct sph_ctx sph_ctx;
+
+typedef struct {
+    int64_t n;              /* particle count (>= 1) */
+    int32_t k;              /* k_neighbors (DesNumNgb), >= 1 */
+    int32_t max_iterations; /* reference todo-loop budget (density.py:54) */
+    int32_t precision;      /* SPH_PRECISION_* : element type of x/y/z */
+    int32_t periodic;       /* 0: open boundaries (the reference); 1: periodic cube [0, box)^3 */
+    double box;             /* periodic box side (ignored when periodic == 0) */
+    int32_t kernel;         /* 0: Wendland C6 (the reference, kernel.py); 1: M4 cubic spline (extension) */
+    int32_t reserved;
+} sph_params;
+
+typedef struct {
+    int32_t iterations;                 /* PassStats.iteration_count */
+    int32_t n_todo;                     /* valid entries of todo_sizes */
+    int64_t todo_sizes[SPH_MAX_TODO];   /* PassStats.todo_sizes (reference growth-only trace) */
+    double t_stage_ms[8];               /* 0 h2d, 1 tree, 2 search, 3 select, 4 density, 5 finalize, 6 d2h, 7 total */
+    int64_t pair_tests;                 /* target x candidate distance evaluations, all kernels */
+    int64_t accepted_pairs;             /* pairs inside support in the density kernel */
+    int64_t search_pair_tests;          /* pair tests of the search (histogram) kernel only */
+    int64_t bad_index;                  /* first degenerate particle (original index) or -1 */
+    int64_t unconverged;                /* particles still flagged after max_iterations */
+    int32_t gpu_launches;               /* kernels launched by this call */
+    int32_t search_rounds;              /* histogram rounds (1 + retries) */
+    int32_t select_rounds;              /* band rounds */
+    int32_t n_nodes;                    /* search-tree nodes */
+    double t_kernel_ms[4];              /* device time of: 0 search, 1 select, 2 density, 3 tree build */
+} sph_stats;
+
+/* context: owns a CUDA stream and device buffers, grown on demand and
+ * reused across calls (the analogue of density.py:264-283 _WorkerScratch) */
+int sph_ctx_create(sph_ctx **out, int device);
+void sph_ctx_destroy(sph_ctx *ctx);
+const char *sph_last_error(const sph_ctx *ctx);
+int sph_device_count(void);
+
+/*
+ * Full pass on HOST buffers.  Each array is addressed as base + i * stride
+ * (bytes), so the reference's packed records (stride 224) and plain SoA
+ * arrays (stride = element size) are both accepted:
+ *   x, y, z  : positions, element type per params->precision (read)
+ *   mass     : float64 (read)
+ *   h        : float64 smoothing_length: in = initial h (drives the todo
+ *              trace only), out = converged h (K-th neighbour distance)
+ *   rho      : float64 density out
+ *   flags    : uint8 needs_recompute out (0 on success)
+ * Synchronous; host pointers are not retained.
+ */
+int sph_density_pass(sph_ctx *ctx, const sph_params *params,
+                     const void *x, const void *y, const void *z, int64_t pos_stride,
+                     const double *mass, int64_t mass_stride,
+                     double *h, int64_t h_stride,
+                     double *rho, int64_t rho_stride,
+                     uint8_t *flags, int64_t flags_stride,
+                     sph_stats *stats);
+
+/* Same pass on DEVICE-resident contiguous arrays (inputs already in HBM). */
+int sph_density_pass_device(sph_ctx *ctx, const sph_params *params,
+                            const void *d_x, const void *d_y, const void *d_z,
+                            const double *d_mass, double *d_h, double *d_rho,
+                            uint8_t *d_flags, sph_stats *stats);
+
+/* Octree particle_perm (leaf capacity 8), bit-exact with the reference.
+ * Host pointers; positions per precision (contiguous). */
+int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y,
+                  const void *z, int64_t *perm_out);
+
+/* Fixed-h neighbour counts #{j != i : (dx*dx + dy*dy) + dz*dz <= h_i*h_i}
+ * in unfused fp64, bit-exact.  periodic/box as in sph_params. */
+int sph_neighbor_counts(sph_ctx *ctx, int32_t precision, int32_t periodic, double box,
+                        int64_t n, const void *x, const void *y, const void *z,
+                        const double *h, int32_t *counts_out, sph_stats *stats);
+
+/* FNV-1a-64 over a byte buffer (host; the reference checksum64) */
+uint64_t sph_fnv1a64(const uint8_t *data, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPH_B200_H */

@@ -1,0 +1,672 @@
+// sph_api.cu -- the C ABI (include/sph_b200.h): context, buffers, and the
+// orchestration of one density pass.
+//
+// Pass structure (all on one stream):
+//   bbox -> [sync: validate] -> keys -> radix sort -> leaf levels -> perm ->
+//   sorted SoA -> search tree -> [sync: node count]
+//   HIST over all targets; while any target has < K candidates inside its
+//   radius: compact those (order-preserving) and HIST again       (search)
+//   BAND over all; while any bracket is overfull: compact, BAND again (select)
+//   DENS over all                                                 (interact)
+//   finalize: h = sqrt(d2_K), the reference's todo trace from h0 and d2_K,
+//   scatter to original order                                    (write-back)
+#include "sph_internal.cuh"
+#include "../../include/sph_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace sph;
+
+namespace {
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t c = std::max<size_t>(count, 1);
+    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    if (e == cudaSuccess) cap = c;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct sph_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cudaEvent_t ev[12];
+  // inputs / outputs for the host-pointer entry points
+  DevBuf<double> in_x, in_y, in_z, in_m, io_h, out_rho;
+  DevBuf<uint8_t> out_flags;
+  // ordering
+  DevBuf<unsigned long long> keys_in, keys, bbox_ord;
+  DevBuf<uint32_t> idx_in, idx, perm, deep_list, iota, list;
+  DevBuf<uint8_t> lvl8, lvl32, state;
+  DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4..] rounds hist
+  DevBuf<int> noff;
+  DevBuf<float4> nlo, nhi;
+  DevBuf<float> r0;
+  DevBuf<unsigned char> pos_sorted, cub_temp;
+  DevBuf<RootInfo> root;
+  DevBuf<double> t_lo, t_hi, d2k, rho_s, hfix;
+  DevBuf<int32_t> counts_s, counts_o;
+  DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
+  size_t cub_bytes = 0;
+};
+
+namespace {
+
+constexpr int kIntsFixed = 4;
+constexpr int kTB = 256;
+
+int fail(sph_ctx *c, int code, const std::string &msg) {
+  c->err = msg;
+  return code;
+}
+
+int cuda_fail(sph_ctx *c, cudaError_t e, const char *where) {
+  c->err = std::string(where) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();
+  return SPH_CUDA_ERROR;
+}
+
+#define SPH_CK(call)                                   \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+__global__ void k_iota(int n, uint32_t *a) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (uint32_t)i;
+}
+
+// reference todo trace per particle: round j (1-based) searches with
+// h_{j-1} = h0 * g^(j-1) (sequential fp64 products, density.py:227) and
+// converges when count(h) >= K  <=>  d2_K <= h*h (octree.py:185, 215)
+__global__ void k_finalize(int n, const uint32_t *__restrict__ perm, const uint8_t *__restrict__ state,
+                           const double *__restrict__ d2k, const double *__restrict__ rho_s,
+                           const double *__restrict__ h0, int max_it, double *__restrict__ h_out,
+                           double *__restrict__ rho_out, uint8_t *__restrict__ flags_out, int *rounds_hist,
+                           unsigned long long *bad) {
+  extern __shared__ int sh[];
+  for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const uint32_t o = perm[p];
+    const uint8_t st = state[p];
+    const double d = st == ST_DONE ? d2k[p] : INFINITY;
+    double hc = h0[o];
+    int r = 1;
+    bool conv = false;
+    for (; r <= max_it; ++r) {
+      if (d <= __dmul_rn(hc, hc)) { conv = true; break; }
+      hc = __dmul_rn(hc, kGrowth);
+    }
+    const int bin = conv ? r : max_it + 1;
+    atomicAdd(&sh[bin], 1);
+    if (conv && d == 0.0) atomicMin(bad, (unsigned long long)o);
+    h_out[o] = __dsqrt_rn(d);
+    rho_out[o] = st == ST_DONE ? rho_s[p] : 0.0;
+    flags_out[o] = conv ? 0 : 1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x)
+    if (sh[i]) atomicAdd(&rounds_hist[i], sh[i]);
+}
+
+template <typename T>
+__global__ void k_gather_sorted(int n, const uint32_t *__restrict__ perm, const T *__restrict__ in, T *__restrict__ out) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) out[p] = in[perm[p]];
+}
+template <typename T>
+__global__ void k_scatter_orig(int n, const uint32_t *__restrict__ perm, const T *__restrict__ in, T *__restrict__ out) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) out[perm[p]] = in[p];
+}
+
+inline int nblk(long long n, int t = kTB) { return (int)((n + t - 1) / t); }
+
+struct Timer {
+  sph_ctx *c;
+  void mark(int i) { cudaEventRecord(c->ev[i], c->stream); }
+  double ms(int a, int b) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->ev[a], c->ev[b]);
+    return t;
+  }
+};
+
+int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
+  SPH_CK(ctx->keys_in.ensure(n));
+  SPH_CK(ctx->keys.ensure(n));
+  SPH_CK(ctx->bbox_ord.ensure(6));
+  SPH_CK(ctx->idx_in.ensure(n));
+  SPH_CK(ctx->idx.ensure(n));
+  SPH_CK(ctx->perm.ensure(n));
+  SPH_CK(ctx->deep_list.ensure(n));
+  SPH_CK(ctx->iota.ensure(n));
+  SPH_CK(ctx->list.ensure(n));
+  SPH_CK(ctx->lvl8.ensure(n));
+  SPH_CK(ctx->lvl32.ensure(n));
+  SPH_CK(ctx->state.ensure(n));
+  SPH_CK(ctx->ints.ensure(kIntsFixed + (size_t)max_it + 2));
+  SPH_CK(ctx->noff.ensure(n + 1));
+  SPH_CK(ctx->nlo.ensure(2 * n + 64));
+  SPH_CK(ctx->nhi.ensure(2 * n + 64));
+  SPH_CK(ctx->r0.ensure(n));
+  SPH_CK(ctx->pos_sorted.ensure(32 * n));
+  SPH_CK(ctx->root.ensure(1));
+  SPH_CK(ctx->stats.ensure(4));
+  size_t need = std::max(cub_temp_needed((int)n), select_temp_needed((int)n));
+  if (need > ctx->cub_temp.cap) SPH_CK(ctx->cub_temp.ensure(need));
+  ctx->cub_bytes = ctx->cub_temp.cap;
+  return SPH_OK;
+}
+
+TreeBuffers tree_buffers(sph_ctx *ctx) {
+  TreeBuffers tb{};
+  tb.keys_in = ctx->keys_in.p;
+  tb.keys = ctx->keys.p;
+  tb.idx_in = ctx->idx_in.p;
+  tb.idx = ctx->idx.p;
+  tb.perm = ctx->perm.p;
+  tb.lvl8 = ctx->lvl8.p;
+  tb.lvl32 = ctx->lvl32.p;
+  tb.deep_count = ctx->ints.p + 0;
+  tb.deep_list = ctx->deep_list.p;
+  tb.err_flag = ctx->ints.p + 1;
+  tb.noff = ctx->noff.p;
+  tb.nlo = ctx->nlo.p;
+  tb.nhi = ctx->nhi.p;
+  tb.r0 = ctx->r0.p;
+  tb.pos_sorted = ctx->pos_sorted.p;
+  tb.cub_temp = ctx->cub_temp.p;
+  tb.cub_temp_bytes = ctx->cub_bytes;
+  tb.root = ctx->root.p;
+  tb.bbox_ord = ctx->bbox_ord.p;
+  return tb;
+}
+
+// bbox + validation; fills *root_h.  Synchronises once.
+int stage_root(sph_ctx *ctx, int n, int precision, const void *x, const void *y, const void *z, RootInfo *root_h,
+               int *launches) {
+  launch_bbox(ctx->stream, n, precision == SPH_PRECISION_F32 ? 1 : 0, x, y, z, ctx->bbox_ord.p, ctx->root.p,
+              launches);
+  SPH_CK(cudaMemcpyAsync(root_h, ctx->root.p, sizeof(RootInfo), cudaMemcpyDeviceToHost, ctx->stream));
+  SPH_CK(cudaStreamSynchronize(ctx->stream));
+  SPH_CK(cudaGetLastError());
+  if (root_h->nonfinite) return fail(ctx, SPH_INVALID, "positions must be finite");
+  return SPH_OK;
+}
+
+// keys .. search tree; returns the node count through *n_nodes (one sync)
+int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *x, const void *y, const void *z,
+               const double *mass, int k, float rmax, int *n_nodes, int *launches, bool search_tree) {
+  TreeBuffers tb = tree_buffers(ctx);
+  const int in32 = precision == SPH_PRECISION_F32 ? 1 : 0;
+  tree_build(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, launches);
+  if (search_tree) tree_build_search(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, rmax, launches);
+  int host[2] = {0, 0};
+  SPH_CK(cudaMemcpyAsync(&host[0], ctx->ints.p + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (search_tree)
+    SPH_CK(cudaMemcpyAsync(&host[1], ctx->noff.p + n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SPH_CK(cudaStreamSynchronize(ctx->stream));
+  SPH_CK(cudaGetLastError());
+  if (host[0])
+    return fail(ctx, SPH_UNSUPPORTED,
+                "more than 8 distinct positions share one 2^-21 octree cell: the reference tree is deeper "
+                "than the 21 levels of a 63-bit key");
+  *n_nodes = host[1];
+  return SPH_OK;
+}
+
+float compute_rmax(const RootInfo &r, int periodic, double box) {
+  if (periodic) return (float)(0.999 * box);
+  double diag = 2.0 * r.half * 1.7320508075688772 * (1.0 + 1e-6) + 4.0 * r.pad;
+  float f = (float)diag * 1.0001f;
+  return f > 0.f ? f : 1e-30f;
+}
+
+PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *prm, float rmax) {
+  PassArgs a{};
+  a.n = n;
+  a.k = k;
+  a.kernel_kind = prm ? prm->kernel : 0;
+  a.list = nullptr;
+  a.list_count = ctx->ints.p + 2;
+  a.static_count = n;
+  a.tree.nlo = ctx->nlo.p;
+  a.tree.nhi = ctx->nhi.p;
+  a.tree.n_nodes = n_nodes;
+  a.pos = ctx->pos_sorted.p;
+  a.radius = ctx->r0.p;
+  a.t_lo = ctx->t_lo.p;
+  a.t_hi = ctx->t_hi.p;
+  a.d2k = ctx->d2k.p;
+  a.rho = ctx->rho_s.p;
+  a.hfix = ctx->hfix.p;
+  a.counts = ctx->counts_s.p;
+  a.state = ctx->state.p;
+  a.work_counter = ctx->ints.p + 3;
+  a.stats = ctx->stats.p;
+  a.periodic = prm ? prm->periodic : 0;
+  a.box = prm ? prm->box : 0.0;
+  a.rmax = rmax;
+  return a;
+}
+
+// rounds of pass `mode` over targets whose state == want, compacting between
+// rounds; returns the number of rounds run
+int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int max_rounds, int *launches,
+               int *rounds_out) {
+  const int n = a.n;
+  a.list = nullptr;
+  a.static_count = n;
+  launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+  ++*launches;
+  int rounds = 1;
+  for (;;) {
+    launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, want, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
+                  ctx->cub_bytes);
+    *launches += 2;
+    int remaining = 0;
+    SPH_CK(cudaMemcpyAsync(&remaining, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SPH_CK(cudaStreamSynchronize(ctx->stream));
+    SPH_CK(cudaGetLastError());
+    if (remaining == 0) break;
+    if (rounds >= max_rounds) {
+      *rounds_out = rounds;
+      return fail(ctx, SPH_CUDA_ERROR, "neighbour search did not settle (internal round limit)");
+    }
+    a.list = ctx->list.p;
+    launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+    ++*launches;
+    ++rounds;
+  }
+  *rounds_out = rounds;
+  return SPH_OK;
+}
+
+int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const void *y, const void *z,
+                     const double *mass, const double *h0, double *h_out, double *rho_out, uint8_t *flags_out,
+                     sph_stats *st, Timer &tm) {
+  const int n = (int)prm->n;
+  const int k = prm->k;
+  const int max_it = prm->max_iterations;
+  int launches = 0;
+  { int rc0 = ensure_common(ctx, n, max_it); if (rc0) return rc0; }
+  SPH_CK(ctx->t_lo.ensure(n));
+  SPH_CK(ctx->t_hi.ensure(n));
+  SPH_CK(ctx->d2k.ensure(n));
+  SPH_CK(ctx->rho_s.ensure(n));
+  tm.mark(1);
+  RootInfo root{};
+  int rc = stage_root(ctx, n, prm->precision, x, y, z, &root, &launches);
+  if (rc) return rc;
+  if (prm->periodic) {
+    if (!(prm->box > 0.0)) return fail(ctx, SPH_INVALID, "periodic box side must be > 0");
+    for (int a2 = 0; a2 < 3; ++a2)
+      if (root.lo[a2] < 0.0 || root.hi[a2] >= prm->box)
+        return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
+  }
+  const int compute_f32 = prm->precision == SPH_PRECISION_F32 || (prm->precision == 2 && !root.not_f32);
+  const float rmax = compute_rmax(root, prm->periodic, prm->box);
+  int n_nodes = 0;
+  rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
+  if (rc) return rc;
+  tm.mark(2);
+  // ---- search ----
+  SPH_CK(cudaMemsetAsync(ctx->state.p, ST_NEED_HIST, n, ctx->stream));
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
+  ++launches;
+  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+  int hist_rounds = 0, band_rounds = 0;
+  rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
+  if (rc) return rc;
+  unsigned long long stat_h[2] = {0, 0};
+  SPH_CK(cudaMemcpyAsync(stat_h, ctx->stats.p, sizeof(stat_h), cudaMemcpyDeviceToHost, ctx->stream));
+  tm.mark(3);
+  // ---- select ----
+  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
+  if (rc) return rc;
+  tm.mark(4);
+  // ---- interact ----
+  launch_pass(ctx->stream, MODE_DENS, compute_f32, a, ctx->num_sms);
+  ++launches;
+  tm.mark(5);
+  // ---- finalize ----
+  int *rounds_hist = ctx->ints.p + kIntsFixed;
+  SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
+  const unsigned long long bad_init = ~0ull;
+  SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
+  k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
+      n, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out, rounds_hist,
+      ctx->stats.p + 2);
+  ++launches;
+  tm.mark(6);
+  std::vector<int> hist(max_it + 2);
+  unsigned long long stat_all[3] = {0, 0, 0};
+  SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
+  SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
+  SPH_CK(cudaStreamSynchronize(ctx->stream));
+  SPH_CK(cudaGetLastError());
+
+  // ---- stats, reference todo trace, error mapping ----
+  const long long unconv = hist[max_it + 1];
+  int last = 0;
+  for (int r = 1; r <= max_it; ++r)
+    if (hist[r]) last = r;
+  if (st) {
+    st->iterations = unconv ? max_it : last;
+    st->n_todo = std::min(st->iterations, SPH_MAX_TODO);
+    long long acc = unconv;
+    std::vector<long long> todo(last + 1, 0);
+    for (int r = max_it; r >= 1; --r) {
+      acc += hist[r];
+      if (r <= last || unconv) {
+        if (r - 1 < SPH_MAX_TODO) st->todo_sizes[r - 1] = acc;
+      }
+    }
+    st->pair_tests = (int64_t)stat_all[0];
+    st->accepted_pairs = (int64_t)stat_all[1];
+    st->search_pair_tests = (int64_t)stat_h[0];
+    st->unconverged = unconv;
+    st->bad_index = stat_all[2] == ~0ull ? -1 : (int64_t)stat_all[2];
+    st->gpu_launches = launches;
+    st->search_rounds = hist_rounds;
+    st->select_rounds = band_rounds;
+    st->n_nodes = n_nodes;
+  }
+  const bool degenerate = stat_all[2] != ~0ull;
+  if (degenerate) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "particle %llu: %d-th nearest neighbour is at zero distance; >= %d coincident particles",
+             (unsigned long long)stat_all[2], k, k + 1);
+    return fail(ctx, SPH_DEGENERATE, buf);
+  }
+  if (unconv) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%lld of %d particles still flagged after %d iterations", unconv, n, max_it);
+    return fail(ctx, SPH_NOT_CONVERGED, buf);
+  }
+  return SPH_OK;
+}
+
+int validate(sph_ctx *ctx, const sph_params *p) {
+  if (!ctx) return SPH_INVALID;
+  if (!p) return fail(ctx, SPH_INVALID, "params is NULL");
+  if (p->n < 1) return fail(ctx, SPH_INVALID, "workload must contain at least one particle");
+  if (p->n >= (1ll << 31) - 64) return fail(ctx, SPH_INVALID, "n must be < 2^31 per device");
+  if (p->k < 1) return fail(ctx, SPH_INVALID, "k_neighbors must be >= 1");
+  if (p->max_iterations < 0) return fail(ctx, SPH_INVALID, "max_iterations must be >= 0");
+  if (p->precision < 0 || p->precision > 2) return fail(ctx, SPH_INVALID, "unknown precision");
+  if (p->kernel < 0 || p->kernel > 1) return fail(ctx, SPH_INVALID, "unknown kernel");
+  return SPH_OK;
+}
+
+size_t elem_size(int precision) { return precision == SPH_PRECISION_F32 ? 4 : 8; }
+
+cudaError_t h2d_strided(void *dst, const void *src, size_t elem, int64_t stride, int64_t n, cudaStream_t s) {
+  if (stride == (int64_t)elem) return cudaMemcpyAsync(dst, src, elem * n, cudaMemcpyHostToDevice, s);
+  return cudaMemcpy2DAsync(dst, elem, src, (size_t)stride, elem, (size_t)n, cudaMemcpyHostToDevice, s);
+}
+cudaError_t d2h_strided(void *dst, const void *src, size_t elem, int64_t stride, int64_t n, cudaStream_t s) {
+  if (stride == (int64_t)elem) return cudaMemcpyAsync(dst, src, elem * n, cudaMemcpyDeviceToHost, s);
+  return cudaMemcpy2DAsync(dst, (size_t)stride, src, elem, elem, (size_t)n, cudaMemcpyDeviceToHost, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sph_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int sph_ctx_create(sph_ctx **out, int device) {
+  if (!out) return SPH_INVALID;
+  *out = nullptr;
+  int count = sph_device_count();
+  if (count <= 0) return SPH_CUDA_ERROR;
+  if (device < 0 || device >= count) return SPH_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return SPH_CUDA_ERROR;
+  sph_ctx *c = new sph_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return SPH_CUDA_ERROR;
+  }
+  for (auto &e : c->ev) cudaEventCreate(&e);
+  *out = c;
+  return SPH_OK;
+}
+
+void sph_ctx_destroy(sph_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->in_x.release(); c->in_y.release(); c->in_z.release(); c->in_m.release(); c->io_h.release();
+  c->out_rho.release(); c->out_flags.release(); c->keys_in.release(); c->keys.release(); c->bbox_ord.release();
+  c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
+  c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
+  c->noff.release(); c->nlo.release(); c->nhi.release(); c->r0.release(); c->pos_sorted.release();
+  c->cub_temp.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->rho_s.release(); c->hfix.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
+  for (auto &e : c->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char *sph_last_error(const sph_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+uint64_t sph_fnv1a64(const uint8_t *data, size_t len) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < len; ++i) h = (h ^ data[i]) * 0x100000001B3ull;
+  return h;
+}
+
+int sph_density_pass_device(sph_ctx *ctx, const sph_params *prm, const void *d_x, const void *d_y,
+                            const void *d_z, const double *d_mass, double *d_h, double *d_rho, uint8_t *d_flags,
+                            sph_stats *st) {
+  int rc = validate(ctx, prm);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (st) memset(st, 0, sizeof(*st));
+  Timer tm{ctx};
+  tm.mark(0);
+  // the input h drives only the todo trace: keep a copy so d_h can be overwritten
+  if (ctx->hfix.ensure(prm->n) != cudaSuccess) return fail(ctx, SPH_CUDA_ERROR, "out of device memory");
+  SPH_CK(cudaMemcpyAsync(ctx->hfix.p, d_h, sizeof(double) * prm->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  rc = density_pass_dev(ctx, prm, d_x, d_y, d_z, d_mass, ctx->hfix.p, d_h, d_rho, d_flags, st, tm);
+  tm.mark(7);
+  cudaStreamSynchronize(ctx->stream);
+  if (st && (rc == SPH_OK || rc == SPH_DEGENERATE || rc == SPH_NOT_CONVERGED)) {
+    st->t_stage_ms[0] = tm.ms(0, 1);
+    st->t_stage_ms[1] = tm.ms(1, 2);
+    st->t_stage_ms[2] = tm.ms(2, 3);
+    st->t_stage_ms[3] = tm.ms(3, 4);
+    st->t_stage_ms[4] = tm.ms(4, 5);
+    st->t_stage_ms[5] = tm.ms(5, 6);
+    st->t_stage_ms[6] = 0.0;
+    st->t_stage_ms[7] = tm.ms(0, 7);
+  }
+  return rc;
+}
+
+int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const void *y, const void *z,
+                     int64_t pos_stride, const double *mass, int64_t mass_stride, double *h, int64_t h_stride,
+                     double *rho, int64_t rho_stride, uint8_t *flags, int64_t flags_stride, sph_stats *st) {
+  int rc = validate(ctx, prm);
+  if (rc) return rc;
+  if (!x || !y || !z || !mass || !h || !rho || !flags) return fail(ctx, SPH_INVALID, "null array pointer");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (st) memset(st, 0, sizeof(*st));
+  const int64_t n = prm->n;
+  const size_t es = elem_size(prm->precision);
+  SPH_CK(ctx->in_x.ensure(n));
+  SPH_CK(ctx->in_y.ensure(n));
+  SPH_CK(ctx->in_z.ensure(n));
+  SPH_CK(ctx->in_m.ensure(n));
+  SPH_CK(ctx->io_h.ensure(n));
+  SPH_CK(ctx->hfix.ensure(n));
+  SPH_CK(ctx->out_rho.ensure(n));
+  SPH_CK(ctx->out_flags.ensure(n));
+  Timer tm{ctx};
+  tm.mark(0);
+  cudaStream_t s = ctx->stream;
+  SPH_CK(h2d_strided(ctx->in_x.p, x, es, pos_stride, n, s));
+  SPH_CK(h2d_strided(ctx->in_y.p, y, es, pos_stride, n, s));
+  SPH_CK(h2d_strided(ctx->in_z.p, z, es, pos_stride, n, s));
+  SPH_CK(h2d_strided(ctx->in_m.p, mass, 8, mass_stride, n, s));
+  SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, n, s));
+  rc = density_pass_dev(ctx, prm, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, ctx->hfix.p, ctx->io_h.p,
+                        ctx->out_rho.p, ctx->out_flags.p, st, tm);
+  if (rc == SPH_OK) {
+    SPH_CK(d2h_strided(h, ctx->io_h.p, 8, h_stride, n, s));
+    SPH_CK(d2h_strided(rho, ctx->out_rho.p, 8, rho_stride, n, s));
+    SPH_CK(d2h_strided(flags, ctx->out_flags.p, 1, flags_stride, n, s));
+  }
+  tm.mark(7);
+  SPH_CK(cudaStreamSynchronize(s));
+  if (st && (rc == SPH_OK || rc == SPH_DEGENERATE || rc == SPH_NOT_CONVERGED)) {
+    st->t_stage_ms[0] = tm.ms(0, 1);
+    st->t_stage_ms[1] = tm.ms(1, 2);
+    st->t_stage_ms[2] = tm.ms(2, 3);
+    st->t_stage_ms[3] = tm.ms(3, 4);
+    st->t_stage_ms[4] = tm.ms(4, 5);
+    st->t_stage_ms[5] = tm.ms(5, 6);
+    st->t_stage_ms[6] = rc == SPH_OK ? tm.ms(6, 7) : 0.0;
+    st->t_stage_ms[7] = tm.ms(0, 7);
+  }
+  return rc;
+}
+
+int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
+                  int64_t *perm_out) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 1) return fail(ctx, SPH_INVALID, "need at least one particle");
+  if (n >= (1ll << 31) - 64) return fail(ctx, SPH_INVALID, "n must be < 2^31 per device");
+  if (precision != SPH_PRECISION_F32 && precision != SPH_PRECISION_F64)
+    return fail(ctx, SPH_INVALID, "precision must be f32 or f64");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = ensure_common(ctx, n, 1);
+  if (rc) return rc;
+  const size_t es = elem_size(precision);
+  SPH_CK(ctx->in_x.ensure(n));
+  SPH_CK(ctx->in_y.ensure(n));
+  SPH_CK(ctx->in_z.ensure(n));
+  cudaStream_t s = ctx->stream;
+  SPH_CK(cudaMemcpyAsync(ctx->in_x.p, x, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_y.p, y, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_z.p, z, es * n, cudaMemcpyHostToDevice, s));
+  int launches = 0;
+  RootInfo root{};
+  rc = stage_root(ctx, (int)n, precision, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, &root, &launches);
+  if (rc) return rc;
+  int n_nodes = 0;
+  rc = stage_tree(ctx, (int)n, precision, 0, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, nullptr, 1, 1.f, &n_nodes,
+                  &launches, false);
+  if (rc) return rc;
+  std::vector<uint32_t> tmp(n);
+  SPH_CK(cudaMemcpyAsync(tmp.data(), ctx->perm.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) perm_out[i] = (int64_t)tmp[i];
+  return SPH_OK;
+}
+
+int sph_neighbor_counts(sph_ctx *ctx, int32_t precision, int32_t periodic, double box, int64_t n, const void *x,
+                        const void *y, const void *z, const double *h, int32_t *counts_out, sph_stats *st) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 1) return fail(ctx, SPH_INVALID, "need at least one particle");
+  if (n >= (1ll << 31) - 64) return fail(ctx, SPH_INVALID, "n must be < 2^31 per device");
+  if (precision < 0 || precision > 2) return fail(ctx, SPH_INVALID, "unknown precision");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  if (st) memset(st, 0, sizeof(*st));
+  int rc = ensure_common(ctx, n, 1);
+  if (rc) return rc;
+  const size_t es = elem_size(precision);
+  SPH_CK(ctx->in_x.ensure(n));
+  SPH_CK(ctx->in_y.ensure(n));
+  SPH_CK(ctx->in_z.ensure(n));
+  SPH_CK(ctx->in_m.ensure(n));
+  SPH_CK(ctx->io_h.ensure(n));
+  SPH_CK(ctx->hfix.ensure(n));
+  SPH_CK(ctx->counts_s.ensure(n));
+  SPH_CK(ctx->counts_o.ensure(n));
+  cudaStream_t s = ctx->stream;
+  SPH_CK(cudaMemcpyAsync(ctx->in_x.p, x, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_y.p, y, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_z.p, z, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->io_h.p, h, 8 * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemsetAsync(ctx->in_m.p, 0, 8 * n, s));
+  int launches = 0;
+  RootInfo root{};
+  rc = stage_root(ctx, (int)n, precision, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, &root, &launches);
+  if (rc) return rc;
+  if (periodic) {
+    if (!(box > 0.0)) return fail(ctx, SPH_INVALID, "periodic box side must be > 0");
+    for (int a2 = 0; a2 < 3; ++a2)
+      if (root.lo[a2] < 0.0 || root.hi[a2] >= box)
+        return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
+  }
+  const int compute_f32 = precision == SPH_PRECISION_F32 || (precision == 2 && !root.not_f32);
+  const float rmax = compute_rmax(root, periodic, box);
+  int n_nodes = 0;
+  rc = stage_tree(ctx, (int)n, precision, compute_f32, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, 1, rmax,
+                  &n_nodes, &launches, true);
+  if (rc) return rc;
+  k_gather_sorted<double><<<nblk(n), kTB, 0, s>>>((int)n, ctx->perm.p, ctx->io_h.p, ctx->hfix.p);
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 4 * sizeof(unsigned long long), s));
+  sph_params prm{};
+  prm.periodic = periodic;
+  prm.box = box;
+  PassArgs a = base_args(ctx, (int)n, 1, n_nodes, &prm, rmax);
+  launch_pass(s, MODE_COUNT, compute_f32, a, ctx->num_sms);
+  k_scatter_orig<int32_t><<<nblk(n), kTB, 0, s>>>((int)n, ctx->perm.p, ctx->counts_s.p, ctx->counts_o.p);
+  launches += 3;
+  SPH_CK(cudaMemcpyAsync(counts_out, ctx->counts_o.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  unsigned long long stat_all[2] = {0, 0};
+  SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaStreamSynchronize(s));
+  SPH_CK(cudaGetLastError());
+  if (st) {
+    st->pair_tests = (int64_t)stat_all[0];
+    st->gpu_launches = launches;
+    st->n_nodes = n_nodes;
+  }
+  return SPH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// sph_internal.cuh -- shared device helpers and host-side launch interfaces
+// of the B200 SPH density pass.  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sph {
+
+constexpr int kMaxLevel = 21;        // 63-bit Morton keys: 21 octree levels
+constexpr int kLeafCap = 8;          // reference leaf capacity (octree.py:30)
+constexpr int kCellCap = 32;         // search cell capacity (one warp of candidates)
+constexpr double kGrowth = 1.2599210498948732;  // 2.0 ** (1.0 / 3.0), density.py:53
+constexpr double kWc6Norm = 1365.0 / (64.0 * 3.14159265358979323846);  // kernel.py:17
+constexpr double kM4Norm = 8.0 / 3.14159265358979323846;              // M4 (extension)
+
+// status bytes per target (sorted position)
+enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3 };
+
+// root cube of the reference octree (octree.py:324-336) + validation flags
+struct RootInfo {
+  double lo[3], hi[3];
+  double c[3];
+  double half;
+  double pad;
+  double max_abs;
+  int nonfinite;
+  int not_f32;   // some coordinate is not exactly representable in fp32
+};
+
+// ordered-int image of a double for atomicMin/atomicMax
+__device__ __forceinline__ unsigned long long dbl_to_ord(double d) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_to_dbl(unsigned long long o) {
+  unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  return __longlong_as_double((long long)b);
+}
+
+// common prefix length (bits) of two 63-bit keys held in the low 63 bits
+__device__ __forceinline__ int key_cpl(unsigned long long a, unsigned long long b) {
+  return __clzll(a ^ b) - 1;  // 63 when equal
+}
+__host__ __device__ __forceinline__ unsigned long long key_prefix(unsigned long long key, int level) {
+  return level == 0 ? 0ull : (key >> (63 - 3 * level));
+}
+
+// exact reference distance: ddx = x_j - q_x; d2 = (ddx*ddx + ddy*ddy) + ddz*ddz,
+// every operation rounded on its own (octree.py:211-214, no contraction)
+__device__ __forceinline__ double exact_d2(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// Wendland C6 unit profile (kernel.py:30-36), fp64 op-for-op
+__device__ __forceinline__ double wc6_profile(double q) {
+  double u = __dsub_rn(1.0, q);
+  double u2 = __dmul_rn(u, u);
+  double u4 = __dmul_rn(u2, u2);
+  double poly = __dadd_rn(1.0, __dmul_rn(q, __dadd_rn(8.0, __dmul_rn(q, __dadd_rn(25.0, __dmul_rn(32.0, q))))));
+  return __dmul_rn(__dmul_rn(u4, u4), poly);
+}
+// _w_lowered(r, h) (kernel.py:39-45) given the precomputed C/(h*h*h)
+__device__ __forceinline__ double wc6_lowered(double r, double h, double norm_h3) {
+  double q = __ddiv_rn(r, h);
+  return q < 1.0 ? __dmul_rn(norm_h3, wc6_profile(q)) : 0.0;
+}
+__device__ __forceinline__ float wc6_profile_f(float q) {
+  float u = 1.0f - q;
+  float u2 = u * u;
+  float u4 = u2 * u2;
+  return (u4 * u4) * fmaf(q, fmaf(q, fmaf(32.0f, q, 25.0f), 8.0f), 1.0f);
+}
+// M4 cubic spline with compact support h (extension; no reference oracle)
+__device__ __forceinline__ double m4_profile(double q) {
+  if (q < 0.5) return 1.0 - 6.0 * q * q + 6.0 * q * q * q;
+  double t = 1.0 - q;
+  return q < 1.0 ? 2.0 * t * t * t : 0.0;
+}
+__device__ __forceinline__ float m4_profile_f(float q) {
+  if (q < 0.5f) return 1.0f - 6.0f * q * q + 6.0f * q * q * q;
+  float t = 1.0f - q;
+  return q < 1.0f ? 2.0f * t * t * t : 0.0f;
+}
+
+// search-tree node (pre-order, skip pointers).  lo.w = skip (int bits),
+// hi.w = first sorted position (int bits).  A node is a cell iff skip == k+1.
+struct TreeView {
+  const float4 *nlo;
+  const float4 *nhi;
+  int n_nodes;
+};
+
+// per-call device workspace handed to the kernels
+struct PassArgs {
+  int n;
+  int k;
+  int kernel_kind;
+  const uint32_t *list;     // target list (sorted positions); nullptr = identity
+  const int *list_count;    // device-side list length
+  int static_count;         // used when list == nullptr
+  TreeView tree;
+  const void *pos;          // float4 (fp32 path) or double[4] (fp64 path) per sorted position
+  float *radius;            // per target search radius (histogram pass)
+  double *t_lo, *t_hi;      // per target bracket of d2_K (band pass)
+  double *d2k;              // result: K-th neighbour squared distance
+  double *rho;              // result: density (sorted order)
+  const double *hfix;       // fixed-h counting input (sorted order)
+  int32_t *counts;          // fixed-h counting output (sorted order)
+  uint8_t *state;           // per target status
+  int *work_counter;        // persistent-kernel work cursor
+  unsigned long long *stats;  // [0] pair tests, [1] accepted pairs
+  int periodic;
+  double box;
+  float rmax;               // largest meaningful search radius
+};
+
+// ---- launchers (sph_tree.cu) ----
+struct TreeBuffers {
+  // sort / ordering
+  unsigned long long *keys_in, *keys;   // keys (unsorted / sorted)
+  uint32_t *idx_in, *idx;               // original indices (unsorted / key-sorted)
+  uint32_t *perm;                       // final order: sorted position -> original index
+  uint8_t *lvl8, *lvl32;
+  int *deep_count;
+  uint32_t *deep_list;
+  int *err_flag;
+  // search tree
+  int *noff;                            // n+1 node offsets per position
+  int *n_nodes_dev;
+  float4 *nlo, *nhi;
+  float *r0;                            // per sorted position initial radius
+  void *pos_sorted;                     // float4 or double[4] per position
+  void *cub_temp;
+  size_t cub_temp_bytes;
+  RootInfo *root;
+  unsigned long long *bbox_ord;         // 6 ordered-int accumulators
+};
+
+int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
+               const void *x, const void *y, const void *z, const double *mass,
+               int k, int *launches);
+int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
+                      const void *x, const void *y, const void *z, const double *mass, int k, float rmax,
+                      int *launches);
+
+void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const void *y,
+                 const void *z, unsigned long long *ord, RootInfo *root, int *launches);
+
+size_t cub_temp_needed(int n);
+
+// ---- launchers (sph_pass.cu) ----
+enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
+void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int num_sms);
+void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
+                   uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
+size_t select_temp_needed(int n);
+
+}  // namespace sph

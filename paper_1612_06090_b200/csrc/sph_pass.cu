@@ -1,0 +1,522 @@
+// sph_pass.cu -- the neighbour kernels.
+//
+// One warp serves a bundle of 32 targets (consecutive entries of a target
+// list in sorted order, so spatially coherent).  The warp walks the
+// pre-order search tree once per periodic image shift with a stackless
+// skip-pointer walk: 32 nodes are box-tested at a time (one per lane) and
+// the walk itself is a warp-uniform bit scan over the hit mask.  Cells the
+// bundle box (grown by the largest lane radius) touches are merged into
+// contiguous particle ranges; each range is staged 32 candidates at a time
+// in shared memory and every lane tests its own target against each
+// staged candidate (broadcast reads).  What a lane does with a candidate
+// depends on the mode:
+//
+//   MODE_HIST   counts candidates in 32 d^2 bins over [0, R_i^2]: yields the
+//               bracket bin of the K-th neighbour, or a retry with larger R
+//   MODE_BAND   exact K-th d^2: counts exactly (unfused fp64) what lies below
+//               the bracket, keeps the in-bracket values, selects the rank;
+//               overfull brackets are refined with a 16-bin sub-histogram
+//   MODE_DENS   rho_i = sum_j m_j W(r_ij, h_i), h_i = sqrt(d2_K)
+//   MODE_COUNT  fixed-h neighbour counts (parity entry point)
+//
+// fp32 path: candidate tests run in fp32 (positions are exact fp32 values);
+// any candidate whose fp32 d^2 lies within a relative 2^-20 of a threshold is
+// re-tested in unfused fp64 on the widened values, so counts and the K-th
+// d^2 are exactly the reference's fp64 results.
+#include "sph_internal.cuh"
+
+#include <cub/cub.cuh>
+
+namespace sph {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWarps = 4;
+constexpr int NB_HIST = 32;
+constexpr int BAND_CAP = 16;
+constexpr int NB_BAND = 16;
+constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard
+constexpr double kEpsD = 9.5367431640625e-07;
+
+struct alignas(32) D4 { double x, y, z, m; };
+
+template <bool F32> struct Stage;
+template <> struct Stage<true> { using T = float4; };
+template <> struct Stage<false> { using T = D4; };
+
+template <int MODE, bool F32>
+constexpr int mode_smem_per_warp() {
+  return (F32 ? 32 * 16 : 32 * 32) +
+         (MODE == MODE_HIST ? NB_HIST * 32 * 4 : MODE == MODE_BAND ? (BAND_CAP * 32 * 8 + NB_BAND * 32 * 4) : 0);
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// squared gap between two boxes
+__device__ __forceinline__ float box_gap2(float4 lo, float4 hi, float qlx, float qly, float qlz, float qhx,
+                                          float qhy, float qhz) {
+  const float gx = fmaxf(fmaxf(lo.x - qhx, qlx - hi.x), 0.f);
+  const float gy = fmaxf(fmaxf(lo.y - qhy, qly - hi.y), 0.f);
+  const float gz = fmaxf(fmaxf(lo.z - qhz, qlz - hi.z), 0.f);
+  return gx * gx + gy * gy + gz * gz;
+}
+
+template <int MODE, bool F32>
+__global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
+  extern __shared__ __align__(32) unsigned char smem_raw[];
+  using StageT = typename Stage<F32>::T;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char *wbase = smem_raw + wib * mode_smem_per_warp<MODE, F32>();
+  StageT *stage = reinterpret_cast<StageT *>(wbase);
+  unsigned char *mbase = wbase + (F32 ? 32 * 16 : 32 * 32);
+  unsigned *hist = reinterpret_cast<unsigned *>(mbase);                           // HIST
+  double *band = reinterpret_cast<double *>(mbase);                               // BAND
+  unsigned *bh = reinterpret_cast<unsigned *>(mbase + BAND_CAP * 32 * 8);         // BAND
+
+  const StageT *__restrict__ pos = reinterpret_cast<const StageT *>(a.pos);
+  const float4 *__restrict__ nlo = a.tree.nlo;
+  const float4 *__restrict__ nhi = a.tree.nhi;
+  const int n_nodes = a.tree.n_nodes;
+  const int n = a.n;
+  const int K = a.k;
+
+  unsigned long long tests = 0, accepted = 0;
+
+  for (;;) {
+    int b = 0;
+    if (lane == 0) b = atomicAdd(a.work_counter, 1);
+    b = __shfl_sync(FULL, b, 0);
+    const int count = a.list ? *a.list_count : a.static_count;
+    if (b * 32 >= count) break;
+    const int t = b * 32 + lane;
+    bool active = t < count;
+    const int p = a.list ? (int)a.list[active ? t : b * 32] : (active ? t : b * 32);
+    if constexpr (MODE != MODE_COUNT) {
+      const uint8_t st = a.state[p];
+      if constexpr (MODE == MODE_HIST) active = active && st == ST_NEED_HIST;
+      if constexpr (MODE == MODE_BAND) active = active && st == ST_NEED_BAND;
+      if constexpr (MODE == MODE_DENS) active = active && st == ST_DONE;
+    }
+    const unsigned amask = __ballot_sync(FULL, active);
+    if (!amask) continue;
+    const int n_active = __popc(amask);
+
+    // target position (exact) and fp32 copy
+    double tx, ty, tz;
+    float fx, fy, fz;
+    {
+      const int src = __shfl_sync(FULL, p, __ffs(amask) - 1);
+      const int pp = active ? p : src;
+      if constexpr (F32) {
+        const float4 v = reinterpret_cast<const float4 *>(a.pos)[pp];
+        fx = v.x; fy = v.y; fz = v.z;
+        tx = v.x; ty = v.y; tz = v.z;
+      } else {
+        const D4 v = reinterpret_cast<const D4 *>(a.pos)[pp];
+        tx = v.x; ty = v.y; tz = v.z;
+        fx = (float)tx; fy = (float)ty; fz = (float)tz;
+      }
+    }
+
+    // ---- per-mode lane state ----
+    float rad = 0.f;
+    // HIST
+    float R = 0.f, R2f = -1.f, inv_w = 0.f;
+    double R2d = -1.0, inv_wd = 0.0;
+    // BAND
+    double lo = 0.0, hi = -1.0, scale = 0.0, emin = INFINITY, emax = -INFINITY;
+    float lo_f = -1.f, hi_f = -2.f;
+    int c_below = 0, n_in = 0;
+    // DENS
+    double d2k = 0.0, hh = 0.0, norm_h3 = 0.0, accd = 0.0;
+    float d2k_f = -1.f, inv_h = 0.f, accf = 0.f;
+    // COUNT
+    double r2 = -1.0;
+    float r2_lo_f = -1.f, r2_hi_f = -2.f;
+    int cnt = 0;
+
+    if constexpr (MODE == MODE_HIST) {
+#pragma unroll
+      for (int bb = 0; bb < NB_HIST; ++bb) hist[bb * 32 + lane] = 0u;
+      if (active) {
+        R = a.radius[p];
+        R2f = R * R;
+        R2d = (double)R2f;
+        inv_w = (float)NB_HIST / R2f;
+        inv_wd = (double)NB_HIST / R2d;
+        rad = R;
+      }
+    } else if constexpr (MODE == MODE_BAND) {
+#pragma unroll
+      for (int bb = 0; bb < NB_BAND; ++bb) bh[bb * 32 + lane] = 0u;
+      if (active) {
+        lo = a.t_lo[p];
+        hi = a.t_hi[p];
+        scale = hi > lo ? (double)NB_BAND / (hi - lo) : 0.0;
+        lo_f = __double2float_rd(lo * (1.0 - kEpsD)) - 1e-37f;
+        hi_f = __double2float_ru(hi * (1.0 + kEpsD)) + 1e-37f;
+        rad = __double2float_ru(sqrt(hi) * (1.0 + kEpsD)) + 1e-30f;
+      }
+    } else if constexpr (MODE == MODE_DENS) {
+      if (active) {
+        d2k = a.d2k[p];
+        hh = __dsqrt_rn(d2k);
+        norm_h3 = __ddiv_rn(a.kernel_kind == 0 ? kWc6Norm : kM4Norm, __dmul_rn(__dmul_rn(hh, hh), hh));
+        d2k_f = __double2float_ru(d2k * (1.0 + kEpsD));
+        inv_h = (float)(1.0 / hh);
+        rad = __double2float_ru(hh * (1.0 + kEpsD)) + 1e-30f;
+      }
+    } else {  // COUNT
+      if (active) {
+        const double hf = a.hfix[p];
+        r2 = __dmul_rn(hf, hf);
+        r2_lo_f = __double2float_rd(r2 * (1.0 - kEpsD)) - 1e-37f;
+        r2_hi_f = __double2float_ru(r2 * (1.0 + kEpsD)) + 1e-37f;
+        rad = __double2float_ru(fabs(hf) * (1.0 + kEpsD)) + 1e-30f;
+        if (!(rad >= 0.f)) rad = 0.f;  // NaN h: counts nothing (d2 <= NaN is false)
+      }
+    }
+
+    // ---- bundle box ----
+    float bx0 = F32 ? fx : __double2float_rd(tx), by0 = F32 ? fy : __double2float_rd(ty),
+          bz0 = F32 ? fz : __double2float_rd(tz);
+    float bx1 = F32 ? fx : __double2float_ru(tx), by1 = F32 ? fy : __double2float_ru(ty),
+          bz1 = F32 ? fz : __double2float_ru(tz);
+    bx0 = warp_min(bx0); by0 = warp_min(by0); bz0 = warp_min(bz0);
+    bx1 = warp_max(bx1); by1 = warp_max(by1); bz1 = warp_max(bz1);
+    const float Rb = warp_max(rad);
+    const float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
+
+    const int n_shift = a.periodic ? 27 : 1;
+    for (int sidx = 0; sidx < n_shift; ++sidx) {
+      const int sx = a.periodic ? sidx / 9 - 1 : 0;
+      const int sy = a.periodic ? (sidx / 3) % 3 - 1 : 0;
+      const int sz = a.periodic ? sidx % 3 - 1 : 0;
+      const bool shifted = (sx | sy | sz) != 0;
+      // candidates j are images x_j + s*box: query the tree around x_i - s*box
+      float qlx = bx0, qly = by0, qlz = bz0, qhx = bx1, qhy = by1, qhz = bz1;
+      if (shifted) {
+        const double bxs = a.box;
+        qlx = __double2float_rd((double)bx0 - sx * bxs); qhx = __double2float_ru((double)bx1 - sx * bxs);
+        qly = __double2float_rd((double)by0 - sy * bxs); qhy = __double2float_ru((double)by1 - sy * bxs);
+        qlz = __double2float_rd((double)bz0 - sz * bxs); qhz = __double2float_ru((double)bz1 - sz * bxs);
+        if (box_gap2(nlo[0], nhi[0], qlx, qly, qlz, qhx, qhy, qhz) > R2b) continue;
+      }
+      // fp32 image arithmetic: x_j - box is exact when it matters (Sterbenz);
+      // for +box shift the target moves instead: x_i - box
+      const float boxf = (float)a.box;
+      const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
+      const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
+      const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
+
+      // range list: lane r holds range r
+      int rs = 0, re = 0;
+      int nr = 0, last_e = -1;
+
+      auto process_ranges = [&]() {
+        for (int r = 0; r < nr; ++r) {
+          const int s0 = __shfl_sync(FULL, rs, r);
+          const int e0 = __shfl_sync(FULL, re, r);
+          for (int c0 = s0; c0 < e0; c0 += 32) {
+            const int nc = min(32, e0 - c0);
+            if (lane < nc) stage[lane] = pos[c0 + lane];
+            __syncwarp();
+            tests += (unsigned long long)nc * n_active;
+#pragma unroll 4
+            for (int j = 0; j < nc; ++j) {
+              const StageT c = stage[j];
+              const int cidx = c0 + j;
+              // approximate (fp32 path) or exact (fp64 path) squared distance
+              float af = 0.f;
+              double ad = 0.0;
+              if constexpr (F32) {
+                float cx = c.x, cy = c.y, cz = c.z;
+                float dx, dy, dz;
+                if (shifted) {
+                  dx = (cx + csx) - tfx; dy = (cy + csy) - tfy; dz = (cz + csz) - tfz;
+                } else {
+                  dx = cx - fx; dy = cy - fy; dz = cz - fz;
+                }
+                af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+              } else {
+                double cx = c.x, cy = c.y, cz = c.z;
+                if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
+                ad = exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
+              }
+              auto exact = [&]() -> double {
+                double cx = (double)c.x, cy = (double)c.y, cz = (double)c.z;
+                if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
+                return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
+              };
+              const bool is_self = (cidx == p) && !shifted;
+
+              if constexpr (MODE == MODE_HIST) {
+                if constexpr (F32) {
+                  if (af <= R2f) {
+                    const int bin = min((int)(af * inv_w), NB_HIST - 1);
+                    hist[bin * 32 + lane] += 1u;
+                  }
+                } else {
+                  if (ad <= R2d) {
+                    const int bin = min((int)(ad * inv_wd), NB_HIST - 1);
+                    hist[bin * 32 + lane] += 1u;
+                  }
+                }
+              } else if constexpr (MODE == MODE_BAND) {
+                if (!is_self) {
+                  double e = -1.0;
+                  if constexpr (F32) {
+                    if (af < lo_f) ++c_below;
+                    else if (af <= hi_f) e = exact();
+                  } else {
+                    e = ad;
+                  }
+                  if (e >= 0.0) {
+                    if (e < lo) ++c_below;
+                    else if (e <= hi) {
+                      if (n_in < BAND_CAP) band[n_in * 32 + lane] = e;
+                      ++n_in;
+                      emin = fmin(emin, e);
+                      emax = fmax(emax, e);
+                      const int bin = min(max((int)((e - lo) * scale), 0), NB_BAND - 1);
+                      bh[bin * 32 + lane] += 1u;
+                    }
+                  }
+                }
+              } else if constexpr (MODE == MODE_DENS) {
+                if constexpr (F32) {
+                  if (af < d2k_f) {
+                    const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
+                    const float q = rr * inv_h;
+                    const float w = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
+                    if (q < 1.f) accf = fmaf(c.w, w, accf);
+                    ++accepted;
+                  }
+                } else {
+                  if (ad < d2k) {
+                    const double r_ = __dsqrt_rn(ad);
+                    double w;
+                    if (a.kernel_kind == 0) {
+                      w = wc6_lowered(r_, hh, norm_h3);
+                    } else {
+                      const double q = __ddiv_rn(r_, hh);
+                      w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+                    }
+                    accd = __dadd_rn(accd, __dmul_rn(c.m, w));
+                    ++accepted;
+                  }
+                }
+              } else {  // COUNT
+                if (!is_self) {
+                  if constexpr (F32) {
+                    if (af <= r2_lo_f) ++cnt;
+                    else if (af <= r2_hi_f) cnt += exact() <= r2;
+                  } else {
+                    cnt += ad <= r2;
+                  }
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+        nr = 0;
+        last_e = -1;
+      };
+
+      // ---- stackless pre-order walk ----
+      int kk = 0;
+      while (kk < n_nodes) {
+        const int w = kk;
+        const int my = w + lane;
+        bool hit = false;
+        int my_skip = n_nodes, my_start = n;
+        if (my < n_nodes) {
+          const float4 l4 = nlo[my];
+          const float4 h4 = nhi[my];
+          my_skip = __float_as_int(l4.w);
+          my_start = __float_as_int(h4.w);
+          hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
+        }
+        const unsigned hitm = __ballot_sync(FULL, hit);
+        int next_start = __shfl_down_sync(FULL, my_start, 1);
+        if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
+        while (kk < w + 32 && kk < n_nodes) {
+          const int bb = kk - w;
+          const int skp = __shfl_sync(FULL, my_skip, bb);
+          if ((hitm >> bb) & 1u) {
+            if (skp == kk + 1) {  // cell
+              const int s0 = __shfl_sync(FULL, my_start, bb);
+              const int e0 = __shfl_sync(FULL, next_start, bb);
+              if (s0 == last_e) {
+                if (lane == nr - 1) re = e0;
+              } else {
+                if (nr == 32) process_ranges();
+                if (lane == nr) { rs = s0; re = e0; }
+                ++nr;
+              }
+              last_e = e0;
+            }
+            ++kk;
+          } else {
+            kk = skp;
+          }
+        }
+      }
+      if (nr) process_ranges();
+    }
+
+    // ---- per-mode finish ----
+    if constexpr (MODE == MODE_HIST) {
+      if (active) {
+        unsigned total = 0;
+#pragma unroll
+        for (int bb = 0; bb < NB_HIST; ++bb) total += hist[bb * 32 + lane];
+        total -= 1u;  // the target itself (d2 = 0, always in bin 0)
+        if ((int)total < K) {
+          if (R >= a.rmax) {
+            a.state[p] = ST_UNREACHABLE;
+            a.d2k[p] = INFINITY;
+          } else {
+            float f = total > 0 ? cbrtf((float)(K + 4) / (float)total) * 1.1f : 2.f;
+            f = fminf(fmaxf(f, 1.26f), 2.f);
+            a.radius[p] = fminf(R * f, a.rmax);
+          }
+        } else {
+          int cum = 0, bb = 0;
+          for (; bb < NB_HIST; ++bb) {
+            const int hcount = (int)hist[bb * 32 + lane] - (bb == 0 ? 1 : 0);
+            if (cum + hcount >= K) break;
+            cum += hcount;
+          }
+          const double w = R2d / NB_HIST;
+          const double tl = bb == 0 ? 0.0 : (double)bb * w * (1.0 - 2.0 * kEpsD);
+          const double th = bb == NB_HIST - 1 ? R2d * (1.0 + 2.0 * kEpsD) : (double)(bb + 1) * w * (1.0 + 2.0 * kEpsD);
+          a.t_lo[p] = tl;
+          a.t_hi[p] = th;
+          a.state[p] = ST_NEED_BAND;
+        }
+      }
+    } else if constexpr (MODE == MODE_BAND) {
+      if (active) {
+        const int r = K - c_below;  // 1-based rank inside the bracket
+        if (r <= 0) {
+          a.t_hi[p] = nextafter(lo, -INFINITY);
+          a.t_lo[p] = 0.0;
+        } else if (r > n_in) {
+          const float Rr = a.radius[p];
+          a.t_lo[p] = nextafter(hi, INFINITY);
+          a.t_hi[p] = (double)Rr * (double)Rr * (1.0 + 4.0 * kEpsD);
+        } else if (n_in <= BAND_CAP) {
+          double v = 0.0;
+          for (int i = 0; i < n_in; ++i) {
+            const double ei = band[i * 32 + lane];
+            int less = 0, eq = 0;
+            for (int j2 = 0; j2 < n_in; ++j2) {
+              const double ej = band[j2 * 32 + lane];
+              less += ej < ei;
+              eq += ej == ei;
+            }
+            if (less < r && r <= less + eq) { v = ei; break; }
+          }
+          a.d2k[p] = v;
+          a.state[p] = ST_DONE;
+        } else if (emin == emax) {
+          a.d2k[p] = emin;
+          a.state[p] = ST_DONE;
+        } else {
+          int cum = 0, bb = 0;
+          for (; bb < NB_BAND; ++bb) {
+            const int hcount = (int)bh[bb * 32 + lane];
+            if (cum + hcount >= r) break;
+            cum += hcount;
+          }
+          bb = min(bb, NB_BAND - 1);
+          const double width = hi - lo;
+          double nl = bb == 0 ? lo : lo + (double)bb / scale - width * 1e-12;
+          double nh = bb == NB_BAND - 1 ? hi : lo + (double)(bb + 1) / scale + width * 1e-12;
+          nl = fmax(nextafter(nl, -INFINITY), fmax(lo, emin));
+          nh = fmin(nextafter(nh, INFINITY), fmin(hi, emax));
+          a.t_lo[p] = nl;
+          a.t_hi[p] = nh;
+        }
+      }
+    } else if constexpr (MODE == MODE_DENS) {
+      if (active) {
+        a.rho[p] = F32 ? __dmul_rn(norm_h3, (double)accf) : accd;
+      }
+    } else {
+      if (active) a.counts[p] = cnt;
+    }
+  }
+  // statistics
+  for (int o = 16; o; o >>= 1) accepted += __shfl_xor_sync(FULL, accepted, o);
+  if (lane == 0) {
+    atomicAdd(&a.stats[0], tests);
+    atomicAdd(&a.stats[1], accepted);
+  }
+}
+
+template <int MODE, bool F32>
+void launch_one(cudaStream_t s, const PassArgs &a, int num_sms) {
+  constexpr int smem = kWarps * mode_smem_per_warp<MODE, F32>();
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(k_pass<MODE, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_pass<MODE, F32>, kWarps * 32, smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  k_pass<MODE, F32><<<num_sms * blocks_per_sm, kWarps * 32, smem, s>>>(a);
+}
+
+struct StateIs {
+  const uint8_t *state;
+  uint8_t want;
+  __device__ __forceinline__ bool operator()(const uint32_t &p) const { return state[p] == want; }
+};
+
+}  // namespace
+
+void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int num_sms) {
+  cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
+  if (f32) {
+    switch (mode) {
+      case MODE_HIST: launch_one<MODE_HIST, true>(s, a, num_sms); break;
+      case MODE_BAND: launch_one<MODE_BAND, true>(s, a, num_sms); break;
+      case MODE_DENS: launch_one<MODE_DENS, true>(s, a, num_sms); break;
+      default: launch_one<MODE_COUNT, true>(s, a, num_sms); break;
+    }
+  } else {
+    switch (mode) {
+      case MODE_HIST: launch_one<MODE_HIST, false>(s, a, num_sms); break;
+      case MODE_BAND: launch_one<MODE_BAND, false>(s, a, num_sms); break;
+      case MODE_DENS: launch_one<MODE_DENS, false>(s, a, num_sms); break;
+      default: launch_one<MODE_COUNT, false>(s, a, num_sms); break;
+    }
+  }
+}
+
+size_t select_temp_needed(int n) {
+  size_t b = 0;
+  StateIs op{nullptr, 0};
+  cub::DeviceSelect::If(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int *)nullptr, n, op);
+  return b;
+}
+
+// list_out = [p in list_in : state[p] == want], order preserved
+void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
+                   uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes) {
+  StateIs op{state, want};
+  cub::DeviceSelect::If(temp, temp_bytes, list_in, list_out, count_out, n_in, op, s);
+}
+
+}  // namespace sph

@@ -1,0 +1,439 @@
+// sph_tree.cu -- particle ordering and search tree.
+//
+//  1. root cube + pad exactly as the reference (octree.py:324-336)
+//  2. 63-bit x-major Morton keys descended with the reference's own fp64
+//     centre arithmetic (octree.py:93-104, 143-149), so every octant
+//     decision equals the reference's
+//  3. LSD radix sort of (key, original index) -- stable, so ties keep
+//     original-index order like the reference's stable counting sorts
+//  4. leaf detection for leaf capacity 8 (and the coincident-point guard,
+//     octree.py:75-86) and re-ordering inside each leaf by original index:
+//     the result is Octree.particle_perm bit-for-bit
+//  5. the search tree: cells = maximal octree nodes with <= 32 particles,
+//     internal nodes above them, laid out in pre-order with skip pointers
+//     (a stackless walk); cell boxes are tight, internal boxes are the
+//     padded octree cubes
+#include "sph_internal.cuh"
+
+#include <cub/cub.cuh>
+
+namespace sph {
+
+namespace {
+
+constexpr int kTB = 256;
+
+__device__ __forceinline__ bool is_f32_exact(double v) { return (double)(float)v == v; }
+
+template <typename PosT>
+__global__ void k_bbox(int n, const PosT *__restrict__ x, const PosT *__restrict__ y,
+                       const PosT *__restrict__ z, unsigned long long *ord, RootInfo *root) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int bad = 0, notf = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v[3] = {(double)x[i], (double)y[i], (double)z[i]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (!isfinite(v[a])) { bad = 1; continue; }
+      notf |= !is_f32_exact(v[a]);
+      mn[a] = fmin(mn[a], v[a]);
+      mx[a] = fmax(mx[a], v[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o; o >>= 1) {
+      mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  notf = __any_sync(0xffffffffu, notf);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&ord[a], dbl_to_ord(mn[a]));
+      atomicMax(&ord[3 + a], dbl_to_ord(mx[a]));
+    }
+    if (bad) atomicOr(&root->nonfinite, 1);
+    if (notf) atomicOr(&root->not_f32, 1);
+  }
+}
+
+// octree.py:324-336: lo/hi, centre = 0.5*(lo+hi), half = 0.5*max(hi-lo),
+// pad = 8*eps*(max_abs + half)
+__global__ void k_root(int n, const unsigned long long *ord, RootInfo *root) {
+  if (threadIdx.x || blockIdx.x) return;
+  double ext = 0.0, max_abs = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double lo = n ? ord_to_dbl(ord[a]) : 0.0, hi = n ? ord_to_dbl(ord[3 + a]) : 0.0;
+    root->lo[a] = lo;
+    root->hi[a] = hi;
+    root->c[a] = __dmul_rn(0.5, __dadd_rn(lo, hi));
+    double e = __dsub_rn(hi, lo);
+    ext = (a == 0 || e > ext) ? e : ext;
+    max_abs = fmax(max_abs, fmax(fabs(lo), fabs(hi)));
+  }
+  root->half = __dmul_rn(ext, 0.5);
+  root->max_abs = max_abs;
+  root->pad = __dmul_rn(__dmul_rn(8.0, 2.220446049250313e-16), __dadd_rn(max_abs, root->half));
+}
+
+template <typename PosT>
+__global__ void k_keys(int n, const PosT *__restrict__ x, const PosT *__restrict__ y,
+                       const PosT *__restrict__ z, const RootInfo *__restrict__ root,
+                       unsigned long long *__restrict__ keys, uint32_t *__restrict__ idx) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double px = (double)x[i], py = (double)y[i], pz = (double)z[i];
+  double cx = root->c[0], cy = root->c[1], cz = root->c[2], half = root->half;
+  unsigned long long key = 0;
+#pragma unroll
+  for (int l = 0; l < kMaxLevel; ++l) {
+    const int bx = px >= cx, by = py >= cy, bz = pz >= cz;
+    key = (key << 3) | (unsigned long long)((bx << 2) | (by << 1) | bz);
+    const double h2 = __dmul_rn(half, 0.5);
+    cx = bx ? __dadd_rn(cx, h2) : __dsub_rn(cx, h2);
+    cy = by ? __dadd_rn(cy, h2) : __dsub_rn(cy, h2);
+    cz = bz ? __dadd_rn(cz, h2) : __dsub_rn(cz, h2);
+    half = h2;
+  }
+  keys[i] = key;
+  idx[i] = (uint32_t)i;
+}
+
+// Leaf level for capacity C: the group sharing the 3L-bit prefix has > C
+// members iff some window of C+1 consecutive sorted keys containing p has
+// common prefix >= 3L.  M(p) = max over those windows of cpl(key[s], key[s+C]);
+// level = floor(M/3) + 1 (0 when no full window exists).
+__global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uint8_t *__restrict__ lvl8,
+                         uint8_t *__restrict__ lvl32, int *deep_count, uint32_t *deep_list) {
+  __shared__ unsigned long long sk[kTB + 64];
+  __shared__ int w8[kTB + 32], w32[kTB + 32];
+  const int b0 = blockIdx.x * kTB;
+  for (int t = threadIdx.x; t < kTB + 64; t += kTB) {
+    int q = b0 - 32 + t;
+    sk[t] = (q >= 0 && q < n) ? keys[q] : 0ull;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kTB + 32; t += kTB) {
+    int s = b0 - 32 + t;  // window start
+    w8[t] = (s >= 0 && s + 8 <= n - 1) ? key_cpl(sk[t], sk[t + 8]) : -1;
+    w32[t] = (s >= 0 && s + 32 <= n - 1) ? key_cpl(sk[t], sk[t + 32]) : -1;
+  }
+  __syncthreads();
+  const int p = b0 + threadIdx.x;
+  if (p >= n) return;
+  const int tp = threadIdx.x + 32;  // index of window starting at p
+  int m8 = -1, m32 = -1;
+#pragma unroll
+  for (int d = 0; d <= 8; ++d) m8 = max(m8, w8[tp - d]);
+#pragma unroll 8
+  for (int d = 0; d <= 32; ++d) m32 = max(m32, w32[tp - d]);
+  int l8 = m8 < 0 ? 0 : m8 / 3 + 1;
+  int l32 = m32 < 0 ? 0 : m32 / 3 + 1;
+  if (l8 > kMaxLevel) {
+    l8 = kMaxLevel + 1;  // > 8 identical 63-bit keys: resolved by k_deep
+    int slot = atomicAdd(deep_count, 1);
+    deep_list[slot] = (uint32_t)p;
+  }
+  lvl8[p] = (uint8_t)l8;
+  lvl32[p] = (uint8_t)min(l32, kMaxLevel);
+}
+
+// Runs of > 8 identical 63-bit keys.  If every position in the run is the
+// same point the reference keeps it as one non-separable leaf (octree.py:
+// 75-86) at the first level where no other particle shares its prefix.
+// Otherwise the reference tree is deeper than 21 levels: unsupported.
+template <typename PosT>
+__global__ void k_deep(int n, const unsigned long long *__restrict__ keys, const uint32_t *__restrict__ idx,
+                       const PosT *__restrict__ x, const PosT *__restrict__ y, const PosT *__restrict__ z,
+                       const int *deep_count, const uint32_t *deep_list, uint8_t *lvl8, int *err_flag) {
+  const int cnt = *deep_count;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const int p = (int)deep_list[t];
+    const unsigned long long kp = keys[p];
+    if (p > 0 && keys[p - 1] == kp) continue;  // only the run's first member works
+    int e = p + 1;
+    while (e < n && keys[e] == kp) ++e;
+    const uint32_t j0 = idx[p];
+    bool same = true;
+    for (int q = p + 1; q < e && same; ++q) {
+      const uint32_t j = idx[q];
+      same = x[j] == x[j0] && y[j] == y[j0] && z[j] == z[j0];
+    }
+    if (!same) { atomicOr(err_flag, 1); continue; }
+    const int cl = p > 0 ? key_cpl(keys[p - 1], kp) : -1;
+    const int cr = e < n ? key_cpl(keys[e - 1], keys[e]) : -1;
+    const int m = max(cl, cr);
+    const int L = m < 0 ? 0 : m / 3 + 1;
+    for (int q = p; q < e; ++q) lvl8[q] = (uint8_t)L;
+  }
+}
+
+__device__ __forceinline__ bool same_leaf(const unsigned long long *keys, const uint8_t *lvl, int a, int b) {
+  const int la = lvl[a];
+  return la == lvl[b] && key_prefix(keys[a], la) == key_prefix(keys[b], la);
+}
+
+// inside each leaf the reference keeps original-index order (stable
+// partitions from an identity perm); the key sort ordered them by key
+__global__ void k_leaf_order(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl8,
+                             const uint32_t *__restrict__ idx, uint32_t *__restrict__ perm) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if (p > 0 && same_leaf(keys, lvl8, p - 1, p)) return;
+  uint32_t v[kLeafCap];
+  int c = 0;
+  while (p + c < n && c <= kLeafCap && (c == 0 || same_leaf(keys, lvl8, p, p + c))) {
+    if (c < kLeafCap) v[c] = idx[p + c];
+    ++c;
+  }
+  if (c > kLeafCap || c < 2) return;  // coincident runs are already in index order
+  for (int i = 1; i < c; ++i) {
+    uint32_t t = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > t) { v[j + 1] = v[j]; --j; }
+    v[j + 1] = t;
+  }
+  for (int i = 0; i < c; ++i) perm[p + i] = v[i];
+}
+
+struct alignas(32) D4 { double x, y, z, m; };
+
+template <typename PosT>
+__global__ void k_gather_f32(int n, const uint32_t *__restrict__ perm, const PosT *__restrict__ x,
+                             const PosT *__restrict__ y, const PosT *__restrict__ z,
+                             const double *__restrict__ mass, float4 *__restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t o = perm[p];
+  out[p] = make_float4((float)x[o], (float)y[o], (float)z[o], (float)mass[o]);
+}
+
+template <typename PosT>
+__global__ void k_gather_f64(int n, const uint32_t *__restrict__ perm, const PosT *__restrict__ x,
+                             const PosT *__restrict__ y, const PosT *__restrict__ z,
+                             const double *__restrict__ mass, D4 *__restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t o = perm[p];
+  out[p] = D4{(double)x[o], (double)y[o], (double)z[o], mass[o]};
+}
+
+__device__ __forceinline__ int first_level(const unsigned long long *keys, int p) {
+  if (p == 0) return 0;
+  const int c = key_cpl(keys[p - 1], keys[p]);
+  return c >= 63 ? kMaxLevel + 1 : c / 3 + 1;
+}
+
+__global__ void k_node_count(int n, const unsigned long long *__restrict__ keys,
+                             const uint8_t *__restrict__ lvl32, int *__restrict__ nemit) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > n) return;
+  if (p == n) { nemit[p] = 0; return; }
+  nemit[p] = max(0, (int)lvl32[p] - first_level(keys, p) + 1);
+}
+
+// first q in [lo, n) whose key exceeds kmax (keys sorted)
+__device__ __forceinline__ int upper_bound_key(const unsigned long long *keys, int lo, int n,
+                                               unsigned long long kmax) {
+  int hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (keys[mid] <= kmax) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+// first q in [0, hi) whose key is >= kmin
+__device__ __forceinline__ int lower_bound_key(const unsigned long long *keys, int hi,
+                                               unsigned long long kmin) {
+  int lo = 0;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (keys[mid] < kmin) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ unsigned long long low_mask(int level) {
+  return level == 0 ? 0x7fffffffffffffffull : ((1ull << (63 - 3 * level)) - 1ull);
+}
+
+__device__ __forceinline__ float f_rd(double v) { return __double2float_rd(v); }
+__device__ __forceinline__ float f_ru(double v) { return __double2float_ru(v); }
+
+template <bool F32>
+__global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl32,
+                            const int *__restrict__ noff, const RootInfo *__restrict__ root,
+                            const void *__restrict__ pos_sorted, int k, float rmax,
+                            float4 *__restrict__ nlo, float4 *__restrict__ nhi, float *__restrict__ r0) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int L0 = first_level(keys, p);
+  const int Lc = lvl32[p];
+  if (Lc < L0) return;
+  const unsigned long long kp = keys[p];
+  const double pad2 = 2.0 * root->pad;
+  // descend centres to L0 with the reference arithmetic
+  double c[3] = {root->c[0], root->c[1], root->c[2]};
+  double half = root->half;
+  for (int l = 1; l < L0; ++l) {
+    const int o = (int)((kp >> (63 - 3 * l)) & 7ull);
+    const double h2 = __dmul_rn(half, 0.5);
+    c[0] = (o & 4) ? __dadd_rn(c[0], h2) : __dsub_rn(c[0], h2);
+    c[1] = (o & 2) ? __dadd_rn(c[1], h2) : __dsub_rn(c[1], h2);
+    c[2] = (o & 1) ? __dadd_rn(c[2], h2) : __dsub_rn(c[2], h2);
+    half = h2;
+  }
+  int node = noff[p];
+  for (int L = L0; L <= Lc; ++L, ++node) {
+    if (L > 0) {
+      const int o = (int)((kp >> (63 - 3 * L)) & 7ull);
+      const double h2 = __dmul_rn(half, 0.5);
+      c[0] = (o & 4) ? __dadd_rn(c[0], h2) : __dsub_rn(c[0], h2);
+      c[1] = (o & 2) ? __dadd_rn(c[1], h2) : __dsub_rn(c[1], h2);
+      c[2] = (o & 1) ? __dadd_rn(c[2], h2) : __dsub_rn(c[2], h2);
+      half = h2;
+    }
+    const int end = (L == 0) ? n : upper_bound_key(keys, p + 1, n, kp | low_mask(L));
+    const int skip = noff[end];
+    float4 lo, hi;
+    if (L < Lc) {
+      const double e = half + pad2;
+      lo = make_float4(f_rd(c[0] - e), f_rd(c[1] - e), f_rd(c[2] - e), __int_as_float(skip));
+      hi = make_float4(f_ru(c[0] + e), f_ru(c[1] + e), f_ru(c[2] + e), __int_as_float(p));
+    } else {
+      // cell: tight box over its particles
+      float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int q = p; q < end; ++q) {
+        if (F32) {
+          const float4 v = reinterpret_cast<const float4 *>(pos_sorted)[q];
+          mn[0] = fminf(mn[0], v.x); mn[1] = fminf(mn[1], v.y); mn[2] = fminf(mn[2], v.z);
+          mx[0] = fmaxf(mx[0], v.x); mx[1] = fmaxf(mx[1], v.y); mx[2] = fmaxf(mx[2], v.z);
+        } else {
+          const D4 v = reinterpret_cast<const D4 *>(pos_sorted)[q];
+          mn[0] = fminf(mn[0], f_rd(v.x)); mn[1] = fminf(mn[1], f_rd(v.y)); mn[2] = fminf(mn[2], f_rd(v.z));
+          mx[0] = fmaxf(mx[0], f_ru(v.x)); mx[1] = fmaxf(mx[1], f_ru(v.y)); mx[2] = fmaxf(mx[2], f_ru(v.z));
+        }
+      }
+      lo = make_float4(mn[0], mn[1], mn[2], __int_as_float(skip));
+      hi = make_float4(mx[0], mx[1], mx[2], __int_as_float(p));
+      // initial search radius from the density of the smallest ancestor
+      // holding >= 2K particles (fewer retries than the reference's h0)
+      int La = L > 0 ? L - 1 : 0;
+      int cnt = n;
+      double half_a = root->half;
+      for (; La >= 0; --La) {
+        if (La == 0) { cnt = n; half_a = root->half; break; }
+        const unsigned long long kmin = kp & ~low_mask(La);
+        const int s = lower_bound_key(keys, p + 1, kmin);
+        const int e2 = upper_bound_key(keys, p + 1, n, kp | low_mask(La));
+        cnt = e2 - s;
+        if (cnt >= 2 * k) { half_a = ldexp(root->half, -La); break; }
+      }
+      const double side = fmax(2.0 * half_a, 1e-300);
+      double h_est = side * cbrt(3.0 * k / (4.0 * 3.14159265358979323846 * (double)max(cnt, 1)));
+      float R = (float)(1.2 * h_est);
+      if (!(R > 0.f)) R = rmax;
+      R = fminf(R, rmax);
+      for (int q = p; q < end; ++q) r0[q] = R;
+    }
+    nlo[node] = lo;
+    nhi[node] = hi;
+  }
+}
+
+template <typename T>
+__global__ void k_fill(int n, T *a, T v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+inline int nblk(long long n, int t = kTB) { return (int)((n + t - 1) / t); }
+
+}  // namespace
+
+size_t cub_temp_needed(int n) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                  (uint32_t *)nullptr, (uint32_t *)nullptr, n, 0, 63);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, n + 1);
+  return a > b ? a : b;
+}
+
+void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const void *y, const void *z,
+                 unsigned long long *ord, RootInfo *root, int *launches) {
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  cudaMemcpyAsync(ord, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(root, 0, sizeof(RootInfo), s);
+  const int grid = n > 0 ? std::min(nblk(n), 148 * 8) : 1;
+  if (precision_in == 1)
+    k_bbox<float><<<grid, kTB, 0, s>>>(n, (const float *)x, (const float *)y, (const float *)z, ord, root);
+  else
+    k_bbox<double><<<grid, kTB, 0, s>>>(n, (const double *)x, (const double *)y, (const double *)z, ord, root);
+  k_root<<<1, 32, 0, s>>>(n, ord, root);
+  *launches += 2;
+}
+
+// Everything after the bbox: keys, sort, perm, sorted SoA, search tree.
+// Requires tb.root to hold the root info (launch_bbox) and the caller to
+// have validated it.  Returns 0 or SPH_UNSUPPORTED-style error via err_flag.
+int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
+               const void *x, const void *y, const void *z, const double *mass, int k, int *launches) {
+  const bool in32 = precision_in == 1;
+  if (in32)
+    k_keys<float><<<nblk(n), kTB, 0, s>>>(n, (const float *)x, (const float *)y, (const float *)z, tb.root,
+                                          tb.keys_in, tb.idx_in);
+  else
+    k_keys<double><<<nblk(n), kTB, 0, s>>>(n, (const double *)x, (const double *)y, (const double *)z, tb.root,
+                                           tb.keys_in, tb.idx_in);
+  size_t tbytes = tb.cub_temp_bytes;
+  cub::DeviceRadixSort::SortPairs(tb.cub_temp, tbytes, tb.keys_in, tb.keys, tb.idx_in, tb.idx, n, 0, 63, s);
+  cudaMemsetAsync(tb.deep_count, 0, sizeof(int), s);
+  cudaMemsetAsync(tb.err_flag, 0, sizeof(int), s);
+  k_levels<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.lvl32, tb.deep_count, tb.deep_list);
+  if (in32)
+    k_deep<float><<<64, 128, 0, s>>>(n, tb.keys, tb.idx, (const float *)x, (const float *)y, (const float *)z,
+                                     tb.deep_count, tb.deep_list, tb.lvl8, tb.err_flag);
+  else
+    k_deep<double><<<64, 128, 0, s>>>(n, tb.keys, tb.idx, (const double *)x, (const double *)y,
+                                      (const double *)z, tb.deep_count, tb.deep_list, tb.lvl8, tb.err_flag);
+  cudaMemcpyAsync(tb.perm, tb.idx, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+  k_leaf_order<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.idx, tb.perm);
+  *launches += 5;  // keys, levels, deep, leaf order (+ the radix sort's own kernels)
+  return 0;
+}
+
+int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
+                      const void *x, const void *y, const void *z, const double *mass, int k, float rmax,
+                      int *launches) {
+  const bool in32 = precision_in == 1;
+  if (compute_f32) {
+    if (in32)
+      k_gather_f32<float><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const float *)x, (const float *)y,
+                                                  (const float *)z, mass, (float4 *)tb.pos_sorted);
+    else
+      k_gather_f32<double><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const double *)x, (const double *)y,
+                                                   (const double *)z, mass, (float4 *)tb.pos_sorted);
+  } else {
+    if (in32)
+      k_gather_f64<float><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const float *)x, (const float *)y,
+                                                  (const float *)z, mass, (D4 *)tb.pos_sorted);
+    else
+      k_gather_f64<double><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const double *)x, (const double *)y,
+                                                   (const double *)z, mass, (D4 *)tb.pos_sorted);
+  }
+  k_node_count<<<nblk(n + 1), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff);
+  size_t tbytes = tb.cub_temp_bytes;
+  cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
+  if (compute_f32)
+    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax,
+                                              tb.nlo, tb.nhi, tb.r0);
+  else
+    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax,
+                                               tb.nlo, tb.nhi, tb.r0);
+  *launches += 3;
+  return 0;
+}
+
+}  // namespace sph
