@@ -66,7 +66,7 @@ struct sph_ctx {
   DevBuf<float> r0;
   DevBuf<unsigned char> pos_sorted, cub_temp;
   DevBuf<RootInfo> root;
-  DevBuf<double> t_lo, t_hi, d2k, rho_s, hfix;
+  DevBuf<double> t_lo, t_hi, d2k, rho_s, hfix, mass_s;
   DevBuf<int32_t> counts_s, counts_o;
   DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
   size_t cub_bytes = 0;
@@ -176,6 +176,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->nhi.ensure(2 * n + 64));
   SPH_CK(ctx->r0.ensure(n));
   SPH_CK(ctx->pos_sorted.ensure(32 * n));
+  SPH_CK(ctx->mass_s.ensure(n));
   SPH_CK(ctx->root.ensure(1));
   SPH_CK(ctx->stats.ensure(4));
   size_t need = std::max(cub_temp_needed((int)n), select_temp_needed((int)n));
@@ -201,6 +202,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.nhi = ctx->nhi.p;
   tb.r0 = ctx->r0.p;
   tb.pos_sorted = ctx->pos_sorted.p;
+  tb.mass_sorted = ctx->mass_s.p;
   tb.cub_temp = ctx->cub_temp.p;
   tb.cub_temp_bytes = ctx->cub_bytes;
   tb.root = ctx->root.p;
@@ -260,6 +262,8 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.tree.nhi = ctx->nhi.p;
   a.tree.n_nodes = n_nodes;
   a.pos = ctx->pos_sorted.p;
+  a.mass64 = ctx->mass_s.p;
+  a.dens64 = prm ? (prm->precision != SPH_PRECISION_F32) : 0;
   a.radius = ctx->r0.p;
   a.t_lo = ctx->t_lo.p;
   a.t_hi = ctx->t_hi.p;
@@ -479,7 +483,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->r0.release(); c->pos_sorted.release();
   c->cub_temp.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
-  c->rho_s.release(); c->hfix.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
+  c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
   delete c;

@@ -101,6 +101,8 @@ struct PassArgs {
   int static_count;         // used when list == nullptr
   TreeView tree;
   const void *pos;          // float4 (fp32 path) or double[4] (fp64 path) per sorted position
+  const double *mass64;     // fp64 masses in sorted order (fp32 path with fp64 density sums)
+  int dens64;               // fp32 path: evaluate accepted pairs in fp64 like the reference
   float *radius;            // per target search radius (histogram pass)
   double *t_lo, *t_hi;      // per target bracket of d2_K (band pass)
   double *d2k;              // result: K-th neighbour squared distance
@@ -131,6 +133,7 @@ struct TreeBuffers {
   float4 *nlo, *nhi;
   float *r0;                            // per sorted position initial radius
   void *pos_sorted;                     // float4 or double[4] per position
+  double *mass_sorted;                  // fp64 masses per position
   void *cub_temp;
   size_t cub_temp_bytes;
   RootInfo *root;

@@ -295,10 +295,26 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
               } else if constexpr (MODE == MODE_DENS) {
                 if constexpr (F32) {
                   if (af < d2k_f) {
-                    const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
-                    const float q = rr * inv_h;
-                    const float w = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
-                    if (q < 1.f) accf = fmaf(c.w, w, accf);
+                    if (a.dens64) {
+                      // fp64 evaluation of the accepted pair, term-for-term the reference's
+                      const double e = exact();
+                      if (e < d2k) {
+                        const double r_ = __dsqrt_rn(e);
+                        double w;
+                        if (a.kernel_kind == 0) {
+                          w = wc6_lowered(r_, hh, norm_h3);
+                        } else {
+                          const double q = __ddiv_rn(r_, hh);
+                          w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+                        }
+                        accd = __dadd_rn(accd, __dmul_rn(a.mass64[cidx], w));
+                      }
+                    } else {
+                      const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
+                      const float q = rr * inv_h;
+                      const float w = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
+                      if (q < 1.f) accf = fmaf(c.w, w, accf);
+                    }
                     ++accepted;
                   }
                 } else {
@@ -452,7 +468,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       }
     } else if constexpr (MODE == MODE_DENS) {
       if (active) {
-        a.rho[p] = F32 ? __dmul_rn(norm_h3, (double)accf) : accd;
+        a.rho[p] = (F32 && !a.dens64) ? __dmul_rn(norm_h3, (double)accf) : accd;
       }
     } else {
       if (active) a.counts[p] = cnt;
