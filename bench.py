@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SPH density / smoothing-length pass.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+A step is one full density pass (ordering + search tree + h search + exact
+K-th neighbour + density + write-back) over one synthetic particle set of
+BASELINE.json config C (default 2: 1,048,576 fp32 particles, 80% in 200 NFW
+halos + 20% uniform background, periodic box of side 100, DesNumNgb = 64).
+
+value   : useful particle-pair interactions / s = N*K / t_pass, inputs already
+          resident in HBM, t_pass = CUDA-event time on the library's stream,
+          L2 flushed (256 MiB write) before every step, max over ranks.
+e2e     : the same metric through the public API (density_pass_soa) with
+          pinned host buffers; host->device inputs and device->host results
+          inside the timed region.
+roofline: the dominant kernel (by device time) against the measured FP32-pipe
+          FFMA rate; algorithmic ops = 6 per pair test (+10 per accepted pair
+          in the density kernel), SURVEY 8(d).
+cpu_baseline: the CPU oracle (a C restatement of the reference pass, OpenMP
+          on all host cores) on a bounded random target sample of the same
+          workload, extrapolated: t = t_tree + t_sample * N / S.
+--impl reference times that CPU implementation alone (rank 0 only).
+Multi-GPU (torchrun, N > 1): independent replicas (one config-C box per
+rank, different seeds), no data-path collective: weak scaling.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-pair interactions/sec (device-timed)"
+UNIT = "pairs/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", default="wendland_c6", choices=("wendland_c6", "m4"))
+    return ap.parse_args()
+
+
+def workload_config(cfg: int, seed: int | None):
+    from paper_1612_06090_b200 import workload
+    t0 = time.perf_counter()
+    w = workload.config(cfg, seed)
+    w["gen_s"] = time.perf_counter() - t0
+    return w
+
+
+def config_json(w, cfg, n_gpus, kernel):
+    desc = {
+        1: "C1: 32,768 uniform particles, fp64, K=64, m=1/N, h0=2*N^(-1/3)",
+        2: "C2: 1,048,576 particles, fp32, 80% in 200 NFW halos (c=10, dN/dM~M^-1.9 on [100,5e4]) + 20% uniform, "
+           "periodic box 100, K=64",
+        3: "C3: 16,777,216 particles, fp32, NFW halos (20,000) + background, periodic box 252, K=64",
+        4: "C4: 134,217,728 particles, fp32, NFW halos (150,000) + background, periodic box 400, K=64",
+        5: "C5: 8,388,608 particles, fp32, single NFW halo c=20 r_vir=1 + 5% background, periodic box 4, K=128",
+    }[cfg]
+    return {"workload": desc, "config_index": cfg, "n_particles": int(w["pos"].shape[0]), "k_neighbors": int(w["k"]),
+            "box": float(w["box"]), "periodic": bool(w["periodic"]), "positions": "f32" if w["fp32"] else "f64",
+            "kernel": kernel, "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "1 GPU",
+            "l2": "flushed before every step (256 MiB device write)",
+            "h0": "reference initial_smoothing_length rule" if cfg != 1 else "2*N^(-1/3)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference algorithm restated in C) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_sampled(w, target_seconds: float, seed: int = 0):
+    import oracle
+    pos = w["pos"]
+    n = pos.shape[0]
+    k = int(w["k"])
+    x, y, z = pos[:, 0], pos[:, 1], pos[:, 2]
+    threads = oracle.nthreads()
+    t0 = time.perf_counter()
+    oracle.perm(x, y, z)  # single-threaded tree build, as in the reference
+    t_tree = time.perf_counter() - t0
+    rng = np.random.default_rng(seed)
+    s = 256
+    t_sample = 0.0
+    while True:
+        tg = np.sort(rng.choice(n, size=min(s, n), replace=False))
+        t0 = time.perf_counter()
+        if w["periodic"]:
+            oracle.density_pass_periodic(x, y, z, w["mass"], w["h0"], k, float(w["box"]), threads=threads, targets=tg)
+        else:
+            oracle.density_pass(x, y, z, w["mass"], w["h0"], k, threads=threads, targets=tg)
+        t_sample = time.perf_counter() - t0 - (t_tree if True else 0.0)
+        t_sample = max(t_sample, 1e-6)
+        if t_sample * 4 > target_seconds or s >= n:
+            break
+        s = min(n, int(s * max(2.0, min(16.0, 0.5 * target_seconds / t_sample))))
+    t_full = t_tree + t_sample * n / tg.size
+    return {"value": n * k / t_full, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{tg.size} random targets of {n} (full tree build {t_tree:.2f}s, sample {t_sample:.2f}s), "
+                      f"extrapolated to all targets: t = t_tree + t_sample*N/S = {t_full:.1f}s",
+            "converged_particles_per_s": n / t_full, "cpu_count": os.cpu_count()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = workload_config(args.config, args.seed)
+    n, k = w["pos"].shape[0], int(w["k"])
+    vals = []
+    base = None
+    for step in range(args.warmup + args.steps):
+        base = cpu_sampled(w, target_seconds=args.cpu_seconds / 2, seed=step)
+        if step >= args.warmup:
+            vals.append(base["value"])
+    value = statistics.median(vals)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": n * k / value * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(w, args.config, args.gpus, "wendland_c6"), "impl": "reference",
+            "cpu_baseline": dict(base, value=value),
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "converged_particles_per_s": n / (n * k / value)}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes
+
+    import torch
+
+    from paper_1612_06090_b200 import _lib
+    from paper_1612_06090_b200.density import density_pass_soa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    torch.cuda.set_device(device)
+    seed = (args.seed if args.seed is not None else args.config) + 1000 * rank
+    w = workload_config(args.config, seed)
+    n, k = w["pos"].shape[0], int(w["k"])
+    pos = w["pos"]
+    f32 = bool(w["fp32"])
+    pdt = torch.float32 if f32 else torch.float64
+    dx = torch.from_numpy(np.ascontiguousarray(pos[:, 0])).to(device=device, dtype=pdt)
+    dy = torch.from_numpy(np.ascontiguousarray(pos[:, 1])).to(device=device, dtype=pdt)
+    dz = torch.from_numpy(np.ascontiguousarray(pos[:, 2])).to(device=device, dtype=pdt)
+    dm = torch.from_numpy(w["mass"]).to(device)
+    dh0 = torch.from_numpy(w["h0"]).to(device)
+    dh = dh0.clone()
+    drho = torch.empty(n, dtype=torch.float64, device=device)
+    dfl = torch.empty(n, dtype=torch.uint8, device=device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+
+    L = _lib.load()
+    ctx = _lib.context(device)
+    stream = torch.cuda.ExternalStream(_lib.stream_handle(ctx), device=device)
+    prm = _lib.SphParams(n=n, k=k, max_iterations=100, precision=_lib.PRECISION["f32" if f32 else "f64"],
+                         periodic=1 if w["periodic"] else 0, box=float(w["box"]), kernel=_lib.KERNELS[args.kernel],
+                         reserved=0)
+    vp = ctypes.c_void_p
+
+    def one_pass(st):
+        rc = L.sph_density_pass_device(ctx, prm, vp(dx.data_ptr()), vp(dy.data_ptr()), vp(dz.data_ptr()),
+                                       vp(dm.data_ptr()), vp(dh.data_ptr()), vp(drho.data_ptr()),
+                                       vp(dfl.data_ptr()), st)
+        if rc != _lib.SPH_OK:
+            raise RuntimeError(f"density pass failed ({rc}): {_lib.last_error(ctx)}")
+
+    st = _lib.SphStats()
+    for i in range(args.warmup):
+        with torch.cuda.stream(stream):
+            dh.copy_(dh0)
+            flush.fill_(i & 255)
+        one_pass(st)
+    torch.cuda.synchronize(device)
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize(device)
+
+    clocks = ClockSampler(device)
+    clocks.start()
+    step_ms, kern = [], {"search": 0.0, "select": 0.0, "density": 0.0, "tree": 0.0}
+    tests = accepted = search_tests = launches = 0
+    stage_tot = {}
+    last = None
+    for i in range(args.steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            dh.copy_(dh0)
+            flush.fill_((i + 7) & 255)
+            ev0.record(stream)
+        st = _lib.SphStats()
+        one_pass(st)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        d = st.as_dict()
+        for kk in kern:
+            kern[kk] += d["t_kernel_ms"][kk]
+        for kk, v in d["t_stage_ms"].items():
+            stage_tot[kk] = stage_tot.get(kk, 0.0) + v
+        tests += d["pair_tests"]
+        accepted += d["accepted_pairs"]
+        search_tests += d["search_pair_tests"]
+        launches += d["gpu_launches"]
+        last = d
+    torch.cuda.synchronize(device)
+    clk = clocks.stop()
+    ms_per_step = sum(step_ms) / len(step_ms)
+    t_local = torch.tensor([ms_per_step], dtype=torch.float64, device=device)
+    n_total = torch.tensor([float(n)], dtype=torch.float64, device=device)
+    if dist:
+        tdist.all_reduce(t_local, op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(n_total, op=tdist.ReduceOp.SUM)
+        tdist.barrier()
+    ms_max = float(t_local.item())
+    total_particles = float(n_total.item())
+    value = total_particles * k / (ms_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (per launch averages over the timed steps) ----
+    peak_ffma = float(L.sph_fp32_peak(ctx))
+    search_ops = 6.0 * search_tests
+    other_tests = tests - search_tests
+    dom = max(("search", "select", "density"), key=lambda s_: kern[s_])
+    if dom == "search":
+        ops, t_k = search_ops, kern["search"]
+    elif dom == "density":
+        dens_tests = max(other_tests - 0, 0)
+        ops, t_k = 6.0 * dens_tests + 10.0 * accepted, kern["density"]
+    else:
+        ops, t_k = 6.0 * other_tests, kern["select"]
+    achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
+    peak = peak_ffma / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{dom}_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
+            "config": config_json(w, args.config, world, args.kernel),
+            "converged_particles_per_s": total_particles / (ms_max * 1e-3),
+            "gpu_launches": launches // args.steps,
+            "clocks": clk,
+            "roofline": {"bound": "fp32", "kernel": f"k_pass<{dom}>", "achieved": achieved, "peak": peak,
+                         "unit": "Tops/s (fp32-pipe ops)", "frac": achieved / peak if peak else None,
+                         "traffic": traffic,
+                         "peak_source": "measured FFMA issue rate on this B200 (sph_fp32_peak); MEASURED_PEAKS.json "
+                                        "has no FP32 vector figure",
+                         "ops_model": "6 per pair test, +10 per accepted pair (density)"},
+            "search_efficiency": n * k / (search_tests / args.steps) if search_tests else None,
+            "pair_tests_per_step": tests / args.steps,
+            "kernel_ms_per_step": {kk: v / args.steps for kk, v in kern.items()},
+            "stage_ms_per_step": {kk: v / args.steps for kk, v in stage_tot.items()},
+            "todo_sizes": last["todo_sizes"] if last else None,
+            "search_rounds": last["search_rounds"] if last else None,
+            "select_rounds": last["select_rounds"] if last else None}
+
+    # ---- end to end through the public API with pinned host buffers ----
+    if not args.no_e2e:
+        def pinned(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return t, t.numpy()
+        hx = pinned(pos[:, 0].astype(np.float32 if f32 else np.float64))
+        hy = pinned(pos[:, 1].astype(np.float32 if f32 else np.float64))
+        hz = pinned(pos[:, 2].astype(np.float32 if f32 else np.float64))
+        hm = pinned(w["mass"])
+        hh = pinned(w["h0"].copy())
+        hrho = pinned(np.zeros(n))
+        hfl = pinned(np.zeros(n, dtype=np.uint8))
+        e2e_ms = []
+        for i in range(args.warmup + args.steps):
+            hh[1][:] = w["h0"]
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            density_pass_soa(hx[1], hy[1], hz[1], hm[1], None, k, periodic=bool(w["periodic"]),
+                             box=float(w["box"]), kernel=args.kernel, device=device, out=(hh[1], hrho[1], hfl[1]))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_ms.append(dt * 1e3)
+        e2e_local = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=device)
+        if dist:
+            tdist.all_reduce(e2e_local, op=tdist.ReduceOp.MAX)
+        e_ms = float(e2e_local.item())
+        es = 4 if f32 else 8
+        line["e2e"] = {"value": total_particles * k / (e_ms * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(n * (3 * es + 8 + 8)), "d2h_bytes_per_step": int(n * (8 + 8 + 1)),
+                       "ms_per_step": e_ms, "api": "paper_1612_06090_b200.density_pass_soa (C ABI sph_density_pass), "
+                                                   "pinned host buffers"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_sampled(w, args.cpu_seconds)
+        except Exception as exc:  # the baseline is reported, never gating
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -43,6 +43,8 @@ extern "C" {
 #define SPH_PRECISION_F64 0 /* positions are float64 */
 #define SPH_PRECISION_F32 1 /* positions are float32 (the fp32 configs); results stay bit-exact
                                against the fp64 reference on the widened values */
+#define SPH_PRECISION_AUTO 2 /* positions are float64; the fp32 search kernels are used when every
+                                coordinate is exactly fp32-representable (densities still summed in fp64) */
 
 #define SPH_MAX_TODO 128
 
@@ -82,6 +84,9 @@ int sph_ctx_create(sph_ctx **out, int device);
 void sph_ctx_destroy(sph_ctx *ctx);
 const char *sph_last_error(const sph_ctx *ctx);
 int sph_device_count(void);
+/* the context's CUDA stream (a cudaStream_t as an opaque pointer), so a
+ * caller can time the pass with its own events on the launching stream */
+void *sph_ctx_stream(sph_ctx *ctx);
 
 /*
  * Full pass on HOST buffers.  Each array is addressed as base + i * stride
@@ -119,6 +124,10 @@ int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, con
 int sph_neighbor_counts(sph_ctx *ctx, int32_t precision, int32_t periodic, double box,
                         int64_t n, const void *x, const void *y, const void *z,
                         const double *h, int32_t *counts_out, sph_stats *stats);
+
+/* measured FP32-pipe FFMA issue rate of the context's device (FFMA/s): the
+ * roofline denominator of the neighbour kernels */
+double sph_fp32_peak(sph_ctx *ctx);
 
 /* FNV-1a-64 over a byte buffer (host; the reference checksum64) */
 uint64_t sph_fnv1a64(const uint8_t *data, size_t len);

@@ -26,7 +26,7 @@ MAX_TODO = 128
 EXPORTED_SYMBOLS = (
     "sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_device_count",
     "sph_density_pass", "sph_density_pass_device", "sph_sort_perm",
-    "sph_neighbor_counts", "sph_fnv1a64",
+    "sph_neighbor_counts", "sph_fnv1a64", "sph_ctx_stream", "sph_fp32_peak",
 )
 
 
@@ -60,6 +60,8 @@ class SphStats(ctypes.Structure):
             "search_rounds": int(self.search_rounds),
             "select_rounds": int(self.select_rounds),
             "n_nodes": int(self.n_nodes),
+            "t_kernel_ms": {name: float(self.t_kernel_ms[i]) for i, name in enumerate(
+                ("search", "select", "density", "tree"))},
         }
 
 
@@ -92,6 +94,10 @@ def load():
         L.sph_sort_perm.argtypes = [vp, i32, i64, vp, vp, vp, vp]
         L.sph_neighbor_counts.argtypes = [vp, i32, i32, ctypes.c_double, i64, vp, vp, vp, vp, vp,
                                           ctypes.POINTER(SphStats)]
+        L.sph_fp32_peak.argtypes = [vp]
+        L.sph_fp32_peak.restype = ctypes.c_double
+        L.sph_ctx_stream.argtypes = [vp]
+        L.sph_ctx_stream.restype = vp
         L.sph_fnv1a64.argtypes = [vp, ctypes.c_size_t]
         L.sph_fnv1a64.restype = ctypes.c_uint64
         _lib = L
@@ -123,6 +129,11 @@ def context(device: int = 0):
             c = h
             _ctx[device] = c
         return c
+
+
+def stream_handle(ctx) -> int:
+    """The context's cudaStream_t (for torch.cuda.ExternalStream)."""
+    return int(load().sph_ctx_stream(ctx) or 0)
 
 
 def last_error(ctx) -> str:

@@ -48,6 +48,9 @@ struct DevBuf {
 }  // namespace
 
 struct sph_ctx {
+  cudaEvent_t kev[2 * 64];
+  int n_kev = 0;
+  int kev_mode[64];
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
@@ -146,6 +149,23 @@ __global__ void k_scatter_orig(int n, const uint32_t *__restrict__ perm, const T
 }
 
 inline int nblk(long long n, int t = kTB) { return (int)((n + t - 1) / t); }
+
+// FP32-pipe throughput probe: 16 independent register-operand FFMA chains
+// per thread (the roofline denominator for the neighbour kernels)
+__global__ void __launch_bounds__(256) k_ffma_probe(float *out, int iters) {
+  float a = 1.0f + threadIdx.x * 1e-7f, b = 1e-3f * (threadIdx.x & 7);
+  float x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = threadIdx.x * 1e-3f + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += x[j];
+  if (s == 1234.5f) out[0] = s;
+}
 
 struct Timer {
   sph_ctx *c;
@@ -280,6 +300,31 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   return a;
 }
 
+// launch a pass kernel between two events (per-kernel device time)
+void timed_pass(sph_ctx *ctx, int mode, int f32, const PassArgs &a) {
+  const int i = ctx->n_kev;
+  if (i < 64) {
+    ctx->kev_mode[i] = mode;
+    cudaEventRecord(ctx->kev[2 * i], ctx->stream);
+  }
+  launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+  if (i < 64) {
+    cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
+    ctx->n_kev = i + 1;
+  }
+}
+
+// sum of recorded kernel times per mode (call after a stream sync)
+void collect_kernel_times(sph_ctx *ctx, sph_stats *st) {
+  for (int i = 0; i < ctx->n_kev; ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ctx->kev[2 * i], ctx->kev[2 * i + 1]);
+    const int m = ctx->kev_mode[i];
+    if (st && m >= 0 && m < 3) st->t_kernel_ms[m] += t;
+  }
+  ctx->n_kev = 0;
+}
+
 // rounds of pass `mode` over targets whose state == want, compacting between
 // rounds; returns the number of rounds run
 int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int max_rounds, int *launches,
@@ -287,7 +332,7 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
   const int n = a.n;
   a.list = nullptr;
   a.static_count = n;
-  launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+  timed_pass(ctx, mode, f32, a);
   ++*launches;
   int rounds = 1;
   for (;;) {
@@ -304,7 +349,7 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
       return fail(ctx, SPH_CUDA_ERROR, "neighbour search did not settle (internal round limit)");
     }
     a.list = ctx->list.p;
-    launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+    timed_pass(ctx, mode, f32, a);
     ++*launches;
     ++rounds;
   }
@@ -319,6 +364,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const int k = prm->k;
   const int max_it = prm->max_iterations;
   int launches = 0;
+  ctx->n_kev = 0;
   { int rc0 = ensure_common(ctx, n, max_it); if (rc0) return rc0; }
   SPH_CK(ctx->t_lo.ensure(n));
   SPH_CK(ctx->t_hi.ensure(n));
@@ -357,7 +403,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (rc) return rc;
   tm.mark(4);
   // ---- interact ----
-  launch_pass(ctx->stream, MODE_DENS, compute_f32, a, ctx->num_sms);
+  timed_pass(ctx, MODE_DENS, compute_f32, a);
   ++launches;
   tm.mark(5);
   // ---- finalize ----
@@ -376,6 +422,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
   SPH_CK(cudaStreamSynchronize(ctx->stream));
   SPH_CK(cudaGetLastError());
+  collect_kernel_times(ctx, st);
+  if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
 
   // ---- stats, reference todo trace, error mapping ----
   const long long unconv = hist[max_it + 1];
@@ -469,6 +517,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
     return SPH_CUDA_ERROR;
   }
   for (auto &e : c->ev) cudaEventCreate(&e);
+  for (auto &e : c->kev) cudaEventCreate(&e);
   *out = c;
   return SPH_OK;
 }
@@ -485,9 +534,12 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->cub_temp.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
+  for (auto &e : c->kev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
   delete c;
 }
+
+void *sph_ctx_stream(sph_ctx *c) { return c ? (void *)c->stream : nullptr; }
 
 const char *sph_last_error(const sph_ctx *c) { return c ? c->err.c_str() : "null context"; }
 
@@ -495,6 +547,23 @@ uint64_t sph_fnv1a64(const uint8_t *data, size_t len) {
   uint64_t h = 0xCBF29CE484222325ull;
   for (size_t i = 0; i < len; ++i) h = (h ^ data[i]) * 0x100000001B3ull;
   return h;
+}
+
+double sph_fp32_peak(sph_ctx *ctx) {
+  if (!ctx) return 0.0;
+  cudaSetDevice(ctx->device);
+  float *d = nullptr;
+  if (cudaMalloc(&d, sizeof(float)) != cudaSuccess) return 0.0;
+  const int blocks = ctx->num_sms * 8, threads = 256, iters = 4096;
+  k_ffma_probe<<<blocks, threads, 0, ctx->stream>>>(d, iters);  // warm-up
+  cudaEventRecord(ctx->ev[10], ctx->stream);
+  k_ffma_probe<<<blocks, threads, 0, ctx->stream>>>(d, iters);
+  cudaEventRecord(ctx->ev[11], ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[10], ctx->ev[11]);
+  cudaFree(d);
+  return ms > 0.f ? (double)blocks * threads * iters * 16.0 / (ms * 1e-3) : 0.0;
 }
 
 int sph_density_pass_device(sph_ctx *ctx, const sph_params *prm, const void *d_x, const void *d_y,

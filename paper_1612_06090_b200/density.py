@@ -272,10 +272,12 @@ def ctypes_addr(a: int):
 
 def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MAX_ITERATIONS, *,
                      precision: str | None = None, periodic: bool = False, box: float = 0.0,
-                     kernel: str = "wendland_c6", device: int = 0):
+                     kernel: str = "wendland_c6", device: int = 0, out=None):
     """SoA form of the pass on host arrays: returns (h, rho, flags, PassStats).
 
     ``precision`` defaults to the dtype of x ("f32" for float32 inputs).
+    ``out`` = optional preallocated (h, rho, flags) host arrays (e.g. pinned);
+    h is read as the initial smoothing length when ``h0`` is None.
     """
     x = np.ascontiguousarray(x)
     if precision is None:
@@ -288,9 +290,14 @@ def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MA
     n = x.shape[0]
     if n == 0:
         raise ValueError("workload must contain at least one particle")
-    h = np.array(np.broadcast_to(np.asarray(h0, dtype=np.float64), (n,)))
-    rho = np.zeros(n, dtype=np.float64)
-    flags = np.zeros(n, dtype=np.uint8)
+    if out is not None:
+        h, rho, flags = out
+        if h0 is not None:
+            h[:] = h0
+    else:
+        h = np.array(np.broadcast_to(np.asarray(h0, dtype=np.float64), (n,)))
+        rho = np.zeros(n, dtype=np.float64)
+        flags = np.zeros(n, dtype=np.uint8)
     ctx = _lib.context(device)
     L = _lib.load()
     prm = _lib.SphParams(n=n, k=k, max_iterations=max_iterations, precision=_lib.PRECISION[precision],
