@@ -33,8 +33,12 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWarps = 4;
-constexpr int NB_HIST = 32;
-constexpr int BAND_CAP = 16;
+// geometric histogram: bin = exponent and top two mantissa bits of d2/R_b^2,
+// 4 bins per octave of d2 over [2^-12, 1) plus an underflow bin and x == 1
+constexpr int kHistOctaves = 12;
+constexpr int kHistBase = (127 - kHistOctaves) << 2;
+constexpr int NB_HIST = kHistOctaves * 4 + 2;
+constexpr int BAND_CAP = 32;
 constexpr int NB_BAND = 16;
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard
 constexpr double kEpsD = 9.5367431640625e-07;
@@ -58,6 +62,13 @@ __device__ __forceinline__ float warp_min(float v) {
 __device__ __forceinline__ float warp_max(float v) {
   for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
   return v;
+}
+
+// unfused fp64 d2 of candidate image x_j + s*box from target x_i
+__device__ __forceinline__ double exact_image_d2(double cx, double cy, double cz, bool shifted, double dsx,
+                                                 double dsy, double dsz, double tx, double ty, double tz) {
+  if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
+  return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
 }
 
 // squared gap between two boxes
@@ -108,7 +119,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
     }
     const unsigned amask = __ballot_sync(FULL, active);
     if (!amask) continue;
-    const int n_active = __popc(amask);
 
     // target position (exact) and fp32 copy
     double tx, ty, tz;
@@ -127,11 +137,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       }
     }
 
-    // ---- per-mode lane state ----
+    // ---- per-lane state ----
     float rad = 0.f;
-    // HIST
-    float R = 0.f, R2f = -1.f, inv_w = 0.f;
-    double R2d = -1.0, inv_wd = 0.0;
+    float hR2 = 0.f;  // HIST: histogram range R_b^2 of this lane's sub-bundle
     // BAND
     double lo = 0.0, hi = -1.0, scale = 0.0, emin = INFINITY, emax = -INFINITY;
     float lo_f = -1.f, hi_f = -2.f;
@@ -147,14 +155,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
     if constexpr (MODE == MODE_HIST) {
 #pragma unroll
       for (int bb = 0; bb < NB_HIST; ++bb) hist[bb * 32 + lane] = 0u;
-      if (active) {
-        R = a.radius[p];
-        R2f = R * R;
-        R2d = (double)R2f;
-        inv_w = (float)NB_HIST / R2f;
-        inv_wd = (double)NB_HIST / R2d;
-        rad = R;
-      }
+      if (active) rad = a.radius[p];
     } else if constexpr (MODE == MODE_BAND) {
 #pragma unroll
       for (int bb = 0; bb < NB_BAND; ++bb) bh[bb * 32 + lane] = 0u;
@@ -186,209 +187,237 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       }
     }
 
-    // ---- bundle box ----
-    float bx0 = F32 ? fx : __double2float_rd(tx), by0 = F32 ? fy : __double2float_rd(ty),
-          bz0 = F32 ? fz : __double2float_rd(tz);
-    float bx1 = F32 ? fx : __double2float_ru(tx), by1 = F32 ? fy : __double2float_ru(ty),
-          bz1 = F32 ? fz : __double2float_ru(tz);
-    bx0 = warp_min(bx0); by0 = warp_min(by0); bz0 = warp_min(bz0);
-    bx1 = warp_max(bx1); by1 = warp_max(by1); bz1 = warp_max(bz1);
-    const float Rb = warp_max(rad);
-    const float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
+    // ---- spatially coherent sub-bundles ----
+    // A list chunk can hold targets from distant places (compacted retry
+    // lists in clustered data); each sub-bundle = the pending targets within
+    // 1.5 radii (Chebyshev) of its leader, walked and tested on its own.
+    unsigned pending = amask;
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const float lx = __shfl_sync(FULL, fx, leader), ly = __shfl_sync(FULL, fy, leader),
+                  lz = __shfl_sync(FULL, fz, leader);
+      const float D = 1.5f * __shfl_sync(FULL, rad, leader) + 1e-30f;
+      const bool mem = ((pending >> lane) & 1u) && fabsf(fx - lx) <= D && fabsf(fy - ly) <= D &&
+                       fabsf(fz - lz) <= D;
+      const unsigned mmask = __ballot_sync(FULL, mem) | (1u << leader);
+      const bool member = (mmask >> lane) & 1u;
+      pending &= ~mmask;
+      const int n_mem = __popc(mmask);
 
-    const int n_shift = a.periodic ? 27 : 1;
-    for (int sidx = 0; sidx < n_shift; ++sidx) {
-      const int sx = a.periodic ? sidx / 9 - 1 : 0;
-      const int sy = a.periodic ? (sidx / 3) % 3 - 1 : 0;
-      const int sz = a.periodic ? sidx % 3 - 1 : 0;
-      const bool shifted = (sx | sy | sz) != 0;
-      // candidates j are images x_j + s*box: query the tree around x_i - s*box
-      float qlx = bx0, qly = by0, qlz = bz0, qhx = bx1, qhy = by1, qhz = bz1;
-      if (shifted) {
-        const double bxs = a.box;
-        qlx = __double2float_rd((double)bx0 - sx * bxs); qhx = __double2float_ru((double)bx1 - sx * bxs);
-        qly = __double2float_rd((double)by0 - sy * bxs); qhy = __double2float_ru((double)by1 - sy * bxs);
-        qlz = __double2float_rd((double)bz0 - sz * bxs); qhz = __double2float_ru((double)bz1 - sz * bxs);
-        if (box_gap2(nlo[0], nhi[0], qlx, qly, qlz, qhx, qhy, qhz) > R2b) continue;
+      // sub-bundle box and radius
+      float bx0 = member ? (F32 ? fx : __double2float_rd(tx)) : INFINITY;
+      float by0 = member ? (F32 ? fy : __double2float_rd(ty)) : INFINITY;
+      float bz0 = member ? (F32 ? fz : __double2float_rd(tz)) : INFINITY;
+      float bx1 = member ? (F32 ? fx : __double2float_ru(tx)) : -INFINITY;
+      float by1 = member ? (F32 ? fy : __double2float_ru(ty)) : -INFINITY;
+      float bz1 = member ? (F32 ? fz : __double2float_ru(tz)) : -INFINITY;
+      bx0 = warp_min(bx0); by0 = warp_min(by0); bz0 = warp_min(bz0);
+      bx1 = warp_max(bx1); by1 = warp_max(by1); bz1 = warp_max(bz1);
+      const float Rb = warp_max(member ? rad : 0.f);
+      const float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
+
+      // effective per-lane thresholds for this sub-bundle (non-members: none)
+      float h_r2 = -1.f, h_inv = 0.f;  // HIST
+      if constexpr (MODE == MODE_HIST) {
+        if (member) {
+          hR2 = Rb * Rb;
+          h_r2 = hR2;
+          h_inv = 1.0f / hR2;
+        }
       }
-      // fp32 image arithmetic: x_j - box is exact when it matters (Sterbenz);
-      // for +box shift the target moves instead: x_i - box
-      const float boxf = (float)a.box;
-      const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
-      const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
-      const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
+      const double h_r2d = (double)h_r2, h_invd = (double)h_inv;
+      const float e_lo_f = member ? lo_f : -1.f, e_hi_f = member ? hi_f : -2.f;
+      const float e_d2k_f = member ? d2k_f : -1.f;
+      const double e_d2k = member ? d2k : -1.0;
+      const float e_r2_lo_f = member ? r2_lo_f : -1.f, e_r2_hi_f = member ? r2_hi_f : -2.f;
+      const double e_r2 = member ? r2 : -1.0;
 
-      // range list: lane r holds range r
-      int rs = 0, re = 0;
-      int nr = 0, last_e = -1;
+      const int n_shift = a.periodic ? 27 : 1;
+      for (int sidx = 0; sidx < n_shift; ++sidx) {
+        const int sx = a.periodic ? sidx / 9 - 1 : 0;
+        const int sy = a.periodic ? (sidx / 3) % 3 - 1 : 0;
+        const int sz = a.periodic ? sidx % 3 - 1 : 0;
+        const bool shifted = (sx | sy | sz) != 0;
+        // candidates j are images x_j + s*box: query the tree around x_i - s*box
+        float qlx = bx0, qly = by0, qlz = bz0, qhx = bx1, qhy = by1, qhz = bz1;
+        if (shifted) {
+          const double bxs = a.box;
+          qlx = __double2float_rd((double)bx0 - sx * bxs); qhx = __double2float_ru((double)bx1 - sx * bxs);
+          qly = __double2float_rd((double)by0 - sy * bxs); qhy = __double2float_ru((double)by1 - sy * bxs);
+          qlz = __double2float_rd((double)bz0 - sz * bxs); qhz = __double2float_ru((double)bz1 - sz * bxs);
+          if (box_gap2(nlo[0], nhi[0], qlx, qly, qlz, qhx, qhy, qhz) > R2b) continue;
+        }
+        // fp32 image arithmetic: x_j - box is exact when it matters (Sterbenz);
+        // for a +box shift the target moves instead: x_i - box
+        const float boxf = (float)a.box;
+        const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
+        const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
+        const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
 
-      auto process_ranges = [&]() {
-        for (int r = 0; r < nr; ++r) {
-          const int s0 = __shfl_sync(FULL, rs, r);
-          const int e0 = __shfl_sync(FULL, re, r);
-          for (int c0 = s0; c0 < e0; c0 += 32) {
-            const int nc = min(32, e0 - c0);
-            if (lane < nc) stage[lane] = pos[c0 + lane];
-            __syncwarp();
-            tests += (unsigned long long)nc * n_active;
+        // range list: lane r holds range r
+        int rs = 0, re = 0;
+        int nr = 0, last_e = -1;
+
+        // ---- stackless pre-order walk, interleaved with candidate processing ----
+        int kk = 0;
+        for (;;) {
+          bool full = false;
+          while (kk < n_nodes && !full) {
+            const int w = kk;
+            const int my = w + lane;
+            bool hit = false;
+            int my_skip = n_nodes, my_start = n;
+            if (my < n_nodes) {
+              const float4 l4 = nlo[my];
+              const float4 h4 = nhi[my];
+              my_skip = __float_as_int(l4.w);
+              my_start = __float_as_int(h4.w);
+              hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
+            }
+            const unsigned hitm = __ballot_sync(FULL, hit);
+            int next_start = __shfl_down_sync(FULL, my_start, 1);
+            if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
+            while (kk < w + 32 && kk < n_nodes) {
+              const int bb = kk - w;
+              const int skp = __shfl_sync(FULL, my_skip, bb);
+              if ((hitm >> bb) & 1u) {
+                if (skp == kk + 1) {  // cell
+                  const int s0 = __shfl_sync(FULL, my_start, bb);
+                  const int e0 = __shfl_sync(FULL, next_start, bb);
+                  if (s0 == last_e) {
+                    if (lane == nr - 1) re = e0;
+                  } else {
+                    if (nr == 32) { full = true; break; }  // resume at kk after processing
+                    if (lane == nr) { rs = s0; re = e0; }
+                    ++nr;
+                  }
+                  last_e = e0;
+                }
+                ++kk;
+              } else {
+                kk = skp;
+              }
+            }
+          }
+          for (int r = 0; r < nr; ++r) {
+            const int s0 = __shfl_sync(FULL, rs, r);
+            const int e0 = __shfl_sync(FULL, re, r);
+            for (int c0 = s0; c0 < e0; c0 += 32) {
+              const int nc = min(32, e0 - c0);
+              if (lane < nc) stage[lane] = pos[c0 + lane];
+              __syncwarp();
+              tests += (unsigned long long)nc * n_mem;
 #pragma unroll 4
-            for (int j = 0; j < nc; ++j) {
-              const StageT c = stage[j];
-              const int cidx = c0 + j;
-              // approximate (fp32 path) or exact (fp64 path) squared distance
-              float af = 0.f;
-              double ad = 0.0;
-              if constexpr (F32) {
-                float cx = c.x, cy = c.y, cz = c.z;
-                float dx, dy, dz;
-                if (shifted) {
-                  dx = (cx + csx) - tfx; dy = (cy + csy) - tfy; dz = (cz + csz) - tfz;
-                } else {
-                  dx = cx - fx; dy = cy - fy; dz = cz - fz;
-                }
-                af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-              } else {
-                double cx = c.x, cy = c.y, cz = c.z;
-                if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
-                ad = exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
-              }
-              auto exact = [&]() -> double {
-                double cx = (double)c.x, cy = (double)c.y, cz = (double)c.z;
-                if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
-                return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
-              };
-              const bool is_self = (cidx == p) && !shifted;
-
-              if constexpr (MODE == MODE_HIST) {
+              for (int j = 0; j < nc; ++j) {
+                const StageT c = stage[j];
+                const int cidx = c0 + j;
+                float af = 0.f;
+                double ad = 0.0;
                 if constexpr (F32) {
-                  if (af <= R2f) {
-                    const int bin = min((int)(af * inv_w), NB_HIST - 1);
-                    hist[bin * 32 + lane] += 1u;
-                  }
-                } else {
-                  if (ad <= R2d) {
-                    const int bin = min((int)(ad * inv_wd), NB_HIST - 1);
-                    hist[bin * 32 + lane] += 1u;
-                  }
-                }
-              } else if constexpr (MODE == MODE_BAND) {
-                if (!is_self) {
-                  double e = -1.0;
-                  if constexpr (F32) {
-                    if (af < lo_f) ++c_below;
-                    else if (af <= hi_f) e = exact();
+                  float dx, dy, dz;
+                  if (shifted) {
+                    dx = (c.x + csx) - tfx; dy = (c.y + csy) - tfy; dz = (c.z + csz) - tfz;
                   } else {
-                    e = ad;
+                    dx = c.x - fx; dy = c.y - fy; dz = c.z - fz;
                   }
-                  if (e >= 0.0) {
-                    if (e < lo) ++c_below;
-                    else if (e <= hi) {
-                      if (n_in < BAND_CAP) band[n_in * 32 + lane] = e;
-                      ++n_in;
-                      emin = fmin(emin, e);
-                      emax = fmax(emax, e);
-                      const int bin = min(max((int)((e - lo) * scale), 0), NB_BAND - 1);
-                      bh[bin * 32 + lane] += 1u;
-                    }
-                  }
+                  af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                } else {
+                  double cx = c.x, cy = c.y, cz = c.z;
+                  if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
+                  ad = exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
                 }
-              } else if constexpr (MODE == MODE_DENS) {
-                if constexpr (F32) {
-                  if (af < d2k_f) {
-                    if (a.dens64) {
-                      // fp64 evaluation of the accepted pair, term-for-term the reference's
-                      const double e = exact();
-                      if (e < d2k) {
-                        const double r_ = __dsqrt_rn(e);
-                        double w;
-                        if (a.kernel_kind == 0) {
-                          w = wc6_lowered(r_, hh, norm_h3);
-                        } else {
-                          const double q = __ddiv_rn(r_, hh);
-                          w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
-                        }
-                        accd = __dadd_rn(accd, __dmul_rn(a.mass64[cidx], w));
+#define EXACT_D2() exact_image_d2((double)c.x, (double)c.y, (double)c.z, shifted, dsx, dsy, dsz, tx, ty, tz)
+                const bool is_self = (cidx == p) && !shifted;
+
+                if constexpr (MODE == MODE_HIST) {
+                  // geometric bins: exponent + 2 mantissa bits of d2 / R_b^2
+                  bool in;
+                  float x;
+                  if constexpr (F32) { in = af <= h_r2; x = af * h_inv; }
+                  else { in = ad <= h_r2d; x = (float)(ad * h_invd); }
+                  if (in) {
+                    const int bin = min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
+                    hist[bin * 32 + lane] += 1u;
+                  }
+                } else if constexpr (MODE == MODE_BAND) {
+                  if (!is_self) {
+                    double e = -1.0;
+                    if constexpr (F32) {
+                      if (af < e_lo_f) ++c_below;
+                      else if (af <= e_hi_f) e = EXACT_D2();
+                    } else {
+                      e = member ? ad : -1.0;
+                    }
+                    if (e >= 0.0) {
+                      if (e < lo) ++c_below;
+                      else if (e <= hi) {
+                        if (n_in < BAND_CAP) band[n_in * 32 + lane] = e;
+                        ++n_in;
+                        emin = fmin(emin, e);
+                        emax = fmax(emax, e);
+                        const int bin = min(max((int)((e - lo) * scale), 0), NB_BAND - 1);
+                        bh[bin * 32 + lane] += 1u;
                       }
-                    } else {
-                      const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
-                      const float q = rr * inv_h;
-                      const float w = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
-                      if (q < 1.f) accf = fmaf(c.w, w, accf);
                     }
-                    ++accepted;
                   }
-                } else {
-                  if (ad < d2k) {
-                    const double r_ = __dsqrt_rn(ad);
-                    double w;
-                    if (a.kernel_kind == 0) {
-                      w = wc6_lowered(r_, hh, norm_h3);
-                    } else {
-                      const double q = __ddiv_rn(r_, hh);
-                      w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
-                    }
-                    accd = __dadd_rn(accd, __dmul_rn(c.m, w));
-                    ++accepted;
-                  }
-                }
-              } else {  // COUNT
-                if (!is_self) {
+                } else if constexpr (MODE == MODE_DENS) {
                   if constexpr (F32) {
-                    if (af <= r2_lo_f) ++cnt;
-                    else if (af <= r2_hi_f) cnt += exact() <= r2;
+                    if (af < e_d2k_f) {
+                      if (a.dens64) {
+                        // fp64 evaluation of the accepted pair, term-for-term the reference's
+                        const double e = EXACT_D2();
+                        if (e < d2k) {
+                          const double r_ = __dsqrt_rn(e);
+                          double w;
+                          if (a.kernel_kind == 0) {
+                            w = wc6_lowered(r_, hh, norm_h3);
+                          } else {
+                            const double q = __ddiv_rn(r_, hh);
+                            w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+                          }
+                          accd = __dadd_rn(accd, __dmul_rn(a.mass64[cidx], w));
+                        }
+                      } else {
+                        const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
+                        const float q = rr * inv_h;
+                        const float w = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
+                        if (q < 1.f) accf = fmaf(c.w, w, accf);
+                      }
+                      ++accepted;
+                    }
                   } else {
-                    cnt += ad <= r2;
+                    if (ad < e_d2k) {
+                      const double r_ = __dsqrt_rn(ad);
+                      double w;
+                      if (a.kernel_kind == 0) {
+                        w = wc6_lowered(r_, hh, norm_h3);
+                      } else {
+                        const double q = __ddiv_rn(r_, hh);
+                        w = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+                      }
+                      accd = __dadd_rn(accd, __dmul_rn(c.m, w));
+                      ++accepted;
+                    }
+                  }
+                } else {  // COUNT
+                  if (!is_self) {
+                    if constexpr (F32) {
+                      if (af <= e_r2_lo_f) ++cnt;
+                      else if (af <= e_r2_hi_f) cnt += EXACT_D2() <= r2;
+                    } else {
+                      cnt += ad <= e_r2;
+                    }
                   }
                 }
               }
+              __syncwarp();
             }
-            __syncwarp();
           }
-        }
-        nr = 0;
-        last_e = -1;
-      };
-
-      // ---- stackless pre-order walk ----
-      int kk = 0;
-      while (kk < n_nodes) {
-        const int w = kk;
-        const int my = w + lane;
-        bool hit = false;
-        int my_skip = n_nodes, my_start = n;
-        if (my < n_nodes) {
-          const float4 l4 = nlo[my];
-          const float4 h4 = nhi[my];
-          my_skip = __float_as_int(l4.w);
-          my_start = __float_as_int(h4.w);
-          hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
-        }
-        const unsigned hitm = __ballot_sync(FULL, hit);
-        int next_start = __shfl_down_sync(FULL, my_start, 1);
-        if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
-        while (kk < w + 32 && kk < n_nodes) {
-          const int bb = kk - w;
-          const int skp = __shfl_sync(FULL, my_skip, bb);
-          if ((hitm >> bb) & 1u) {
-            if (skp == kk + 1) {  // cell
-              const int s0 = __shfl_sync(FULL, my_start, bb);
-              const int e0 = __shfl_sync(FULL, next_start, bb);
-              if (s0 == last_e) {
-                if (lane == nr - 1) re = e0;
-              } else {
-                if (nr == 32) process_ranges();
-                if (lane == nr) { rs = s0; re = e0; }
-                ++nr;
-              }
-              last_e = e0;
-            }
-            ++kk;
-          } else {
-            kk = skp;
-          }
+          nr = 0;
+          last_e = -1;
+          if (!full) break;
         }
       }
-      if (nr) process_ranges();
     }
 
     // ---- per-mode finish ----
@@ -397,15 +426,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
         unsigned total = 0;
 #pragma unroll
         for (int bb = 0; bb < NB_HIST; ++bb) total += hist[bb * 32 + lane];
-        total -= 1u;  // the target itself (d2 = 0, always in bin 0)
+        total -= 1u;  // the target itself (d2 = 0, bin 0)
+        const float Rused = sqrtf(hR2);
         if ((int)total < K) {
-          if (R >= a.rmax) {
+          if (Rused >= a.rmax) {
             a.state[p] = ST_UNREACHABLE;
             a.d2k[p] = INFINITY;
           } else {
-            float f = total > 0 ? cbrtf((float)(K + 4) / (float)total) * 1.1f : 2.f;
-            f = fminf(fmaxf(f, 1.26f), 2.f);
-            a.radius[p] = fminf(R * f, a.rmax);
+            float f = total > 0 ? cbrtf((float)(K + 8) / (float)total) * 1.15f : 2.f;
+            f = fminf(fmaxf(f, 1.26f), 2.5f);
+            a.radius[p] = fminf(fmaxf(Rused, rad) * f, a.rmax);
           }
         } else {
           int cum = 0, bb = 0;
@@ -414,11 +444,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
             if (cum + hcount >= K) break;
             cum += hcount;
           }
-          const double w = R2d / NB_HIST;
-          const double tl = bb == 0 ? 0.0 : (double)bb * w * (1.0 - 2.0 * kEpsD);
-          const double th = bb == NB_HIST - 1 ? R2d * (1.0 + 2.0 * kEpsD) : (double)(bb + 1) * w * (1.0 + 2.0 * kEpsD);
+          const double R2d = (double)hR2;
+          double tl, th;
+          if (bb == 0) {
+            tl = 0.0;
+            th = (double)__int_as_float(kHistBase << 21) * R2d * (1.0 + 8.0 * kEpsD);
+          } else if (bb >= NB_HIST - 1) {
+            tl = R2d * (1.0 - 8.0 * kEpsD);
+            th = R2d * (1.0 + 8.0 * kEpsD);
+          } else {
+            tl = (double)__int_as_float((kHistBase + bb - 1) << 21) * R2d * (1.0 - 8.0 * kEpsD);
+            th = (double)__int_as_float((kHistBase + bb) << 21) * R2d * (1.0 + 8.0 * kEpsD);
+          }
           a.t_lo[p] = tl;
           a.t_hi[p] = th;
+          a.radius[p] = Rused;
           a.state[p] = ST_NEED_BAND;
         }
       }
@@ -431,7 +471,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
         } else if (r > n_in) {
           const float Rr = a.radius[p];
           a.t_lo[p] = nextafter(hi, INFINITY);
-          a.t_hi[p] = (double)Rr * (double)Rr * (1.0 + 4.0 * kEpsD);
+          a.t_hi[p] = (double)Rr * (double)Rr * (1.0 + 16.0 * kEpsD);
         } else if (n_in <= BAND_CAP) {
           double v = 0.0;
           for (int i = 0; i < n_in; ++i) {
