@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -63,7 +64,9 @@ struct sph_ctx {
   DevBuf<unsigned long long> keys_in, keys, bbox_ord;
   DevBuf<uint32_t> idx_in, idx, perm, deep_list, iota, list;
   DevBuf<uint8_t> lvl8, lvl32, state;
-  DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4..] rounds hist
+  DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4] task count [5] member cursor [6..] rounds hist
+  DevBuf<int2> tasks;
+  DevBuf<uint32_t> members;
   DevBuf<int> noff;
   DevBuf<float4> nlo, nhi;
   DevBuf<float> r0;
@@ -72,12 +75,17 @@ struct sph_ctx {
   DevBuf<double> t_lo, t_hi, d2k, rho_s, hfix, mass_s;
   DevBuf<int32_t> counts_s, counts_o;
   DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
+  DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
+  bool debug = false;
+  float sub_d = 1.5f;
+  float r0_scale = 1.1f;
+  int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
   size_t cub_bytes = 0;
 };
 
 namespace {
 
-constexpr int kIntsFixed = 4;
+constexpr int kIntsFixed = 6;
 constexpr int kTB = 256;
 
 int fail(sph_ctx *c, int code, const std::string &msg) {
@@ -199,6 +207,8 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->mass_s.ensure(n));
   SPH_CK(ctx->root.ensure(1));
   SPH_CK(ctx->stats.ensure(4));
+  SPH_CK(ctx->tasks.ensure(n + 32));
+  SPH_CK(ctx->members.ensure(n + 32));
   size_t need = std::max(cub_temp_needed((int)n), select_temp_needed((int)n));
   if (need > ctx->cub_temp.cap) SPH_CK(ctx->cub_temp.ensure(need));
   ctx->cub_bytes = ctx->cub_temp.cap;
@@ -227,6 +237,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.cub_temp_bytes = ctx->cub_bytes;
   tb.root = ctx->root.p;
   tb.bbox_ord = ctx->bbox_ord.p;
+  tb.r0_scale = ctx->r0_scale;
   return tb;
 }
 
@@ -297,20 +308,53 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.periodic = prm ? prm->periodic : 0;
   a.box = prm ? prm->box : 0.0;
   a.rmax = rmax;
+  a.dbg = nullptr;
+  a.sub_d = ctx->sub_d;
+  a.tasks = ctx->tasks.p;
+  a.members = ctx->members.p;
+  a.task_count = ctx->ints.p + 4;
+  a.member_cursor = ctx->ints.p + 5;
+  a.shortcut = ctx->shortcut;
+  if (ctx->debug && ctx->dbg.ensure(4 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
   return a;
 }
 
 // launch a pass kernel between two events (per-kernel device time)
-void timed_pass(sph_ctx *ctx, int mode, int f32, const PassArgs &a) {
+void timed_pass(sph_ctx *ctx, int mode, int f32, const PassArgs &a, int count, uint8_t want) {
   const int i = ctx->n_kev;
   if (i < 64) {
     ctx->kev_mode[i] = mode;
     cudaEventRecord(ctx->kev[2 * i], ctx->stream);
   }
-  launch_pass(ctx->stream, mode, f32, a, ctx->num_sms);
+  launch_pass(ctx->stream, mode, f32, a, count, want, ctx->num_sms);
   if (i < 64) {
     cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
     ctx->n_kev = i + 1;
+  }
+}
+
+// SPH_DEBUG=1: print the most expensive bundles of the last launch
+void debug_report(sph_ctx *ctx, int mode, int count) {
+  if (!ctx->debug) return;
+  int nb = 0;
+  cudaStreamSynchronize(ctx->stream);
+  cudaMemcpy(&nb, ctx->ints.p + 4, sizeof(int), cudaMemcpyDeviceToHost);
+  std::vector<unsigned long long> h(4 * (size_t)nb);
+  cudaMemcpy(h.data(), ctx->dbg.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+  std::vector<int> idx(nb);
+  for (int i = 0; i < nb; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return h[4 * x] > h[4 * y]; });
+  unsigned long long tot = 0, tt = 0;
+  for (int i = 0; i < nb; ++i) { tot += h[4 * i]; tt += h[4 * i + 1]; }
+  fprintf(stderr, "[sph dbg] mode %d: %d targets, %d bundles, sum cycles %.3g, tests %.3g\n", mode, count, nb,
+          (double)tot, (double)tt);
+  for (int i = 0; i < std::min(nb, 6); ++i) {
+    const unsigned long long *d = &h[4 * idx[i]];
+    float rb;
+    unsigned bits = (unsigned)d[3];
+    memcpy(&rb, &bits, 4);
+    fprintf(stderr, "   bundle %d: cycles %.3g tests %.3g p0 %u targets %u subs %u Rb %g\n", idx[i], (double)d[0],
+            (double)d[1], (unsigned)(d[2] >> 32), (unsigned)((d[2] >> 8) & 0xff), (unsigned)(d[2] & 0xff), rb);
   }
 }
 
@@ -332,7 +376,8 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
   const int n = a.n;
   a.list = nullptr;
   a.static_count = n;
-  timed_pass(ctx, mode, f32, a);
+  timed_pass(ctx, mode, f32, a, n, want);
+  debug_report(ctx, mode, n);
   ++*launches;
   int rounds = 1;
   for (;;) {
@@ -349,7 +394,8 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
       return fail(ctx, SPH_CUDA_ERROR, "neighbour search did not settle (internal round limit)");
     }
     a.list = ctx->list.p;
-    timed_pass(ctx, mode, f32, a);
+    timed_pass(ctx, mode, f32, a, remaining, want);
+    debug_report(ctx, mode, remaining);
     ++*launches;
     ++rounds;
   }
@@ -403,7 +449,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (rc) return rc;
   tm.mark(4);
   // ---- interact ----
-  timed_pass(ctx, MODE_DENS, compute_f32, a);
+  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
+  debug_report(ctx, MODE_DENS, n);
   ++launches;
   tm.mark(5);
   // ---- finalize ----
@@ -518,6 +565,11 @@ int sph_ctx_create(sph_ctx **out, int device) {
   }
   for (auto &e : c->ev) cudaEventCreate(&e);
   for (auto &e : c->kev) cudaEventCreate(&e);
+  const char *dbg = getenv("SPH_DEBUG");
+  c->debug = dbg && dbg[0] == '1';
+  if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
+  if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
+  if (const char *v = getenv("SPH_SHORTCUT")) c->shortcut = atoi(v);
   *out = c;
   return SPH_OK;
 }
@@ -531,7 +583,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
@@ -726,7 +778,7 @@ int sph_neighbor_counts(sph_ctx *ctx, int32_t precision, int32_t periodic, doubl
   prm.periodic = periodic;
   prm.box = box;
   PassArgs a = base_args(ctx, (int)n, 1, n_nodes, &prm, rmax);
-  launch_pass(s, MODE_COUNT, compute_f32, a, ctx->num_sms);
+  launch_pass(s, MODE_COUNT, compute_f32, a, (int)n, 0, ctx->num_sms);
   k_scatter_orig<int32_t><<<nblk(n), kTB, 0, s>>>((int)n, ctx->perm.p, ctx->counts_s.p, ctx->counts_o.p);
   launches += 3;
   SPH_CK(cudaMemcpyAsync(counts_out, ctx->counts_o.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));

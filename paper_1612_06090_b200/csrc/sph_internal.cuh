@@ -115,6 +115,13 @@ struct PassArgs {
   int periodic;
   double box;
   float rmax;               // largest meaningful search radius
+  unsigned long long *dbg;  // optional per-bundle diagnostics (4 words per bundle) or nullptr
+  float sub_d;              // task grouping: Chebyshev radius in units of the leader's radius
+  int2 *tasks;              // (offset into members, count) per task
+  uint32_t *members;        // task member targets (sorted positions)
+  int *task_count;          // device task counter
+  int *member_cursor;       // device member allocation cursor
+  int shortcut;             // bit per mode: count whole cells from their box when possible
 };
 
 // ---- launchers (sph_tree.cu) ----
@@ -138,6 +145,7 @@ struct TreeBuffers {
   size_t cub_temp_bytes;
   RootInfo *root;
   unsigned long long *bbox_ord;         // 6 ordered-int accumulators
+  float r0_scale;                       // initial radius = r0_scale * density estimate
 };
 
 int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
@@ -154,7 +162,7 @@ size_t cub_temp_needed(int n);
 
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
-void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int num_sms);
+void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
 size_t select_temp_needed(int n);

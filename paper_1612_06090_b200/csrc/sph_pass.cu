@@ -27,6 +27,8 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 namespace sph {
 
 namespace {
@@ -49,9 +51,15 @@ template <bool F32> struct Stage;
 template <> struct Stage<true> { using T = float4; };
 template <> struct Stage<false> { using T = D4; };
 
+// per warp: two staging buffers of 32 candidates + their sorted indices,
+// the range prefix sums and range bases, then the mode's per-lane tables
+template <bool F32>
+constexpr int stage_bytes() {
+  return 2 * 32 * (F32 ? 16 : 32) + 4 * 32 * 4;
+}
 template <int MODE, bool F32>
 constexpr int mode_smem_per_warp() {
-  return (F32 ? 32 * 16 : 32 * 32) +
+  return stage_bytes<F32>() +
          (MODE == MODE_HIST ? NB_HIST * 32 * 4 : MODE == MODE_BAND ? (BAND_CAP * 32 * 8 + NB_BAND * 32 * 4) : 0);
 }
 
@@ -88,7 +96,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
   const int wib = threadIdx.x >> 5;
   unsigned char *wbase = smem_raw + wib * mode_smem_per_warp<MODE, F32>();
   StageT *stage = reinterpret_cast<StageT *>(wbase);
-  unsigned char *mbase = wbase + (F32 ? 32 * 16 : 32 * 32);
+  int *sidxbuf = reinterpret_cast<int *>(wbase + 2 * 32 * sizeof(StageT));
+  int *spfx = sidxbuf + 64;
+  int *srsm = spfx + 32;
+  unsigned char *mbase = wbase + stage_bytes<F32>();
   unsigned *hist = reinterpret_cast<unsigned *>(mbase);                           // HIST
   double *band = reinterpret_cast<double *>(mbase);                               // BAND
   unsigned *bh = reinterpret_cast<unsigned *>(mbase + BAND_CAP * 32 * 8);         // BAND
@@ -103,22 +114,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
   unsigned long long tests = 0, accepted = 0;
 
   for (;;) {
+    // one task = one spatially coherent group of <= 32 targets (k_form)
     int b = 0;
     if (lane == 0) b = atomicAdd(a.work_counter, 1);
     b = __shfl_sync(FULL, b, 0);
-    const int count = a.list ? *a.list_count : a.static_count;
-    if (b * 32 >= count) break;
-    const int t = b * 32 + lane;
-    bool active = t < count;
-    const int p = a.list ? (int)a.list[active ? t : b * 32] : (active ? t : b * 32);
-    if constexpr (MODE != MODE_COUNT) {
-      const uint8_t st = a.state[p];
-      if constexpr (MODE == MODE_HIST) active = active && st == ST_NEED_HIST;
-      if constexpr (MODE == MODE_BAND) active = active && st == ST_NEED_BAND;
-      if constexpr (MODE == MODE_DENS) active = active && st == ST_DONE;
-    }
+    if (b >= *a.task_count) break;
+    const int2 task = a.tasks[b];
+    const long long dbg_t0 = a.dbg ? clock64() : 0;
+    const unsigned long long dbg_tests0 = tests;
+    int dbg_subs = 0;
+    float dbg_rb = 0.f;
+    const bool active = lane < task.y;
+    const int p = (int)a.members[task.x + (active ? lane : 0)];
     const unsigned amask = __ballot_sync(FULL, active);
-    if (!amask) continue;
 
     // target position (exact) and fp32 copy
     double tx, ty, tz;
@@ -196,13 +204,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       const int leader = __ffs(pending) - 1;
       const float lx = __shfl_sync(FULL, fx, leader), ly = __shfl_sync(FULL, fy, leader),
                   lz = __shfl_sync(FULL, fz, leader);
-      const float D = 1.5f * __shfl_sync(FULL, rad, leader) + 1e-30f;
+      const float D = INFINITY;  // tasks are already coherent groups
       const bool mem = ((pending >> lane) & 1u) && fabsf(fx - lx) <= D && fabsf(fy - ly) <= D &&
                        fabsf(fz - lz) <= D;
       const unsigned mmask = __ballot_sync(FULL, mem) | (1u << leader);
       const bool member = (mmask >> lane) & 1u;
       pending &= ~mmask;
       const int n_mem = __popc(mmask);
+      ++dbg_subs;
 
       // sub-bundle box and radius
       float bx0 = member ? (F32 ? fx : __double2float_rd(tx)) : INFINITY;
@@ -215,12 +224,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       bx1 = warp_max(bx1); by1 = warp_max(by1); bz1 = warp_max(bz1);
       const float Rb = warp_max(member ? rad : 0.f);
       const float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
+      dbg_rb = fmaxf(dbg_rb, Rb);
 
       // effective per-lane thresholds for this sub-bundle (non-members: none)
       float h_r2 = -1.f, h_inv = 0.f;  // HIST
       if constexpr (MODE == MODE_HIST) {
         if (member) {
-          hR2 = Rb * Rb;
+          hR2 = rad * rad;
           h_r2 = hR2;
           h_inv = 1.0f / hR2;
         }
@@ -253,6 +263,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
         const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
         const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
         const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
+        // this lane's target in the tree frame of the shift (x_i - s*box), plus slack
+        const float pqx = shifted ? (float)(tx - dsx) : fx, pqy = shifted ? (float)(ty - dsy) : fy,
+                    pqz = shifted ? (float)(tz - dsz) : fz;
+        const float pslack = shifted ? boxf * 4.8e-7f : (F32 ? 0.f : fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))) * 1.2e-7f);
 
         // range list: lane r holds range r
         int rs = 0, re = 0;
@@ -267,9 +281,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
             const int my = w + lane;
             bool hit = false;
             int my_skip = n_nodes, my_start = n;
+            float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), h4 = l4;
             if (my < n_nodes) {
-              const float4 l4 = nlo[my];
-              const float4 h4 = nhi[my];
+              l4 = nlo[my];
+              h4 = nhi[my];
               my_skip = __float_as_int(l4.w);
               my_start = __float_as_int(h4.w);
               hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
@@ -281,9 +296,57 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
               const int bb = kk - w;
               const int skp = __shfl_sync(FULL, my_skip, bb);
               if ((hitm >> bb) & 1u) {
-                if (skp == kk + 1) {  // cell
+                if (skp == kk + 1) {
+                  // Cell: classify it against each member's own thresholds from
+                  // its box alone.  If no member needs its particles (outside
+                  // every sphere, or wholly inside one histogram bin / wholly
+                  // below the bracket), count it without pair tests and skip it.
+                  const float cx0 = __shfl_sync(FULL, l4.x, bb), cy0 = __shfl_sync(FULL, l4.y, bb),
+                              cz0 = __shfl_sync(FULL, l4.z, bb), cx1 = __shfl_sync(FULL, h4.x, bb),
+                              cy1 = __shfl_sync(FULL, h4.y, bb), cz1 = __shfl_sync(FULL, h4.z, bb);
                   const int s0 = __shfl_sync(FULL, my_start, bb);
                   const int e0 = __shfl_sync(FULL, next_start, bb);
+                  const float gx = fmaxf(fmaxf(cx0 - pqx, pqx - cx1) - pslack, 0.f);
+                  const float gy = fmaxf(fmaxf(cy0 - pqy, pqy - cy1) - pslack, 0.f);
+                  const float gz = fmaxf(fmaxf(cz0 - pqz, pqz - cz1) - pslack, 0.f);
+                  const float gap2 = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps);
+                  const float fxa = fmaxf(pqx - cx0, cx1 - pqx) + pslack;
+                  const float fya = fmaxf(pqy - cy0, cy1 - pqy) + pslack;
+                  const float fza = fmaxf(pqz - cz0, cz1 - pqz) + pslack;
+                  const float dmax2 = (fxa * fxa + fya * fya + fza * fza) * (1.0f + 4.0f * kEps);
+                  const int ncell = e0 - s0;
+                  const int self_in = (!shifted && s0 <= p && p < e0) ? 1 : 0;
+                  bool need = false;
+                  int sc = -1;
+                  if constexpr (MODE == MODE_HIST) {
+                    if (gap2 <= h_r2) {
+                      const int b0 = min(max((__float_as_int(gap2 * h_inv) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
+                      const int b1 = min(max((__float_as_int(dmax2 * h_inv) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
+                      if (dmax2 <= h_r2 && b0 == b1) sc = b0; else need = true;
+                    }
+                  } else if constexpr (MODE == MODE_BAND) {
+                    if (!(gap2 > e_hi_f)) {
+                      if (dmax2 < e_lo_f) sc = ncell - self_in; else need = true;
+                    }
+                  } else if constexpr (MODE == MODE_COUNT) {
+                    if (!(gap2 > e_r2_hi_f)) {
+                      if (dmax2 <= e_r2_lo_f) sc = ncell - self_in; else need = true;
+                    }
+                  } else {
+                    need = gap2 < e_d2k_f;
+                  }
+                  if (!((a.shortcut >> MODE) & 1)) need = need || sc >= 0;
+                  if (!__any_sync(FULL, need)) {
+                    if constexpr (MODE == MODE_HIST) {
+                      if (sc >= 0) hist[sc * 32 + lane] += (unsigned)ncell;
+                    } else if constexpr (MODE == MODE_BAND) {
+                      if (sc > 0) c_below += sc;
+                    } else if constexpr (MODE == MODE_COUNT) {
+                      if (sc > 0) cnt += sc;
+                    }
+                    ++kk;
+                    continue;
+                  }
                   if (s0 == last_e) {
                     if (lane == nr - 1) re = e0;
                   } else {
@@ -299,18 +362,46 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
               }
             }
           }
-          for (int r = 0; r < nr; ++r) {
-            const int s0 = __shfl_sync(FULL, rs, r);
-            const int e0 = __shfl_sync(FULL, re, r);
-            for (int c0 = s0; c0 < e0; c0 += 32) {
-              const int nc = min(32, e0 - c0);
-              if (lane < nc) stage[lane] = pos[c0 + lane];
+          {
+            // Pack the ranges into one candidate stream, 32 per chunk, double
+            // buffered: the next chunk's loads are in flight while this chunk
+            // is tested.  Stream index s maps to range r = #{pfx <= s}.
+            const int len = lane < nr ? re - rs : 0;
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(FULL, incl, o);
+              if (lane >= o) incl += v;
+            }
+            const int total = __shfl_sync(FULL, incl, 31);
+            spfx[lane] = incl;
+            srsm[lane] = rs - (incl - len);
+            __syncwarp();
+            auto cand_of = [&](int sidx) -> int {
+              int r = 0;
+#pragma unroll
+              for (int step = 16; step; step >>= 1)
+                if (spfx[r + step - 1] <= sidx) r += step;
+              return srsm[r] + sidx;
+            };
+            int my_ci = lane < total ? cand_of(lane) : 0;
+            StageT v_cur;
+            if (lane < total) v_cur = pos[my_ci];
+            for (int c0 = 0; c0 < total; c0 += 32) {
+              StageT *stb = stage + ((c0 >> 5) & 1) * 32;
+              int *sti = sidxbuf + ((c0 >> 5) & 1) * 32;
+              const int nc = min(32, total - c0);
+              if (lane < nc) { stb[lane] = v_cur; sti[lane] = my_ci; }
               __syncwarp();
+              if (c0 + 32 + lane < total) {
+                my_ci = cand_of(c0 + 32 + lane);
+                v_cur = pos[my_ci];
+              }
               tests += (unsigned long long)nc * n_mem;
 #pragma unroll 4
               for (int j = 0; j < nc; ++j) {
-                const StageT c = stage[j];
-                const int cidx = c0 + j;
+                const StageT c = stb[j];
+                const int cidx = sti[j];
                 float af = 0.f;
                 double ad = 0.0;
                 if constexpr (F32) {
@@ -410,8 +501,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
                   }
                 }
               }
-              __syncwarp();
             }
+            __syncwarp();
           }
           nr = 0;
           last_e = -1;
@@ -420,6 +511,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       }
     }
 
+    if (a.dbg && lane == 0) {
+      unsigned long long *d = a.dbg + 4ull * b;
+      d[0] = (unsigned long long)(clock64() - dbg_t0);
+      d[1] = tests - dbg_tests0;
+      d[2] = ((unsigned long long)(unsigned)p << 32) | ((unsigned)__popc(amask) << 8) | (unsigned)dbg_subs;
+      d[3] = (unsigned long long)__float_as_uint(dbg_rb);
+    }
     // ---- per-mode finish ----
     if constexpr (MODE == MODE_HIST) {
       if (active) {
@@ -522,6 +620,62 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
   }
 }
 
+
+// Group the pending targets of a list into spatially coherent tasks: each
+// warp takes 32 consecutive list entries (sorted order) and splits them
+// greedily into groups whose members lie within sub_d * (leader radius) of
+// the leader (Chebyshev).  Groups are written contiguously to `members` and
+// described by (offset, count) in `tasks`; the pass kernels then schedule
+// tasks dynamically, one per warp, so distant targets never share a walk.
+template <int MODE, bool F32>
+__global__ void k_form(const PassArgs a, int count, uint8_t want) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = gw; c * 32 < count; c += nw) {
+    const int t = c * 32 + lane;
+    bool active = t < count;
+    const int p = a.list ? (int)a.list[active ? t : c * 32] : (active ? t : c * 32);
+    if constexpr (MODE != MODE_COUNT) active = active && a.state[p] == want;
+    float rad = 0.f;
+    if (active) {
+      if constexpr (MODE == MODE_HIST) rad = a.radius[p];
+      else if constexpr (MODE == MODE_BAND) rad = (float)sqrt(a.t_hi[p]);
+      else if constexpr (MODE == MODE_DENS) rad = (float)sqrt(a.d2k[p]);
+      else rad = fabsf((float)a.hfix[p]);
+      if (!(rad >= 0.f)) rad = 0.f;
+    }
+    float fx, fy, fz;
+    if constexpr (F32) {
+      const float4 v = reinterpret_cast<const float4 *>(a.pos)[p];
+      fx = v.x; fy = v.y; fz = v.z;
+    } else {
+      const D4 v = reinterpret_cast<const D4 *>(a.pos)[p];
+      fx = (float)v.x; fy = (float)v.y; fz = (float)v.z;
+    }
+    unsigned pending = __ballot_sync(FULL, active);
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const float lx = __shfl_sync(FULL, fx, leader), ly = __shfl_sync(FULL, fy, leader),
+                  lz = __shfl_sync(FULL, fz, leader);
+      const float D = a.sub_d * __shfl_sync(FULL, rad, leader) + 1e-30f;
+      const bool mem = ((pending >> lane) & 1u) && fabsf(fx - lx) <= D && fabsf(fy - ly) <= D &&
+                       fabsf(fz - lz) <= D;
+      const unsigned mmask = __ballot_sync(FULL, mem) | (1u << leader);
+      pending &= ~mmask;
+      const int nm = __popc(mmask);
+      int off = 0;
+      if (lane == 0) {
+        off = atomicAdd(a.member_cursor, nm);
+        const int slot = atomicAdd(a.task_count, 1);
+        a.tasks[slot] = make_int2(off, nm);
+      }
+      off = __shfl_sync(FULL, off, 0);
+      if ((mmask >> lane) & 1u) a.members[off + __popc(mmask & ((1u << lane) - 1u))] = (uint32_t)p;
+    }
+  }
+}
+
 template <int MODE, bool F32>
 void launch_one(cudaStream_t s, const PassArgs &a, int num_sms) {
   constexpr int smem = kWarps * mode_smem_per_warp<MODE, F32>();
@@ -542,23 +696,36 @@ struct StateIs {
 
 }  // namespace
 
-void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int num_sms) {
+template <int MODE, bool F32>
+void launch_form(cudaStream_t s, const PassArgs &a, int count, uint8_t want, int num_sms) {
+  const int warps = (count + 31) / 32;
+  const int blocks = std::max(1, std::min((warps + 7) / 8, num_sms * 16));
+  k_form<MODE, F32><<<blocks, 256, 0, s>>>(a, count, want);
+}
+
+void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {
   cudaMemsetAsync(a.work_counter, 0, sizeof(int), s);
+  cudaMemsetAsync(a.task_count, 0, sizeof(int), s);
+  cudaMemsetAsync(a.member_cursor, 0, sizeof(int), s);
+#define SPH_PASS_CASE(M, F)                 \
+  launch_form<M, F>(s, a, count, want, num_sms); \
+  launch_one<M, F>(s, a, num_sms);
   if (f32) {
     switch (mode) {
-      case MODE_HIST: launch_one<MODE_HIST, true>(s, a, num_sms); break;
-      case MODE_BAND: launch_one<MODE_BAND, true>(s, a, num_sms); break;
-      case MODE_DENS: launch_one<MODE_DENS, true>(s, a, num_sms); break;
-      default: launch_one<MODE_COUNT, true>(s, a, num_sms); break;
+      case MODE_HIST: SPH_PASS_CASE(MODE_HIST, true) break;
+      case MODE_BAND: SPH_PASS_CASE(MODE_BAND, true) break;
+      case MODE_DENS: SPH_PASS_CASE(MODE_DENS, true) break;
+      default: SPH_PASS_CASE(MODE_COUNT, true) break;
     }
   } else {
     switch (mode) {
-      case MODE_HIST: launch_one<MODE_HIST, false>(s, a, num_sms); break;
-      case MODE_BAND: launch_one<MODE_BAND, false>(s, a, num_sms); break;
-      case MODE_DENS: launch_one<MODE_DENS, false>(s, a, num_sms); break;
-      default: launch_one<MODE_COUNT, false>(s, a, num_sms); break;
+      case MODE_HIST: SPH_PASS_CASE(MODE_HIST, false) break;
+      case MODE_BAND: SPH_PASS_CASE(MODE_BAND, false) break;
+      case MODE_DENS: SPH_PASS_CASE(MODE_DENS, false) break;
+      default: SPH_PASS_CASE(MODE_COUNT, false) break;
     }
   }
+#undef SPH_PASS_CASE
 }
 
 size_t select_temp_needed(int n) {

@@ -268,7 +268,7 @@ __device__ __forceinline__ float f_ru(double v) { return __double2float_ru(v); }
 template <bool F32>
 __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl32,
                             const int *__restrict__ noff, const RootInfo *__restrict__ root,
-                            const void *__restrict__ pos_sorted, int k, float rmax,
+                            const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale,
                             float4 *__restrict__ nlo, float4 *__restrict__ nhi, float *__restrict__ r0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -321,22 +321,29 @@ __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, 
       }
       lo = make_float4(mn[0], mn[1], mn[2], __int_as_float(skip));
       hi = make_float4(mx[0], mx[1], mx[2], __int_as_float(p));
-      // initial search radius from the density of the smallest ancestor
-      // holding >= 2K particles (fewer retries than the reference's h0)
-      int La = L > 0 ? L - 1 : 0;
-      int cnt = n;
-      double half_a = root->half;
-      for (; La >= 0; --La) {
-        if (La == 0) { cnt = n; half_a = root->half; break; }
-        const unsigned long long kmin = kp & ~low_mask(La);
-        const int s = lower_bound_key(keys, p + 1, kmin);
-        const int e2 = upper_bound_key(keys, p + 1, n, kp | low_mask(La));
-        cnt = e2 - s;
-        if (cnt >= 2 * k) { half_a = ldexp(root->half, -La); break; }
+      // Initial search radius.  Density estimates from the smallest ancestors
+      // holding >= K/2 and >= 2K particles; the smaller of the two (an
+      // under-estimate costs one cheap retry, an over-estimate costs a large
+      // candidate volume), capped by the guaranteed bound sqrt(3)*side of the
+      // smallest ancestor holding >= K+1 particles.
+      double est_a = 0.0, est_b = 0.0, bound = 0.0;
+      for (int La = L; La >= 0; --La) {
+        int cnt;
+        if (La == 0) {
+          cnt = n;
+        } else {
+          const unsigned long long kmin = kp & ~low_mask(La);
+          const int s = lower_bound_key(keys, p + 1, kmin);
+          const int e2 = upper_bound_key(keys, p + 1, n, kp | low_mask(La));
+          cnt = e2 - s;
+        }
+        const double side = fmax(2.0 * ldexp(root->half, -La), 1e-300);
+        const double est = side * cbrt(3.0 * k / (4.0 * 3.14159265358979323846 * (double)max(cnt, 1)));
+        if (est_a == 0.0 && (cnt >= (k + 1) / 2 || La == 0)) est_a = est;
+        if (bound == 0.0 && (cnt >= k + 1 || La == 0)) bound = 1.7320508075688772 * side * (1.0 + 1e-6);
+        if (cnt >= 2 * k || La == 0) { est_b = est; break; }
       }
-      const double side = fmax(2.0 * half_a, 1e-300);
-      double h_est = side * cbrt(3.0 * k / (4.0 * 3.14159265358979323846 * (double)max(cnt, 1)));
-      float R = (float)(1.2 * h_est);
+      float R = (float)fmin(r0_scale * fmin(est_a, est_b), bound);
       if (!(R > 0.f)) R = rmax;
       R = fminf(R, rmax);
       for (int q = p; q < end; ++q) r0[q] = R;
@@ -430,10 +437,10 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   size_t tbytes = tb.cub_temp_bytes;
   cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
   if (compute_f32)
-    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax,
+    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
                                               tb.nlo, tb.nhi, tb.r0);
   else
-    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax,
+    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
                                                tb.nlo, tb.nhi, tb.r0);
   *launches += 3;
   return 0;

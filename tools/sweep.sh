@@ -1,0 +1,6 @@
+for cfg in "1.1" "0.8" "0.6" "0.45"; do
+  SPH_R0SCALE=$cfg python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/sw.json 2>/dev/null
+  python -c "
+import json; d=json.load(open('gpurun_out/sw.json'))
+print('r0 $cfg', round(d['ms_per_step'],2), {k: round(v,2) for k,v in d['kernel_ms_per_step'].items()}, d['pair_tests_per_step'], d['search_rounds'], d['select_rounds'])"
+done
