@@ -67,6 +67,7 @@ struct sph_ctx {
   DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4] task count [5] member cursor [6..] rounds hist
   DevBuf<int2> tasks;
   DevBuf<uint32_t> members;
+  DevBuf<int> cells;
   DevBuf<int> noff;
   DevBuf<float4> nlo, nhi;
   DevBuf<float> r0;
@@ -77,6 +78,7 @@ struct sph_ctx {
   DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
   bool debug = false;
+  bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
   float sub_d = 1.5f;
   float r0_scale = 1.1f;
   int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
@@ -206,7 +208,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->pos_sorted.ensure(32 * n));
   SPH_CK(ctx->mass_s.ensure(n));
   SPH_CK(ctx->root.ensure(1));
-  SPH_CK(ctx->stats.ensure(4));
+  SPH_CK(ctx->stats.ensure(8));
   SPH_CK(ctx->tasks.ensure(n + 32));
   SPH_CK(ctx->members.ensure(n + 32));
   size_t need = std::max(cub_temp_needed((int)n), select_temp_needed((int)n));
@@ -432,17 +434,56 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
   if (rc) return rc;
   tm.mark(2);
+  int hist_rounds = 0, band_rounds = 0;
+  if (ctx->fused) {
+  // ---- search + select + density: one fused persistent kernel over tasks ----
+  SPH_CK(cudaMemsetAsync(ctx->state.p, ST_NEED_HIST, n, ctx->stream));
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+  launch_form_only(ctx->stream, compute_f32, a, n, ST_NEED_HIST, ctx->num_sms);
+  SPH_CK(ctx->cells.ensure(fused_cell_list_ints(compute_f32, ctx->num_sms)));
+  FusedArgs fa{};
+  fa.n = n;
+  fa.k = k;
+  fa.kernel_kind = prm->kernel;
+  fa.dens64 = a.dens64;
+  fa.periodic = prm->periodic;
+  fa.box = prm->box;
+  fa.rmax = rmax;
+  fa.nlo = ctx->nlo.p;
+  fa.nhi = ctx->nhi.p;
+  fa.n_nodes = n_nodes;
+  fa.pos = ctx->pos_sorted.p;
+  fa.mass64 = ctx->mass_s.p;
+  fa.r0 = ctx->r0.p;
+  fa.tasks = ctx->tasks.p;
+  fa.members = ctx->members.p;
+  fa.task_count = a.task_count;
+  fa.work_counter = a.work_counter;
+  fa.d2k = ctx->d2k.p;
+  fa.rho = ctx->rho_s.p;
+  fa.state = ctx->state.p;
+  fa.cell_lists = ctx->cells.p;
+  fa.stats = ctx->stats.p;
+  fa.dbg = a.dbg;
+  tm.mark(3);
+  launch_fused(ctx->stream, compute_f32, fa, ctx->num_sms);
+  launches += 2;
+  tm.mark(4);
+  debug_report(ctx, 9, n);
+  tm.mark(5);
+  } else {
   // ---- search ----
   SPH_CK(cudaMemsetAsync(ctx->state.p, ST_NEED_HIST, n, ctx->stream));
-  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
   ++launches;
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  int hist_rounds = 0, band_rounds = 0;
   rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
   if (rc) return rc;
-  unsigned long long stat_h[2] = {0, 0};
-  SPH_CK(cudaMemcpyAsync(stat_h, ctx->stats.p, sizeof(stat_h), cudaMemcpyDeviceToHost, ctx->stream));
+  // search pair tests so far -> stats[3]
+  SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
   tm.mark(3);
   // ---- select ----
   rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
@@ -453,6 +494,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   debug_report(ctx, MODE_DENS, n);
   ++launches;
   tm.mark(5);
+  }
   // ---- finalize ----
   int *rounds_hist = ctx->ints.p + kIntsFixed;
   SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
@@ -464,12 +506,18 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   ++launches;
   tm.mark(6);
   std::vector<int> hist(max_it + 2);
-  unsigned long long stat_all[3] = {0, 0, 0};
+  unsigned long long stat_all[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
   SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
   SPH_CK(cudaStreamSynchronize(ctx->stream));
   SPH_CK(cudaGetLastError());
   collect_kernel_times(ctx, st);
+  if (st && ctx->fused) {
+    // split the fused kernel's device time over its phases by their warp cycles
+    const double fused_ms = tm.ms(3, 4);
+    const double cyc = (double)stat_all[5] + (double)stat_all[6] + (double)stat_all[7];
+    for (int i = 0; i < 3; ++i) st->t_kernel_ms[i] = cyc > 0 ? fused_ms * (double)stat_all[5 + i] / cyc : 0.0;
+  }
   if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
 
   // ---- stats, reference todo trace, error mapping ----
@@ -490,7 +538,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     }
     st->pair_tests = (int64_t)stat_all[0];
     st->accepted_pairs = (int64_t)stat_all[1];
-    st->search_pair_tests = (int64_t)stat_h[0];
+    st->search_pair_tests = (int64_t)stat_all[3];
     st->unconverged = unconv;
     st->bad_index = stat_all[2] == ~0ull ? -1 : (int64_t)stat_all[2];
     st->gpu_launches = launches;
@@ -498,6 +546,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     st->select_rounds = band_rounds;
     st->n_nodes = n_nodes;
   }
+  if (stat_all[4])
+    return fail(ctx, SPH_CUDA_ERROR, "exact K-th neighbour selection did not settle (internal round limit)");
   const bool degenerate = stat_all[2] != ~0ull;
   if (degenerate) {
     char buf[256];
@@ -567,6 +617,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   for (auto &e : c->kev) cudaEventCreate(&e);
   const char *dbg = getenv("SPH_DEBUG");
   c->debug = dbg && dbg[0] == '1';
+  if (const char *v = getenv("SPH_FUSED")) c->fused = v[0] == '1';
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
   if (const char *v = getenv("SPH_SHORTCUT")) c->shortcut = atoi(v);
@@ -583,7 +634,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
@@ -639,7 +690,7 @@ int sph_density_pass_device(sph_ctx *ctx, const sph_params *prm, const void *d_x
     st->t_stage_ms[1] = tm.ms(1, 2);
     st->t_stage_ms[2] = tm.ms(2, 3);
     st->t_stage_ms[3] = tm.ms(3, 4);
-    st->t_stage_ms[4] = tm.ms(4, 5);
+    st->t_stage_ms[4] = 0.0;
     st->t_stage_ms[5] = tm.ms(5, 6);
     st->t_stage_ms[6] = 0.0;
     st->t_stage_ms[7] = tm.ms(0, 7);
@@ -688,7 +739,7 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     st->t_stage_ms[1] = tm.ms(1, 2);
     st->t_stage_ms[2] = tm.ms(2, 3);
     st->t_stage_ms[3] = tm.ms(3, 4);
-    st->t_stage_ms[4] = tm.ms(4, 5);
+    st->t_stage_ms[4] = 0.0;
     st->t_stage_ms[5] = tm.ms(5, 6);
     st->t_stage_ms[6] = rc == SPH_OK ? tm.ms(6, 7) : 0.0;
     st->t_stage_ms[7] = tm.ms(0, 7);

@@ -15,7 +15,7 @@ constexpr double kWc6Norm = 1365.0 / (64.0 * 3.14159265358979323846);  // kernel
 constexpr double kM4Norm = 8.0 / 3.14159265358979323846;              // M4 (extension)
 
 // status bytes per target (sorted position)
-enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3 };
+enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3, ST_FAILED = 4 };
 
 // root cube of the reference octree (octree.py:324-336) + validation flags
 struct RootInfo {
@@ -123,6 +123,33 @@ struct PassArgs {
   int *member_cursor;       // device member allocation cursor
   int shortcut;             // bit per mode: count whole cells from their box when possible
 };
+
+// arguments of the fused search/select/density kernel (sph_fused.cu)
+struct FusedArgs {
+  int n, k, kernel_kind, dens64, periodic;
+  double box;
+  float rmax;
+  const float4 *nlo;
+  const float4 *nhi;
+  int n_nodes;
+  const void *pos;
+  const double *mass64;
+  const float *r0;
+  const int2 *tasks;
+  const uint32_t *members;
+  const int *task_count;
+  int *work_counter;
+  double *d2k;
+  double *rho;
+  uint8_t *state;
+  int *cell_lists;
+  unsigned long long *stats;  // [0] tests [1] accepted [2] bad index [3] search tests [4] unsettled
+  unsigned long long *dbg;
+};
+int fused_warps(int f32, int num_sms);
+size_t fused_cell_list_ints(int f32, int num_sms);
+void launch_fused(cudaStream_t s, int f32, const FusedArgs &a, int num_sms);
+void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
 
 // ---- launchers (sph_tree.cu) ----
 struct TreeBuffers {

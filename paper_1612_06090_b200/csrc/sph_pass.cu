@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
       bx0 = warp_min(bx0); by0 = warp_min(by0); bz0 = warp_min(bz0);
       bx1 = warp_max(bx1); by1 = warp_max(by1); bz1 = warp_max(bz1);
       const float Rb = warp_max(member ? rad : 0.f);
-      const float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
+      float R2b = Rb * Rb * (1.0f + 4.0f * kEps) + 1e-37f;
       dbg_rb = fmaxf(dbg_rb, Rb);
 
       // effective per-lane thresholds for this sub-bundle (non-members: none)
@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
           h_inv = 1.0f / hR2;
         }
       }
-      const double h_r2d = (double)h_r2, h_invd = (double)h_inv;
+      double h_r2d = (double)h_r2;
+      const double h_invd = (double)h_inv;
+      int seen = 0;  // HIST: candidates counted so far (self included)
       const float e_lo_f = member ? lo_f : -1.f, e_hi_f = member ? hi_f : -2.f;
       const float e_d2k_f = member ? d2k_f : -1.f;
       const double e_d2k = member ? d2k : -1.0;
@@ -273,30 +275,54 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
         int nr = 0, last_e = -1;
 
         // ---- stackless pre-order walk, interleaved with candidate processing ----
+        // A window of 32 consecutive pre-order nodes is box-tested at once (one
+        // per lane).  A missed node hides its subtree (the nodes up to its skip
+        // pointer); the visited nodes of the window are the hits not hidden by
+        // an earlier miss, found with one OR-reduction, and the walk jumps to
+        // the farthest skip of an unhidden miss.  Only visited cells are then
+        // handled one by one, in pre-order.
         int kk = 0;
+        unsigned pend = 0u;
+        int w = 0;
+        float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), h4 = l4;
+        int my_start = n, next_start = n;
         for (;;) {
           bool full = false;
-          while (kk < n_nodes && !full) {
-            const int w = kk;
-            const int my = w + lane;
-            bool hit = false;
-            int my_skip = n_nodes, my_start = n;
-            float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), h4 = l4;
-            if (my < n_nodes) {
-              l4 = nlo[my];
-              h4 = nhi[my];
-              my_skip = __float_as_int(l4.w);
-              my_start = __float_as_int(h4.w);
-              hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
+          for (;;) {
+            if (!pend) {
+              if (kk >= n_nodes) break;
+              w = kk;
+              const int my = w + lane;
+              bool hit = false;
+              int my_skip = n_nodes;
+              my_start = n;
+              l4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              h4 = l4;
+              if (my < n_nodes) {
+                l4 = nlo[my];
+                h4 = nhi[my];
+                my_skip = __float_as_int(l4.w);
+                my_start = __float_as_int(h4.w);
+                hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
+              }
+              next_start = __shfl_down_sync(FULL, my_start, 1);
+              if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
+              unsigned cov = 0u;
+              if (my < n_nodes && !hit) {
+                const int e = min(my_skip - w, 32);
+                cov = (e >= 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((2u << lane) - 1u);
+              }
+              const unsigned covered = __reduce_or_sync(FULL, cov);
+              const unsigned hitm = __ballot_sync(FULL, hit);
+              const unsigned cellm = __ballot_sync(FULL, my < n_nodes && my_skip == my + 1);
+              const bool jump = my < n_nodes && !hit && !((covered >> lane) & 1u);
+              const int far = (int)__reduce_max_sync(FULL, jump ? (unsigned)my_skip : 0u);
+              kk = max(w + 32, far);
+              pend = hitm & ~covered & cellm;
+              continue;
             }
-            const unsigned hitm = __ballot_sync(FULL, hit);
-            int next_start = __shfl_down_sync(FULL, my_start, 1);
-            if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
-            while (kk < w + 32 && kk < n_nodes) {
-              const int bb = kk - w;
-              const int skp = __shfl_sync(FULL, my_skip, bb);
-              if ((hitm >> bb) & 1u) {
-                if (skp == kk + 1) {
+            const int bb = __ffs(pend) - 1;
+            {
                   // Cell: classify it against each member's own thresholds from
                   // its box alone.  If no member needs its particles (outside
                   // every sphere, or wholly inside one histogram bin / wholly
@@ -338,29 +364,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
                   if (!((a.shortcut >> MODE) & 1)) need = need || sc >= 0;
                   if (!__any_sync(FULL, need)) {
                     if constexpr (MODE == MODE_HIST) {
-                      if (sc >= 0) hist[sc * 32 + lane] += (unsigned)ncell;
+                      if (sc >= 0) { hist[sc * 32 + lane] += (unsigned)ncell; seen += ncell; }
                     } else if constexpr (MODE == MODE_BAND) {
                       if (sc > 0) c_below += sc;
                     } else if constexpr (MODE == MODE_COUNT) {
                       if (sc > 0) cnt += sc;
                     }
-                    ++kk;
+                    pend &= pend - 1u;
                     continue;
                   }
                   if (s0 == last_e) {
                     if (lane == nr - 1) re = e0;
                   } else {
-                    if (nr == 32) { full = true; break; }  // resume at kk after processing
+                    if (nr == 32) { full = true; break; }  // resume at this cell after processing
                     if (lane == nr) { rs = s0; re = e0; }
                     ++nr;
                   }
                   last_e = e0;
-                }
-                ++kk;
-              } else {
-                kk = skp;
-              }
             }
+            pend &= pend - 1u;
           }
           {
             // Pack the ranges into one candidate stream, 32 per chunk, double
@@ -429,6 +451,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
                   if (in) {
                     const int bin = min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
                     hist[bin * 32 + lane] += 1u;
+                    ++seen;
                   }
                 } else if constexpr (MODE == MODE_BAND) {
                   if (!is_self) {
@@ -503,6 +526,24 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
               }
             }
             __syncwarp();
+          }
+          if constexpr (MODE == MODE_HIST) {
+            // Adaptive shrink: once >= K others are counted, the K-th lies at or
+            // below the upper edge of the bin holding the K-th so far; farther
+            // candidates cannot change it, so the lane stops looking beyond.
+            if (member && seen > K) {
+              int cum = 0, bb = 0;
+              for (; bb < NB_HIST; ++bb) {
+                cum += (int)hist[bb * 32 + lane];
+                if (cum > K) break;
+              }
+              if (bb < NB_HIST - 1) {
+                const float edge = __int_as_float((kHistBase + bb) << 21) * hR2 * (1.0f + 4.0f * kEps);
+                h_r2 = fminf(h_r2, edge);
+                h_r2d = (double)h_r2;
+              }
+            }
+            R2b = fminf(R2b, warp_max(member ? h_r2 : 0.f) * (1.0f + 4.0f * kEps) + 1e-37f);
           }
           nr = 0;
           last_e = -1;
@@ -726,6 +767,13 @@ void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count
     }
   }
 #undef SPH_PASS_CASE
+}
+
+void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {
+  cudaMemsetAsync(a.task_count, 0, sizeof(int), s);
+  cudaMemsetAsync(a.member_cursor, 0, sizeof(int), s);
+  if (f32) launch_form<MODE_HIST, true>(s, a, count, want, num_sms);
+  else launch_form<MODE_HIST, false>(s, a, count, want, num_sms);
 }
 
 size_t select_temp_needed(int n) {
