@@ -77,6 +77,7 @@ def config_json(w, cfg, n_gpus, kernel):
         3: "C3: 16,777,216 particles, fp32, NFW halos (20,000) + background, periodic box 252, K=64",
         4: "C4: 134,217,728 particles, fp32, NFW halos (150,000) + background, periodic box 400, K=64",
         5: "C5: 8,388,608 particles, fp32, single NFW halo c=20 r_vir=1 + 5% background, periodic box 4, K=128",
+        6: "diagnostic: 1,048,576 uniform particles, fp32, periodic box 100, K=64 (not a BASELINE config)",
     }[cfg]
     return {"workload": desc, "config_index": cfg, "n_particles": int(w["pos"].shape[0]), "k_neighbors": int(w["k"]),
             "box": float(w["box"]), "periodic": bool(w["periodic"]), "positions": "f32" if w["fp32"] else "f64",

@@ -70,6 +70,7 @@ struct sph_ctx {
   DevBuf<int> cells;
   DevBuf<int> noff;
   DevBuf<float4> nlo, nhi;
+  DevBuf<int> nsize;
   DevBuf<float> r0;
   DevBuf<unsigned char> pos_sorted, cub_temp;
   DevBuf<RootInfo> root;
@@ -80,6 +81,7 @@ struct sph_ctx {
   bool debug = false;
   bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
   float sub_d = 1.5f;
+  float sub_d_retry = 0.5f;  // retry rounds: smaller tasks (their targets are the expensive ones)
   float r0_scale = 1.1f;
   int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
   size_t cub_bytes = 0;
@@ -204,6 +206,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->noff.ensure(n + 1));
   SPH_CK(ctx->nlo.ensure(2 * n + 64));
   SPH_CK(ctx->nhi.ensure(2 * n + 64));
+  SPH_CK(ctx->nsize.ensure(2 * n + 64));
   SPH_CK(ctx->r0.ensure(n));
   SPH_CK(ctx->pos_sorted.ensure(32 * n));
   SPH_CK(ctx->mass_s.ensure(n));
@@ -232,6 +235,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.noff = ctx->noff.p;
   tb.nlo = ctx->nlo.p;
   tb.nhi = ctx->nhi.p;
+  tb.nsize = ctx->nsize.p;
   tb.r0 = ctx->r0.p;
   tb.pos_sorted = ctx->pos_sorted.p;
   tb.mass_sorted = ctx->mass_s.p;
@@ -293,6 +297,7 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.static_count = n;
   a.tree.nlo = ctx->nlo.p;
   a.tree.nhi = ctx->nhi.p;
+  a.tree.nsize = ctx->nsize.p;
   a.tree.n_nodes = n_nodes;
   a.pos = ctx->pos_sorted.p;
   a.mass64 = ctx->mass_s.p;
@@ -317,7 +322,7 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.task_count = ctx->ints.p + 4;
   a.member_cursor = ctx->ints.p + 5;
   a.shortcut = ctx->shortcut;
-  if (ctx->debug && ctx->dbg.ensure(4 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
+  if (ctx->debug && ctx->dbg.ensure(8 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
   return a;
 }
 
@@ -341,17 +346,22 @@ void debug_report(sph_ctx *ctx, int mode, int count) {
   int nb = 0;
   cudaStreamSynchronize(ctx->stream);
   cudaMemcpy(&nb, ctx->ints.p + 4, sizeof(int), cudaMemcpyDeviceToHost);
-  std::vector<unsigned long long> h(4 * (size_t)nb);
+  std::vector<unsigned long long> h(8 * (size_t)nb);
   cudaMemcpy(h.data(), ctx->dbg.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
   std::vector<int> idx(nb);
   for (int i = 0; i < nb; ++i) idx[i] = i;
-  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return h[4 * x] > h[4 * y]; });
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return h[8 * x] > h[8 * y]; });
   unsigned long long tot = 0, tt = 0;
-  for (int i = 0; i < nb; ++i) { tot += h[4 * i]; tt += h[4 * i + 1]; }
+  double win = 0, cvis = 0, cneed = 0, fl = 0;
+  for (int i = 0; i < nb; ++i) {
+    tot += h[8 * i]; tt += h[8 * i + 1];
+    win += h[8 * i + 4]; cvis += h[8 * i + 5]; cneed += h[8 * i + 6]; fl += h[8 * i + 7];
+  }
+  fprintf(stderr, "[sph dbg]   windows %.3g cells visited %.3g needed %.3g flushes %.3g\n", win, cvis, cneed, fl);
   fprintf(stderr, "[sph dbg] mode %d: %d targets, %d bundles, sum cycles %.3g, tests %.3g\n", mode, count, nb,
           (double)tot, (double)tt);
   for (int i = 0; i < std::min(nb, 6); ++i) {
-    const unsigned long long *d = &h[4 * idx[i]];
+    const unsigned long long *d = &h[8 * idx[i]];
     float rb;
     unsigned bits = (unsigned)d[3];
     memcpy(&rb, &bits, 4);
@@ -396,6 +406,7 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
       return fail(ctx, SPH_CUDA_ERROR, "neighbour search did not settle (internal round limit)");
     }
     a.list = ctx->list.p;
+    a.sub_d = ctx->sub_d_retry;
     timed_pass(ctx, mode, f32, a, remaining, want);
     debug_report(ctx, mode, remaining);
     ++*launches;
@@ -619,6 +630,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   c->debug = dbg && dbg[0] == '1';
   if (const char *v = getenv("SPH_FUSED")) c->fused = v[0] == '1';
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
+  if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
   if (const char *v = getenv("SPH_SHORTCUT")) c->shortcut = atoi(v);
   *out = c;
@@ -633,7 +645,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->out_rho.release(); c->out_flags.release(); c->keys_in.release(); c->keys.release(); c->bbox_ord.release();
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
-  c->noff.release(); c->nlo.release(); c->nhi.release(); c->r0.release(); c->pos_sorted.release();
+  c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
   c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);

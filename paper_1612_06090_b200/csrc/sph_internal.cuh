@@ -88,6 +88,7 @@ __device__ __forceinline__ float m4_profile_f(float q) {
 struct TreeView {
   const float4 *nlo;
   const float4 *nhi;
+  const int *nsize;   // particles in the node's subtree
   int n_nodes;
 };
 
@@ -165,6 +166,7 @@ struct TreeBuffers {
   int *noff;                            // n+1 node offsets per position
   int *n_nodes_dev;
   float4 *nlo, *nhi;
+  int *nsize;                           // particles per node subtree
   float *r0;                            // per sorted position initial radius
   void *pos_sorted;                     // float4 or double[4] per position
   double *mass_sorted;                  // fp64 masses per position

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
     const unsigned long long dbg_tests0 = tests;
     int dbg_subs = 0;
     float dbg_rb = 0.f;
+    unsigned long long dbg_win = 0, dbg_cvis = 0, dbg_cneed = 0, dbg_flush = 0;
     const bool active = lane < task.y;
     const int p = (int)a.members[task.x + (active ? lane : 0)];
     const unsigned amask = __ballot_sync(FULL, active);
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
             if (!pend) {
               if (kk >= n_nodes) break;
               w = kk;
+              ++dbg_win;
               const int my = w + lane;
               bool hit = false;
               int my_skip = n_nodes;
@@ -304,6 +306,37 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
                 my_skip = __float_as_int(l4.w);
                 my_start = __float_as_int(h4.w);
                 hit = box_gap2(l4, h4, qlx, qly, qlz, qhx, qhy, qhz) <= R2b;
+              }
+              // Internal nodes with many particles that are small next to the
+              // group's search region: keep them only if some member's own
+              // sphere reaches them (a dense clump at the edge of the group box
+              // would otherwise be descended cell by cell).
+              {
+                const bool big = hit && my_skip != my + 1 &&
+                                 fmaxf(h4.x - l4.x, fmaxf(h4.y - l4.y, h4.z - l4.z)) < 2.0f * Rb &&
+                                 a.tree.nsize[my] > 128;
+                const unsigned bigm = __ballot_sync(FULL, big);
+                if (bigm) {
+                  float wr2;
+                  if constexpr (MODE == MODE_HIST) wr2 = h_r2;
+                  else if constexpr (MODE == MODE_BAND) wr2 = e_hi_f;
+                  else if constexpr (MODE == MODE_DENS) wr2 = e_d2k_f;
+                  else wr2 = e_r2_hi_f;
+                  bool keep = false;
+                  unsigned mm = __ballot_sync(FULL, member);
+                  while (mm) {
+                    const int m = __ffs(mm) - 1;
+                    mm &= mm - 1u;
+                    const float mx = __shfl_sync(FULL, pqx, m), my_ = __shfl_sync(FULL, pqy, m),
+                                mz = __shfl_sync(FULL, pqz, m), mr2 = __shfl_sync(FULL, wr2, m),
+                                ms = __shfl_sync(FULL, pslack, m);
+                    const float gx = fmaxf(fmaxf(l4.x - mx, mx - h4.x) - ms, 0.f);
+                    const float gy = fmaxf(fmaxf(l4.y - my_, my_ - h4.y) - ms, 0.f);
+                    const float gz = fmaxf(fmaxf(l4.z - mz, mz - h4.z) - ms, 0.f);
+                    keep = keep || (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= mr2;
+                  }
+                  if (big) hit = keep;
+                }
               }
               next_start = __shfl_down_sync(FULL, my_start, 1);
               if (lane == 31) next_start = (w + 32 < n_nodes) ? __float_as_int(nhi[w + 32].w) : n;
@@ -322,6 +355,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
               continue;
             }
             const int bb = __ffs(pend) - 1;
+            ++dbg_cvis;
             {
                   // Cell: classify it against each member's own thresholds from
                   // its box alone.  If no member needs its particles (outside
@@ -373,10 +407,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
                     pend &= pend - 1u;
                     continue;
                   }
+                  ++dbg_cneed;
                   if (s0 == last_e) {
                     if (lane == nr - 1) re = e0;
                   } else {
-                    if (nr == 32) { full = true; break; }  // resume at this cell after processing
+                    if (nr == 32) { full = true; --dbg_cneed; break; }  // resume at this cell after processing
                     if (lane == nr) { rs = s0; re = e0; }
                     ++nr;
                   }
@@ -388,6 +423,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
             // Pack the ranges into one candidate stream, 32 per chunk, double
             // buffered: the next chunk's loads are in flight while this chunk
             // is tested.  Stream index s maps to range r = #{pfx <= s}.
+            ++dbg_flush;
             const int len = lane < nr ? re - rs : 0;
             int incl = len;
 #pragma unroll
@@ -553,7 +589,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_pass(const PassArgs a) {
     }
 
     if (a.dbg && lane == 0) {
-      unsigned long long *d = a.dbg + 4ull * b;
+      unsigned long long *d = a.dbg + 8ull * b;
+      d[4] = dbg_win;
+      d[5] = dbg_cvis;
+      d[6] = dbg_cneed;
+      d[7] = dbg_flush;
       d[0] = (unsigned long long)(clock64() - dbg_t0);
       d[1] = tests - dbg_tests0;
       d[2] = ((unsigned long long)(unsigned)p << 32) | ((unsigned)__popc(amask) << 8) | (unsigned)dbg_subs;

@@ -269,7 +269,8 @@ template <bool F32>
 __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl32,
                             const int *__restrict__ noff, const RootInfo *__restrict__ root,
                             const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale,
-                            float4 *__restrict__ nlo, float4 *__restrict__ nhi, float *__restrict__ r0) {
+                            float4 *__restrict__ nlo, float4 *__restrict__ nhi, int *__restrict__ nsize,
+                            float *__restrict__ r0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int L0 = first_level(keys, p);
@@ -350,6 +351,7 @@ __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, 
     }
     nlo[node] = lo;
     nhi[node] = hi;
+    nsize[node] = end - p;
   }
 }
 
@@ -438,10 +440,10 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
   if (compute_f32)
     k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
-                                              tb.nlo, tb.nhi, tb.r0);
+                                              tb.nlo, tb.nhi, tb.nsize, tb.r0);
   else
     k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
-                                               tb.nlo, tb.nhi, tb.r0);
+                                               tb.nlo, tb.nhi, tb.nsize, tb.r0);
   *launches += 3;
   return 0;
 }

@@ -165,6 +165,13 @@ def config(number: int, seed: int | None = None):
         h0 = _initial_h(box, n, 128)
         return dict(pos=pos, vel=vel, mass=np.full(n, 1.0 / n), h0=np.full(n, h0), k=128, box=box,
                     periodic=True, fp32=True, name="C5 single NFW halo 8388608 fp32")
+    if number == 6:  # diagnostic (not a BASELINE config): C2's size and box, uniform
+        n, box = 1 << 20, 100.0
+        pos = (np.random.default_rng(seed).random((n, 3)) * box).astype(np.float32).astype(np.float64)
+        pos[pos >= box] = np.float64(np.nextafter(np.float32(box), np.float32(0.0)))
+        return dict(pos=pos, vel=np.zeros((n, 3), np.float32), mass=np.full(n, 1.0 / n),
+                    h0=np.full(n, _initial_h(box, n, 64)), k=64, box=box, periodic=True, fp32=True,
+                    name="uniform 1048576 fp32 (diagnostic)")
     raise ValueError(f"unknown config {number}")
 
 
