@@ -59,6 +59,10 @@ typedef struct {
     double box;             /* periodic box side (ignored when periodic == 0) */
     int32_t kernel;         /* 0: Wendland C6 (the reference, kernel.py); 1: M4 cubic spline (extension) */
     int32_t reserved;
+    int64_t n_targets;      /* 0: every particle is a target.  Otherwise particles [0, n_targets) are
+                               targets and [n_targets, n) are ghosts (neighbour candidates only, e.g.
+                               the halo layer of a domain-decomposed run); h / rho / flags then hold
+                               n_targets entries */
 } sph_params;
 
 typedef struct {

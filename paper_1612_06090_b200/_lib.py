@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
 class SphParams(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("k", ctypes.c_int32), ("max_iterations", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("periodic", ctypes.c_int32), ("box", ctypes.c_double),
-                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32), ("n_targets", ctypes.c_int64)]
 
 
 class SphStats(ctypes.Structure):

@@ -109,6 +109,11 @@ int cuda_fail(sph_ctx *c, cudaError_t e, const char *where) {
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
   } while (0)
 
+__global__ void k_init_state(int n, int n_targets, const uint32_t *__restrict__ perm, uint8_t *__restrict__ state) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) state[p] = (int)perm[p] < n_targets ? ST_NEED_HIST : ST_GHOST;
+}
+
 __global__ void k_iota(int n, uint32_t *a) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (uint32_t)i;
@@ -117,7 +122,7 @@ __global__ void k_iota(int n, uint32_t *a) {
 // reference todo trace per particle: round j (1-based) searches with
 // h_{j-1} = h0 * g^(j-1) (sequential fp64 products, density.py:227) and
 // converges when count(h) >= K  <=>  d2_K <= h*h (octree.py:185, 215)
-__global__ void k_finalize(int n, const uint32_t *__restrict__ perm, const uint8_t *__restrict__ state,
+__global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ perm, const uint8_t *__restrict__ state,
                            const double *__restrict__ d2k, const double *__restrict__ rho_s,
                            const double *__restrict__ h0, int max_it, double *__restrict__ h_out,
                            double *__restrict__ rho_out, uint8_t *__restrict__ flags_out, int *rounds_hist,
@@ -126,7 +131,7 @@ __global__ void k_finalize(int n, const uint32_t *__restrict__ perm, const uint8
   for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) {
+  if (p < n && (int)perm[p] < n_targets) {  // ghosts (original index >= n_targets) are candidates only
     const uint32_t o = perm[p];
     const uint8_t st = state[p];
     const double d = st == ST_DONE ? d2k[p] : INFINITY;
@@ -420,6 +425,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
                      const double *mass, const double *h0, double *h_out, double *rho_out, uint8_t *flags_out,
                      sph_stats *st, Timer &tm) {
   const int n = (int)prm->n;
+  const int n_targets = prm->n_targets > 0 ? (int)prm->n_targets : n;
   const int k = prm->k;
   const int max_it = prm->max_iterations;
   int launches = 0;
@@ -448,7 +454,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   int hist_rounds = 0, band_rounds = 0;
   if (ctx->fused) {
   // ---- search + select + density: one fused persistent kernel over tasks ----
-  SPH_CK(cudaMemsetAsync(ctx->state.p, ST_NEED_HIST, n, ctx->stream));
+  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
   launch_form_only(ctx->stream, compute_f32, a, n, ST_NEED_HIST, ctx->num_sms);
@@ -485,7 +491,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   tm.mark(5);
   } else {
   // ---- search ----
-  SPH_CK(cudaMemsetAsync(ctx->state.p, ST_NEED_HIST, n, ctx->stream));
+  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
   ++launches;
@@ -512,7 +518,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const unsigned long long bad_init = ~0ull;
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
   k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
-      n, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out, rounds_hist,
+      n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out, rounds_hist,
       ctx->stats.p + 2);
   ++launches;
   tm.mark(6);
@@ -568,7 +574,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   if (unconv) {
     char buf[256];
-    snprintf(buf, sizeof(buf), "%lld of %d particles still flagged after %d iterations", unconv, n, max_it);
+    snprintf(buf, sizeof(buf), "%lld of %d particles still flagged after %d iterations", unconv, n_targets, max_it);
     return fail(ctx, SPH_NOT_CONVERGED, buf);
   }
   return SPH_OK;
@@ -583,6 +589,7 @@ int validate(sph_ctx *ctx, const sph_params *p) {
   if (p->max_iterations < 0) return fail(ctx, SPH_INVALID, "max_iterations must be >= 0");
   if (p->precision < 0 || p->precision > 2) return fail(ctx, SPH_INVALID, "unknown precision");
   if (p->kernel < 0 || p->kernel > 1) return fail(ctx, SPH_INVALID, "unknown kernel");
+  if (p->n_targets < 0 || p->n_targets > p->n) return fail(ctx, SPH_INVALID, "n_targets must be in [0, n]");
   return SPH_OK;
 }
 
@@ -693,7 +700,8 @@ int sph_density_pass_device(sph_ctx *ctx, const sph_params *prm, const void *d_x
   tm.mark(0);
   // the input h drives only the todo trace: keep a copy so d_h can be overwritten
   if (ctx->hfix.ensure(prm->n) != cudaSuccess) return fail(ctx, SPH_CUDA_ERROR, "out of device memory");
-  SPH_CK(cudaMemcpyAsync(ctx->hfix.p, d_h, sizeof(double) * prm->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  SPH_CK(cudaMemcpyAsync(ctx->hfix.p, d_h, sizeof(double) * (prm->n_targets > 0 ? prm->n_targets : prm->n),
+                         cudaMemcpyDeviceToDevice, ctx->stream));
   rc = density_pass_dev(ctx, prm, d_x, d_y, d_z, d_mass, ctx->hfix.p, d_h, d_rho, d_flags, st, tm);
   tm.mark(7);
   cudaStreamSynchronize(ctx->stream);
@@ -736,13 +744,14 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(h2d_strided(ctx->in_y.p, y, es, pos_stride, n, s));
   SPH_CK(h2d_strided(ctx->in_z.p, z, es, pos_stride, n, s));
   SPH_CK(h2d_strided(ctx->in_m.p, mass, 8, mass_stride, n, s));
-  SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, n, s));
+  const int64_t nt = prm->n_targets > 0 ? prm->n_targets : n;
+  SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, nt, s));
   rc = density_pass_dev(ctx, prm, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, ctx->hfix.p, ctx->io_h.p,
                         ctx->out_rho.p, ctx->out_flags.p, st, tm);
   if (rc == SPH_OK) {
-    SPH_CK(d2h_strided(h, ctx->io_h.p, 8, h_stride, n, s));
-    SPH_CK(d2h_strided(rho, ctx->out_rho.p, 8, rho_stride, n, s));
-    SPH_CK(d2h_strided(flags, ctx->out_flags.p, 1, flags_stride, n, s));
+    SPH_CK(d2h_strided(h, ctx->io_h.p, 8, h_stride, nt, s));
+    SPH_CK(d2h_strided(rho, ctx->out_rho.p, 8, rho_stride, nt, s));
+    SPH_CK(d2h_strided(flags, ctx->out_flags.p, 1, flags_stride, nt, s));
   }
   tm.mark(7);
   SPH_CK(cudaStreamSynchronize(s));

@@ -15,7 +15,7 @@ constexpr double kWc6Norm = 1365.0 / (64.0 * 3.14159265358979323846);  // kernel
 constexpr double kM4Norm = 8.0 / 3.14159265358979323846;              // M4 (extension)
 
 // status bytes per target (sorted position)
-enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3, ST_FAILED = 4 };
+enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3, ST_FAILED = 4, ST_GHOST = 5 };
 
 // root cube of the reference octree (octree.py:324-336) + validation flags
 struct RootInfo {

@@ -274,12 +274,15 @@ def ctypes_addr(a: int):
 
 def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MAX_ITERATIONS, *,
                      precision: str | None = None, periodic: bool = False, box: float = 0.0,
-                     kernel: str = "wendland_c6", device: int = 0, out=None):
+                     kernel: str = "wendland_c6", device: int = 0, out=None, n_targets: int | None = None):
     """SoA form of the pass on host arrays: returns (h, rho, flags, PassStats).
 
     ``precision`` defaults to the dtype of x ("f32" for float32 inputs).
     ``out`` = optional preallocated (h, rho, flags) host arrays (e.g. pinned);
     h is read as the initial smoothing length when ``h0`` is None.
+    ``n_targets``: only particles [0, n_targets) are targets; the rest are
+    ghosts (neighbour candidates only).  h0 / outputs then have n_targets
+    entries.
     """
     x = np.ascontiguousarray(x)
     if precision is None:
@@ -292,19 +295,22 @@ def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MA
     n = x.shape[0]
     if n == 0:
         raise ValueError("workload must contain at least one particle")
+    nt = n if n_targets is None else int(n_targets)
+    if not 0 < nt <= n:
+        raise ValueError(f"n_targets must be in [1, {n}], got {nt}")
     if out is not None:
         h, rho, flags = out
         if h0 is not None:
             h[:] = h0
     else:
-        h = np.array(np.broadcast_to(np.asarray(h0, dtype=np.float64), (n,)))
-        rho = np.zeros(n, dtype=np.float64)
-        flags = np.zeros(n, dtype=np.uint8)
+        h = np.array(np.broadcast_to(np.asarray(h0, dtype=np.float64), (nt,)))
+        rho = np.zeros(nt, dtype=np.float64)
+        flags = np.zeros(nt, dtype=np.uint8)
     ctx = _lib.context(device)
     L = _lib.load()
     prm = _lib.SphParams(n=n, k=k, max_iterations=max_iterations, precision=_lib.PRECISION[precision],
                          periodic=1 if periodic else 0, box=float(box), kernel=_lib.KERNELS[kernel],
-                         reserved=0)
+                         reserved=0, n_targets=0 if nt == n else nt)
     st = _lib.SphStats()
     t0 = time.perf_counter()
     es = x.itemsize

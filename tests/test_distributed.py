@@ -1,0 +1,117 @@
+"""Domain decomposition (paper_1612_06090_b200.distributed) on CPU: world
+size 2 (and 3) over gloo, the CPU oracle as the per-rank compute.  The
+decomposed result must equal the single-process reference pass bit for bit
+(h, density and the todo trace), open and periodic."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1612_06090_b200 import distributed as D
+from paper_1612_06090_b200 import workload
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def oracle_local_pass(x, y, z, m, h0_t, k, n_targets, periodic, box, max_iterations):
+    n = len(x)
+    h0 = np.concatenate([np.asarray(h0_t, np.float64), np.ones(n - n_targets)])
+    tg = np.arange(n_targets)
+    if periodic:
+        r = oracle.density_pass_periodic(x, y, z, m, h0, k, box, max_iterations, threads=1, targets=tg)
+    else:
+        r = oracle.density_pass(x, y, z, m, h0, k, max_iterations, threads=1, targets=tg)
+    return r.h[:n_targets], r.rho[:n_targets], r.todo_sizes
+
+
+def _dataset(n, periodic, seed):
+    if periodic:
+        pos, _, _ = workload.nfw_halos(n, 10.0, 6, seed=seed)
+        box = 10.0
+    else:
+        rng = np.random.default_rng(seed)
+        pos = np.concatenate([rng.normal(3.0, 0.4, (n // 2, 3)), rng.random((n - n // 2, 3)) * 8.0])
+        box = 0.0
+    mass = np.random.default_rng(seed + 1).random(n) + 0.5
+    h0 = np.full(n, 0.2)
+    return pos, mass, h0, box
+
+
+def _worker(rank, world, port, n, k, periodic, seed, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos, mass, h0, box = _dataset(n, periodic, seed)
+    sel = np.arange(rank, n, world)  # an arbitrary initial split
+    res = D.density_pass_distributed(pos[sel, 0], pos[sel, 1], pos[sel, 2], mass[sel], h0[sel], sel, k,
+                                     oracle_local_pass, periodic=periodic, box=box, samples=64)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), gid=res.gid, h=res.h, rho=res.rho, hist=res.todo_hist,
+             ghosts=res.n_ghosts, margin=res.margin)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,periodic", [(2, False), (2, True), (3, False)])
+def test_decomposition_matches_single_process(tmp_path, world, periodic):
+    import torch.multiprocessing as mp
+    n, k, seed = 1500, 16, 11
+    mp.spawn(_worker, args=(world, _free_port(), n, k, periodic, seed, str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
+    gid = np.concatenate([p["gid"] for p in parts])
+    assert np.array_equal(np.sort(gid), np.arange(n))  # every particle owned exactly once
+    h = np.empty(n)
+    rho = np.empty(n)
+    h[gid] = np.concatenate([p["h"] for p in parts])
+    rho[gid] = np.concatenate([p["rho"] for p in parts])
+    pos, mass, h0, box = _dataset(n, periodic, seed)
+    if periodic:
+        want = oracle.density_pass_periodic(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, box, threads=1)
+    else:
+        want = oracle.density_pass(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, threads=1)
+    assert np.array_equal(h, want.h)
+    assert np.array_equal(rho, want.rho)
+    hist = sum(p["hist"] for p in parts)
+    assert np.array_equal(D.todo_sizes_from_hist(hist), want.todo_sizes)
+    assert all(int(p["ghosts"]) > 0 for p in parts)
+
+
+def test_morton_keys_match_oracle_perm():
+    # the partition keys are the ordering keys: sorting by them (stable) and
+    # ordering leaves by index reproduces the reference perm for capacity-1
+    # separable sets; here: keys sort consistently with the oracle perm
+    rng = np.random.default_rng(3)
+    pos = rng.random((2000, 3))
+    lo, hi = pos.min(0), pos.max(0)
+    c, half = D.root_cube(lo, hi)
+    keys = D.morton_keys(pos, c, half)
+    perm = oracle.perm(pos[:, 0], pos[:, 1], pos[:, 2])
+    # the reference perm visits leaves in key order: keys along perm are
+    # non-decreasing at leaf granularity (prefix of the leaf level)
+    k_perm = keys[perm]
+    shifted = k_perm >> np.uint64(63 - 3 * 2)  # level-2 prefixes (leaves are deeper)
+    assert np.all(np.diff(shifted.astype(np.int64)) >= 0)
+
+
+def test_box_distance_min_image():
+    p = np.array([[0.1, 5.0, 5.0], [9.9, 5.0, 5.0], [5.0, 5.0, 5.0]])
+    lo, hi = np.array([8.0, 4.0, 4.0]), np.array([9.5, 6.0, 6.0])
+    d2 = D.box_distance2(p, lo, hi, True, 10.0)
+    assert np.allclose(d2, [0.6 ** 2, 0.4 ** 2, 3.0 ** 2])
+    d2o = D.box_distance2(p, lo, hi, False, 10.0)
+    assert np.allclose(d2o, [7.9 ** 2, 0.4 ** 2, 3.0 ** 2])
+
+
+def test_todo_hist_roundtrip():
+    todo = np.array([100, 40, 7, 1])
+    hist = D.hist_from_todo_sizes(todo, 10)
+    assert hist.sum() == 100
+    assert np.array_equal(D.todo_sizes_from_hist(hist), todo)
