@@ -50,7 +50,7 @@ class SphStats(ctypes.Structure):
             "iterations": self.iterations,
             "todo_sizes": [int(self.todo_sizes[i]) for i in range(min(self.n_todo, MAX_TODO))],
             "t_stage_ms": {name: float(self.t_stage_ms[i]) for i, name in enumerate(
-                ("h2d", "tree", "group", "neighbours", "unused", "finalize", "d2h", "total"))},
+                ("h2d", "tree", "search", "select", "density", "finalize", "d2h", "total"))},
             "pair_tests": int(self.pair_tests),
             "accepted_pairs": int(self.accepted_pairs),
             "search_pair_tests": int(self.search_pair_tests),

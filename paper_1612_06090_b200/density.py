@@ -187,12 +187,11 @@ def _stats_from(st: _lib.SphStats, t_total: float) -> PassStats:
     todo = np.array(d["todo_sizes"], dtype=np.int64)
     ts = d["t_stage_ms"]
     tk = d["t_kernel_ms"]
-    # the fused kernel's device time split over its phases by warp cycles
     phase = {
         "tree_build": ts["tree"] / 1e3,
-        "search": (ts["group"] + tk["search"]) / 1e3,
-        "select": tk["select"] / 1e3,
-        "interact": tk["density"] / 1e3,
+        "search": ts["search"] / 1e3,
+        "select": ts["select"] / 1e3,
+        "interact": ts["density"] / 1e3,
         "layout": (ts["h2d"] + ts["finalize"] + ts["d2h"]) / 1e3,
     }
     return PassStats(iteration_count=int(st.iterations), todo_sizes=todo, phase_times=phase,
