@@ -80,9 +80,17 @@ struct sph_ctx {
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
   bool debug = false;
   bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
-  float sub_d = 1.5f;
-  float sub_d_retry = 0.5f;  // retry rounds: smaller tasks (their targets are the expensive ones)
+  bool mega = false;   // SPH_MEGA=1: work-queue megakernel instead of round-by-round kernels
+  int mega_fallbacks = 0;
+  double last_mega_ms = 0.0;
+  DevBuf<int4> items;
+  DevBuf<uint32_t> pool;
+  DevBuf<uint8_t> band_rounds;
+  DevBuf<int> qints;
+  float sub_d = 2.0f;
+  float sub_d_retry = 2.0f;  // task extent of retry rounds (SPH_SUBD_RETRY)
   float r0_scale = 1.1f;
+  float c0_scale = 1e30f;  // SPH_C0SCALE: cap R0 by c0 x the cell's tight-box estimate (off by default)
   int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
   size_t cub_bytes = 0;
 };
@@ -249,6 +257,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.root = ctx->root.p;
   tb.bbox_ord = ctx->bbox_ord.p;
   tb.r0_scale = ctx->r0_scale;
+  tb.c0_scale = ctx->c0_scale;
   return tb;
 }
 
@@ -363,6 +372,15 @@ void debug_report(sph_ctx *ctx, int mode, int count) {
     win += h[8 * i + 4]; cvis += h[8 * i + 5]; cneed += h[8 * i + 6]; fl += h[8 * i + 7];
   }
   fprintf(stderr, "[sph dbg]   windows %.3g cells visited %.3g needed %.3g flushes %.3g\n", win, cvis, cneed, fl);
+  if (const char *dump = getenv("SPH_DEBUG_DUMP")) {
+    static int seq = 0;
+    char path[512];
+    snprintf(path, sizeof(path), "%s_%02d_mode%d.bin", dump, seq++, mode);
+    if (FILE *f = fopen(path, "wb")) {
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+  }
   fprintf(stderr, "[sph dbg] mode %d: %d targets, %d bundles, sum cycles %.3g, tests %.3g\n", mode, count, nb,
           (double)tot, (double)tt);
   for (int i = 0; i < std::min(nb, 6); ++i) {
@@ -448,6 +466,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const int compute_f32 = prm->precision == SPH_PRECISION_F32 || (prm->precision == 2 && !root.not_f32);
   const float rmax = compute_rmax(root, prm->periodic, prm->box);
   int n_nodes = 0;
+  ctx->last_mega_ms = 0.0;
   rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
   if (rc) return rc;
   tm.mark(2);
@@ -489,6 +508,45 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   tm.mark(4);
   debug_report(ctx, 9, n);
   tm.mark(5);
+  } else if (ctx->mega) {
+  // ---- search + select + density: one persistent kernel over a device work queue ----
+  bool done_mega = false;
+  {
+    const int item_cap = 2 * n + 65536, pool_cap = 4 * n + 65536;
+    if (ctx->items.ensure(item_cap) == cudaSuccess && ctx->pool.ensure(pool_cap) == cudaSuccess &&
+        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(8) == cudaSuccess) {
+      k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
+      SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+      PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+      tm.mark(3);
+      launch_mega(ctx->stream, compute_f32, a, n, n_targets, ctx->items.p, item_cap, ctx->pool.p, pool_cap,
+                  ctx->qints.p, ctx->band_rounds.p, ctx->num_sms);
+      launches += 3;
+      int ovf = 0;
+      SPH_CK(cudaMemcpyAsync(&ovf, ctx->qints.p + 4, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      SPH_CK(cudaStreamSynchronize(ctx->stream));
+      SPH_CK(cudaGetLastError());
+      tm.mark(4);
+      tm.mark(5);
+      done_mega = ovf == 0;
+      ctx->last_mega_ms = done_mega ? tm.ms(3, 4) : 0.0;
+    }
+  }
+  if (!done_mega) {  // queue storage exhausted: the round-by-round path below
+    ctx->mega_fallbacks++;
+  }
+  if (!done_mega) {
+  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
+  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+  rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
+  if (rc) return rc;
+  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
+  if (rc) return rc;
+  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
+  ++launches;
+  }
   } else {
   // ---- search ----
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
@@ -536,6 +594,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     for (int i = 0; i < 3; ++i) st->t_kernel_ms[i] = cyc > 0 ? fused_ms * (double)stat_all[5 + i] / cyc : 0.0;
   }
   if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
+  if (st && ctx->mega && ctx->last_mega_ms > 0.0) st->t_kernel_ms[0] = ctx->last_mega_ms;
 
   // ---- stats, reference todo trace, error mapping ----
   const long long unconv = hist[max_it + 1];
@@ -636,9 +695,11 @@ int sph_ctx_create(sph_ctx **out, int device) {
   const char *dbg = getenv("SPH_DEBUG");
   c->debug = dbg && dbg[0] == '1';
   if (const char *v = getenv("SPH_FUSED")) c->fused = v[0] == '1';
+  if (const char *v = getenv("SPH_MEGA")) c->mega = v[0] == '1';
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
+  if (const char *v = getenv("SPH_C0SCALE")) c->c0_scale = (float)atof(v);
   if (const char *v = getenv("SPH_SHORTCUT")) c->shortcut = atoi(v);
   *out = c;
   return SPH_OK;
@@ -653,7 +714,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

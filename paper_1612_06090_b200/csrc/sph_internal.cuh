@@ -151,6 +151,8 @@ int fused_warps(int f32, int num_sms);
 size_t fused_cell_list_ints(int f32, int num_sms);
 void launch_fused(cudaStream_t s, int f32, const FusedArgs &a, int num_sms);
 void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
+void launch_mega(cudaStream_t s, int f32, const PassArgs &a, int n, int n_targets, int4 *items, int item_cap,
+                 uint32_t *pool, int pool_cap, int *qints, uint8_t *band_rounds, int num_sms);
 
 // ---- launchers (sph_tree.cu) ----
 struct TreeBuffers {
@@ -175,6 +177,7 @@ struct TreeBuffers {
   RootInfo *root;
   unsigned long long *bbox_ord;         // 6 ordered-int accumulators
   float r0_scale;                       // initial radius = r0_scale * density estimate
+  float c0_scale;                       // ... capped by c0_scale * the cell's own tight-box estimate
 };
 
 int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,

@@ -268,7 +268,7 @@ __device__ __forceinline__ float f_ru(double v) { return __double2float_ru(v); }
 template <bool F32>
 __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl32,
                             const int *__restrict__ noff, const RootInfo *__restrict__ root,
-                            const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale,
+                            const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale, float c0_scale,
                             float4 *__restrict__ nlo, float4 *__restrict__ nhi, int *__restrict__ nsize,
                             float *__restrict__ r0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -344,7 +344,17 @@ __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, 
         if (bound == 0.0 && (cnt >= k + 1 || La == 0)) bound = 1.7320508075688772 * side * (1.0 + 1e-6);
         if (cnt >= 2 * k || La == 0) { est_b = est; break; }
       }
-      float R = (float)fmin(r0_scale * fmin(est_a, est_b), bound);
+      // tight-box density of the cell itself: small dense clumps that sit in a
+      // large, mostly empty ancestor are otherwise over-estimated by far
+      double est_c = INFINITY;
+      if (end - p >= 4) {
+        const double side_c = 2.0 * ldexp(root->half, -L);
+        const double fl = 0.05 * side_c;
+        const double vol = fmax((double)mx[0] - mn[0], fl) * fmax((double)mx[1] - mn[1], fl) *
+                           fmax((double)mx[2] - mn[2], fl);
+        est_c = cbrt(3.0 * k * vol / (4.0 * 3.14159265358979323846 * (double)(end - p)));
+      }
+      float R = (float)fmin(fmin(r0_scale * fmin(est_a, est_b), c0_scale * est_c), bound);
       if (!(R > 0.f)) R = rmax;
       R = fminf(R, rmax);
       for (int q = p; q < end; ++q) r0[q] = R;
@@ -439,10 +449,10 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   size_t tbytes = tb.cub_temp_bytes;
   cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
   if (compute_f32)
-    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
+    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale,
                                               tb.nlo, tb.nhi, tb.nsize, tb.r0);
   else
-    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale,
+    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale,
                                                tb.nlo, tb.nhi, tb.nsize, tb.r0);
   *launches += 3;
   return 0;
