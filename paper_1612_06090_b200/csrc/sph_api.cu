@@ -80,6 +80,12 @@ struct sph_ctx {
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
   bool debug = false;
   bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
+  bool v3 = true;      // SPH_V3=0: the round-by-round k_pass pipeline
+  bool v3band = false; // SPH_V3BAND=1: select from the recorded lists (else k_pass BAND tasks)
+  int last_legacy = 0;
+  DevBuf<uint32_t> mpool;
+  DevBuf<int4> sgs;
+  DevBuf<int> owner, v3scratch, lpool;
   bool mega = false;   // SPH_MEGA=1: work-queue megakernel instead of round-by-round kernels
   int mega_fallbacks = 0;
   double last_mega_ms = 0.0;
@@ -122,6 +128,19 @@ __global__ void k_init_state(int n, int n_targets, const uint32_t *__restrict__ 
   if (p < n) state[p] = (int)perm[p] < n_targets ? ST_NEED_HIST : ST_GHOST;
 }
 
+__global__ void k_append_sgs(const int2 *tasks, const int *count, int4 *sgs, int base) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *count) {
+    const int2 t = tasks[i];
+    sgs[base + i] = make_int4(t.x, t.y, -1, 0);
+  }
+}
+
+__global__ void k_state_map(int n, uint8_t *state, uint8_t from, uint8_t to) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && state[i] == from) state[i] = to;
+}
+
 __global__ void k_iota(int n, uint32_t *a) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (uint32_t)i;
@@ -142,7 +161,8 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
   if (p < n && (int)perm[p] < n_targets) {  // ghosts (original index >= n_targets) are candidates only
     const uint32_t o = perm[p];
     const uint8_t st = state[p];
-    const double d = st == ST_DONE ? d2k[p] : INFINITY;
+    const bool fin = st == ST_DONE || st == ST_FINAL;
+    const double d = fin ? d2k[p] : INFINITY;
     double hc = h0[o];
     int r = 1;
     bool conv = false;
@@ -154,7 +174,7 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
     atomicAdd(&sh[bin], 1);
     if (conv && d == 0.0) atomicMin(bad, (unsigned long long)o);
     h_out[o] = __dsqrt_rn(d);
-    rho_out[o] = st == ST_DONE ? rho_s[p] : 0.0;
+    rho_out[o] = fin ? rho_s[p] : 0.0;
     flags_out[o] = conv ? 0 : 1;
   }
   __syncthreads();
@@ -508,6 +528,121 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   tm.mark(4);
   debug_report(ctx, 9, n);
   tm.mark(5);
+  } else if (ctx->v3) {
+  // ---- "walk once, sweep narrow": k_form groups, one recorded walk per group ----
+  int rc3 = 0;
+  {
+    const size_t member_cap = 3 * (size_t)n + 1024, list_cap = 160 * (size_t)n + (1u << 20);
+    SPH_CK(ctx->mpool.ensure(member_cap));
+    SPH_CK(ctx->sgs.ensure(3 * (size_t)n + 1024));
+    SPH_CK(ctx->owner.ensure(n));
+    SPH_CK(ctx->v3scratch.ensure(v3_scratch_ints(ctx->num_sms)));
+    if (ctx->lpool.ensure(std::min(list_cap, (size_t)INT32_MAX / 2)) != cudaSuccess) SPH_CK(ctx->lpool.ensure(1 << 22));
+    SPH_CK(ctx->qints.ensure(8));
+    cudaStream_t s = ctx->stream;
+    k_init_state<<<nblk(n), kTB, 0, s>>>(n, n_targets, ctx->perm.p, ctx->state.p);
+    k_iota<<<nblk(n), kTB, 0, s>>>(n, ctx->iota.p);
+    SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), s));
+    SPH_CK(cudaMemsetAsync(ctx->owner.p, 0xff, sizeof(int) * n, s));
+    SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 8 * sizeof(int), s));  // [0] member cursor [1] list cursor [2] legacy [3] sg total
+    PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+    V3Args v{};
+    v.a = a;
+    v.f32 = compute_f32;
+    v.sgs = ctx->sgs.p;
+    v.members = ctx->mpool.p;
+    v.owner = ctx->owner.p;
+    v.scratch = ctx->v3scratch.p;
+    v.list_pool = ctx->lpool.p;
+    v.list_cursor = ctx->qints.p + 1;
+    v.list_cap = (int)std::min(ctx->lpool.cap, (size_t)INT32_MAX / 2);
+    v.legacy_count = ctx->qints.p + 2;
+    int sg_total = 0, remaining = n_targets;
+    const uint32_t *list = nullptr;
+    if (ctx->debug) fprintf(stderr, "[sph v3] start n=%d nodes=%d\n", n, n_nodes);
+    for (int round = 0; remaining > 0 && round < 24; ++round) {
+      // group this round's targets into the member pool
+      PassArgs f = a;
+      f.list = list;
+      f.members = ctx->mpool.p;
+      f.member_cursor = ctx->qints.p + 0;
+      SPH_CK(cudaMemsetAsync(f.task_count, 0, sizeof(int), s));
+      launch_form_only_keep(s, compute_f32, f, list ? remaining : n, ST_NEED_HIST, ctx->num_sms);
+      k_append_sgs<<<nblk(list ? remaining : n), kTB, 0, s>>>(ctx->tasks.p, f.task_count, ctx->sgs.p, sg_total);
+      v.sg_begin = sg_total;
+      v.sg_count = f.task_count;
+      launch_v3(s, MODE_HIST, v, ctx->num_sms);
+      launches += 3;
+      ++hist_rounds;
+      int tc = 0;
+      SPH_CK(cudaMemcpyAsync(&tc, f.task_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+      launch_select(s, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
+                    ctx->cub_bytes);
+      int mc = 0;
+      SPH_CK(cudaMemcpyAsync(&remaining, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaMemcpyAsync(&mc, ctx->qints.p + 0, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaStreamSynchronize(s));
+      SPH_CK(cudaGetLastError());
+      sg_total += tc;
+      list = ctx->list.p;
+      if (ctx->debug) fprintf(stderr, "[sph v3] hist round %d: %d groups, %d still searching, members %d\n", round, tc, remaining, mc);
+      if ((size_t)mc + (size_t)remaining > member_cap || (size_t)sg_total + (size_t)remaining > ctx->sgs.cap) {
+        k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_NEED_HIST, ST_LEGACY);
+        break;
+      }
+    }
+    if (remaining > 0) k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_NEED_HIST, ST_LEGACY);
+    tm.mark(3);
+    SPH_CK(cudaMemcpyAsync(ctx->qints.p + 3, &sg_total, sizeof(int), cudaMemcpyHostToDevice, s));
+    SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    // select: every group, lanes whose bracket it found
+    v.sg_begin = 0;
+    v.sg_count = ctx->qints.p + 3;
+    int band_left = ctx->v3band ? 1 : 0;
+    if (!ctx->v3band) {
+      PassArgs b = base_args(ctx, n, k, n_nodes, prm, rmax);
+      rc3 = run_rounds(ctx, MODE_BAND, compute_f32, b, ST_NEED_BAND, 64, &launches, &band_rounds);
+      if (rc3) return rc3;
+    }
+    for (int round = 0; band_left > 0 && round < 40; ++round) {
+      launch_v3(s, MODE_BAND, v, ctx->num_sms);
+      ++launches;
+      ++band_rounds;
+      launch_select(s, ctx->iota.p, n, ctx->state.p, ST_NEED_BAND, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
+                    ctx->cub_bytes);
+      SPH_CK(cudaMemcpyAsync(&band_left, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaStreamSynchronize(s));
+      SPH_CK(cudaGetLastError());
+      if (ctx->debug) fprintf(stderr, "[sph v3] band round %d: %d left\n", round, band_left);
+    }
+    if (band_left > 0) rc3 = fail(ctx, SPH_CUDA_ERROR, "exact K-th neighbour selection did not settle");
+    tm.mark(4);
+    launch_v3(s, MODE_DENS, v, ctx->num_sms);
+    ++launches;
+    // targets the recorded lists could not serve: round-by-round kernels
+    int legacy = 0;
+    SPH_CK(cudaMemcpyAsync(&legacy, ctx->qints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+    launch_select(s, ctx->iota.p, n, ctx->state.p, ST_LEGACY, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
+                  ctx->cub_bytes);
+    int nleg = 0;
+    SPH_CK(cudaMemcpyAsync(&nleg, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPH_CK(cudaStreamSynchronize(s));
+    SPH_CK(cudaGetLastError());
+    ctx->last_legacy = nleg;
+    if (nleg > 0 && rc3 == 0) {
+      k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_LEGACY, ST_NEED_HIST);
+      PassArgs b = base_args(ctx, n, k, n_nodes, prm, rmax);
+      int hr = 0, br = 0;
+      rc = run_rounds(ctx, MODE_HIST, compute_f32, b, ST_NEED_HIST, 64, &launches, &hr);
+      if (rc) return rc;
+      rc = run_rounds(ctx, MODE_BAND, compute_f32, b, ST_NEED_BAND, 64, &launches, &br);
+      if (rc) return rc;
+      timed_pass(ctx, MODE_DENS, compute_f32, b, n, ST_DONE);
+      ++launches;
+    }
+    tm.mark(5);
+  }
+  if (rc3) return rc3;
   } else if (ctx->mega) {
   // ---- search + select + density: one persistent kernel over a device work queue ----
   bool done_mega = false;
@@ -595,6 +730,11 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
   if (st && ctx->mega && ctx->last_mega_ms > 0.0) st->t_kernel_ms[0] = ctx->last_mega_ms;
+  if (st && ctx->v3 && !ctx->fused) {
+    st->t_kernel_ms[0] = tm.ms(2, 3);
+    st->t_kernel_ms[1] = tm.ms(3, 4);
+    st->t_kernel_ms[2] = tm.ms(4, 5);
+  }
 
   // ---- stats, reference todo trace, error mapping ----
   const long long unconv = hist[max_it + 1];
@@ -696,6 +836,8 @@ int sph_ctx_create(sph_ctx **out, int device) {
   c->debug = dbg && dbg[0] == '1';
   if (const char *v = getenv("SPH_FUSED")) c->fused = v[0] == '1';
   if (const char *v = getenv("SPH_MEGA")) c->mega = v[0] == '1';
+  if (const char *v = getenv("SPH_V3")) c->v3 = v[0] == '1';
+  if (const char *v = getenv("SPH_V3BAND")) c->v3band = v[0] == '1';
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
@@ -714,7 +856,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

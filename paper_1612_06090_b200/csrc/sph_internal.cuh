@@ -15,7 +15,8 @@ constexpr double kWc6Norm = 1365.0 / (64.0 * 3.14159265358979323846);  // kernel
 constexpr double kM4Norm = 8.0 / 3.14159265358979323846;              // M4 (extension)
 
 // status bytes per target (sorted position)
-enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3, ST_FAILED = 4, ST_GHOST = 5 };
+enum : uint8_t { ST_NEED_HIST = 0, ST_NEED_BAND = 1, ST_DONE = 2, ST_UNREACHABLE = 3, ST_FAILED = 4, ST_GHOST = 5,
+                 ST_LEGACY = 6, ST_FINAL = 8 };
 
 // root cube of the reference octree (octree.py:324-336) + validation flags
 struct RootInfo {
@@ -151,8 +152,27 @@ int fused_warps(int f32, int num_sms);
 size_t fused_cell_list_ints(int f32, int num_sms);
 void launch_fused(cudaStream_t s, int f32, const FusedArgs &a, int num_sms);
 void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
+void launch_form_only_keep(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
 void launch_mega(cudaStream_t s, int f32, const PassArgs &a, int n, int n_targets, int4 *items, int item_cap,
                  uint32_t *pool, int pool_cap, int *qints, uint8_t *band_rounds, int num_sms);
+
+// "walk once, sweep narrow" kernels (sph_knn.cu)
+struct V3Args {
+  PassArgs a;
+  int f32;
+  int4 *sgs;                 // per group: member offset, member count, list offset (-1: none), list length
+  const int *sg_count;       // groups of this launch
+  int sg_begin;              // first group index of this launch
+  const uint32_t *members;   // member pool (all rounds)
+  int *owner;                // per target: group that found its bracket
+  int *scratch;              // per-warp recorded-cell scratch
+  int *list_pool;
+  int *list_cursor;
+  int list_cap;
+  int *legacy_count;
+};
+size_t v3_scratch_ints(int num_sms);
+void launch_v3(cudaStream_t s, int mode, const V3Args &v, int num_sms);
 
 // ---- launchers (sph_tree.cu) ----
 struct TreeBuffers {

@@ -439,17 +439,31 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
               StageT *stb = stage + ((c0 >> 5) & 1) * 32;
               int *sti = sidxbuf + ((c0 >> 5) & 1) * 32;
               const int nc = min(32, total - c0);
+              // slots past nc hold a NaN sentinel: every test below is a
+              // comparison that is false for NaN, so the batch of 4 needs no tail
               if (lane < nc) { stb[lane] = v_cur; sti[lane] = my_ci; }
+              else { StageT z = v_cur; z.x = __int_as_float(0x7fc00000); stb[lane] = z; sti[lane] = -1; }
               __syncwarp();
               if (c0 + 32 + lane < total) {
                 my_ci = cand_of(c0 + 32 + lane);
                 v_cur = pos[my_ci];
               }
               tests += (unsigned long long)nc * n_mem;
-#pragma unroll 4
-              for (int j = 0; j < nc; ++j) {
-                const StageT c = stb[j];
-                const int cidx = sti[j];
+              // batches of BU loaded before any shared store: the candidate
+              // loads and distance math of a batch overlap (DENS keeps BU=1:
+              // its register budget is taken by the kernel evaluation)
+              constexpr int BU = MODE == MODE_DENS ? 1 : 4;
+              const int ncr = (nc + BU - 1) & ~(BU - 1);
+#pragma unroll 1
+              for (int j0 = 0; j0 < ncr; j0 += BU) {
+               StageT cb[BU];
+               int ib[BU];
+#pragma unroll
+               for (int u = 0; u < BU; ++u) { cb[u] = stb[j0 + u]; ib[u] = sti[j0 + u]; }
+#pragma unroll
+               for (int u = 0; u < BU; ++u) {
+                const StageT c = cb[u];
+                const int cidx = ib[u];
                 float af = 0.f;
                 double ad = 0.0;
                 if constexpr (F32) {
@@ -476,7 +490,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                   else { in = ad <= h_r2d; x = (float)(ad * h_invd); }
                   if (in) {
                     const int bin = min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
-                    hist[bin * 32 + lane] += 1u;
+                    atomicAdd(&hist[bin * 32 + lane], 1u);  // no return value: no LDS->STS chain
                     ++seen;
                   }
                 } else if constexpr (MODE == MODE_BAND) {
@@ -496,7 +510,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                         emin = fmin(emin, e);
                         emax = fmax(emax, e);
                         const int bin = min(max((int)((e - lo) * scale), 0), NB_BAND - 1);
-                        bh[bin * 32 + lane] += 1u;
+                        atomicAdd(&bh[bin * 32 + lane], 1u);
                       }
                     }
                   }
@@ -549,6 +563,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                     }
                   }
                 }
+               }
               }
             }
             __syncwarp();
@@ -1010,6 +1025,12 @@ void launch_mega(cudaStream_t s, int f32, const PassArgs &a, int n, int n_target
     k_mega<true><<<mega_blocks<true>(num_sms), kWarps * 32, kWarps * mode_smem_per_warp<MODE_BAND, true>(), s>>>(m, q);
   else
     k_mega<false><<<mega_blocks<false>(num_sms), kWarps * 32, kWarps * mode_smem_per_warp<MODE_BAND, false>(), s>>>(m, q);
+}
+
+// grouping only, appending to the member pool at *a.member_cursor (not reset)
+void launch_form_only_keep(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {
+  if (f32) launch_form<MODE_HIST, true>(s, a, count, want, num_sms);
+  else launch_form<MODE_HIST, false>(s, a, count, want, num_sms);
 }
 
 void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {

@@ -208,7 +208,7 @@ def test_ghost_targets_match_full_pass():
     h, rho, flags, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0[:nt], k, n_targets=nt)
     assert h.shape == (nt,)
     assert np.array_equal(h, full_h[:nt])
-    assert _rel(rho, full_rho[:nt]) <= 1e-12
+    assert _rel(rho, full_rho[:nt]) <= RTOL_F32  # fp32 sums: the order follows the task grouping
     want = oracle.density_pass(*(pos.astype(np.float64).T), mass, h0, k, targets=np.arange(nt))
     assert np.array_equal(st.todo_sizes, want.todo_sizes)
 
