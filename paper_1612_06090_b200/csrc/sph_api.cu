@@ -80,7 +80,15 @@ struct sph_ctx {
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
   bool debug = false;
   bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
-  bool v3 = true;      // SPH_V3=0: the round-by-round k_pass pipeline
+  bool v3 = false;     // SPH_V3=1: walk-once / sweep-narrow kernels (sph_knn.cu, experimental)
+  bool warp = false;   // SPH_WARP=1: the per-target kernel for every target (no bundle pass)
+  bool hybrid = true;  // SPH_HYBRID=0: bundle histogram rounds until settled
+  bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
+  int list_mult = 4;   // SPH_LISTCAP: neighbour-list capacity per target in units of K
+  int last_list_fallbacks = 0;
+  DevBuf<uint2> nlists;
+  DevBuf<int> kids, parent, cellof;
+  DevBuf<int> ncount;
   bool v3band = false; // SPH_V3BAND=1: select from the recorded lists (else k_pass BAND tasks)
   int last_legacy = 0;
   DevBuf<uint32_t> mpool;
@@ -408,8 +416,9 @@ void debug_report(sph_ctx *ctx, int mode, int count) {
     float rb;
     unsigned bits = (unsigned)d[3];
     memcpy(&rb, &bits, 4);
-    fprintf(stderr, "   bundle %d: cycles %.3g tests %.3g p0 %u targets %u subs %u Rb %g\n", idx[i], (double)d[0],
-            (double)d[1], (unsigned)(d[2] >> 32), (unsigned)((d[2] >> 8) & 0xff), (unsigned)(d[2] & 0xff), rb);
+    fprintf(stderr, "   bundle %d: cycles %.3g tests %.3g p0 %u targets %u subs %u Rb %g win %llu cvis %llu cneed %llu fl %llu\n",
+            idx[i], (double)d[0], (double)d[1], (unsigned)(d[2] >> 32), (unsigned)((d[2] >> 8) & 0xff),
+            (unsigned)(d[2] & 0xff), rb, d[4], d[5], d[6], d[7]);
   }
 }
 
@@ -527,6 +536,66 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   launches += 2;
   tm.mark(4);
   debug_report(ctx, 9, n);
+  tm.mark(5);
+  } else if (ctx->warp && n <= (1 << 27)) {
+  // ---- one warp per target: search, exact select and density in one kernel ----
+  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
+  k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
+  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  SPH_CK(ctx->qints.ensure(8));
+  SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
+  SPH_CK(ctx->kids.ensure(8 * (size_t)n_nodes));
+  SPH_CK(ctx->parent.ensure(n_nodes));
+  SPH_CK(ctx->cellof.ensure(n));
+  launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->kids.p, ctx->parent.p, ctx->cellof.p);
+  a.tree.kids = ctx->kids.p;
+  a.tree.parent = ctx->parent.p;
+  a.tree.cellof = ctx->cellof.p;
+  SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+  {
+    const int i = ctx->n_kev;
+    if (i < 64) {
+      ctx->kev_mode[i] = MODE_HIST;
+      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
+    }
+    launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+    if (i < 64) {
+      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
+      ctx->n_kev = i + 1;
+    }
+  }
+  ++launches;
+  hist_rounds = 1;
+  if (ctx->debug) {
+    int fbk[2] = {0, 0};
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses\n", fbk[0], fbk[1]);
+    std::vector<uint8_t> hs(n);
+    cudaMemcpy(hs.data(), ctx->state.p, n, cudaMemcpyDeviceToHost);
+    int cnt[16] = {0};
+    for (int i = 0; i < n; ++i) cnt[hs[i] & 15]++;
+    fprintf(stderr, "[sph warp] states:");
+    for (int i = 0; i < 16; ++i) if (cnt[i]) fprintf(stderr, " %d:%d", i, cnt[i]);
+    fprintf(stderr, "\n");
+  }
+  SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  tm.mark(3);
+  // targets the stack could not serve: the bundle search passes
+  {
+    int hr = 0;
+    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hr);
+    if (rc) return rc;
+    hist_rounds += hr;
+  }
+  // targets the lists could not serve: walking select + density
+  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
+  if (rc) return rc;
+  tm.mark(4);
+  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
+  ++launches;
   tm.mark(5);
   } else if (ctx->v3) {
   // ---- "walk once, sweep narrow": k_form groups, one recorded walk per group ----
@@ -689,13 +758,86 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
   ++launches;
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
+  // neighbour lists recorded by the histogram pass (entry index field: 27 bits)
+  bool use_lists = false;
+  if (ctx->lists && ctx->list_mult > 0 && n <= (1 << 27)) {
+    const size_t cap = std::min((size_t)ctx->list_mult * (size_t)k, (size_t)lists_max_cap());
+    if (ctx->nlists.ensure(cap * (size_t)n) == cudaSuccess && ctx->ncount.ensure(n) == cudaSuccess &&
+        ctx->qints.ensure(8) == cudaSuccess) {
+      a.nlists = ctx->nlists.p;
+      a.ncount = ctx->ncount.p;
+      a.ncap = (int)cap;
+      use_lists = true;
+    } else {
+      cudaGetLastError();  // allocation failure: walk-based select/density instead
+    }
+  }
+  if (ctx->hybrid && n <= (1 << 27)) {
+    // bundle histogram pass once; the targets it could not settle go to the
+    // per-target kernel (own radius growth, no further rounds)
+    timed_pass(ctx, MODE_HIST, compute_f32, a, n, ST_NEED_HIST);
+    ++launches;
+    launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->list.p, ctx->ints.p + 2,
+                  ctx->cub_temp.p, ctx->cub_bytes);
+    launches += 2;
+    PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
+    SPH_CK(ctx->kids.ensure(8 * (size_t)n_nodes));
+    SPH_CK(ctx->parent.ensure(n_nodes));
+    SPH_CK(ctx->cellof.ensure(n));
+    launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->kids.p, ctx->parent.p, ctx->cellof.p);
+    t.tree.kids = ctx->kids.p;
+    t.tree.parent = ctx->parent.p;
+    t.tree.cellof = ctx->cellof.p;
+    t.list = ctx->list.p;
+    SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
+    SPH_CK(ctx->qints.ensure(8));
+    const int i = ctx->n_kev;
+    if (i < 64) {
+      ctx->kev_mode[i] = MODE_HIST;
+      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
+    }
+    launch_target(ctx->stream, compute_f32, t, target_list_cap(k), nullptr, ctx->num_sms);
+    if (i < 64) {
+      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
+      ctx->n_kev = i + 1;
+    }
+    launches += 2;
+    hist_rounds = 2;
+    // stack overflows (rare) stay NEED_HIST: bundle rounds
+    int hr = 0;
+    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hr);
+  } else {
+    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
+  }
   if (rc) return rc;
   // search pair tests so far -> stats[3]
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);
-  // ---- select ----
+  // ---- select (+ density) ----
+  if (use_lists) {
+    SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+    const int i = ctx->n_kev;
+    if (i < 64) {
+      ctx->kev_mode[i] = MODE_BAND;
+      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
+    }
+    launch_lists(ctx->stream, compute_f32, a, ctx->qints.p + 5, ctx->num_sms);
+    if (i < 64) {
+      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
+      ctx->n_kev = i + 1;
+    }
+    ++launches;
+    if (ctx->debug) {
+      int fbk[3] = {0, 0, 0};
+      cudaStreamSynchronize(ctx->stream);
+      cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
+      ctx->last_list_fallbacks = fbk[0] + fbk[1] + fbk[2];
+      fprintf(stderr, "[sph lists] fall back to the walking select: %d overflowed lists, %d bracket misses, %d crowded brackets\n",
+              fbk[0], fbk[1], fbk[2]);
+    }
+    a.nlists = nullptr;
+  }
   rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
   if (rc) return rc;
   tm.mark(4);
@@ -838,6 +980,10 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_MEGA")) c->mega = v[0] == '1';
   if (const char *v = getenv("SPH_V3")) c->v3 = v[0] == '1';
   if (const char *v = getenv("SPH_V3BAND")) c->v3band = v[0] == '1';
+  if (const char *v = getenv("SPH_LISTS")) c->lists = v[0] == '1';
+  if (const char *v = getenv("SPH_WARP")) c->warp = v[0] == '1';
+  if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
+  if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
@@ -856,7 +1002,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->ncount.release(); c->kids.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -90,6 +90,9 @@ struct TreeView {
   const float4 *nlo;
   const float4 *nhi;
   const int *nsize;   // particles in the node's subtree
+  const int *kids;    // 8 child node ids per node (-1 padded), for the per-target traversal
+  const int *parent;  // parent node id (-1 for the root)
+  const int *cellof;  // cell holding each sorted particle
   int n_nodes;
 };
 
@@ -124,6 +127,11 @@ struct PassArgs {
   int *task_count;          // device task counter
   int *member_cursor;       // device member allocation cursor
   int shortcut;             // bit per mode: count whole cells from their box when possible
+  // neighbour lists recorded by the histogram pass (nullptr = off): per target
+  // ncap entries {idx | shift << 27, fp32 d2 bits} or {cell start | shift << 27, tag | count}
+  uint2 *nlists;
+  int *ncount;              // entries recorded (> ncap: overflowed, list unusable)
+  int ncap;
 };
 
 // arguments of the fused search/select/density kernel (sph_fused.cu)
@@ -215,6 +223,14 @@ size_t cub_temp_needed(int n);
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
 void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
+// exact select + density from the histogram pass's neighbour lists (sph_lists.cu)
+void launch_lists(cudaStream_t s, int f32, const PassArgs &a, int *fallbacks, int num_sms);
+int lists_max_cap();
+// fused per-target search + select + density (sph_warp.cu)
+int target_list_cap(int k);
+void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms);
+void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, int *kids, int *parent,
+                 int *cellof);
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
 size_t select_temp_needed(int n);

@@ -42,6 +42,7 @@ constexpr int kHistBase = (127 - kHistOctaves) << 2;
 constexpr int NB_HIST = kHistOctaves * 4 + 2;
 constexpr int BAND_CAP = 32;
 constexpr int NB_BAND = 16;
+constexpr unsigned kCellTag = 0xff000000u;  // neighbour-list entry: .y = tag | count -> whole cell [.x, .x + count)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard
 constexpr double kEpsD = 9.5367431640625e-07;
 
@@ -139,6 +140,9 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
     // ---- per-lane state ----
     float rad = 0.f;
     float hR2 = 0.f;  // HIST: histogram range R_b^2 of this lane's sub-bundle
+    float h_fin = 0.f;  // HIST: final (shrunk) acceptance radius^2: the recorded list is complete below it
+    int ne = 0;         // HIST: neighbour-list entries recorded for this lane's target
+    uint2 *const nl = (MODE == MODE_HIST && a.nlists && active) ? a.nlists + (size_t)p * a.ncap : nullptr;
     // BAND
     double lo = 0.0, hi = -1.0, scale = 0.0, emin = INFINITY, emax = -INFINITY;
     float lo_f = -1.f, hi_f = -2.f;
@@ -223,12 +227,40 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
         if (member) {
           hR2 = rad * rad;
           h_r2 = hR2;
+          h_fin = hR2;
           h_inv = 1.0f / hR2;
         }
       }
       double h_r2d = (double)h_r2;
       const double h_invd = (double)h_inv;
       int seen = 0;  // HIST: candidates counted so far (self included)
+      int seen_shrunk = 0;
+      // Adaptive shrink: once >= K others are counted, the K-th lies at or
+      // below the upper edge of the bin holding the K-th so far; farther
+      // candidates cannot change it, so the lane stops looking beyond.  A
+      // recorded neighbour list is compacted to the new radius.
+      auto shrink = [&](int, float &hr2) {
+        int cum = 0, bb = 0;
+        for (; bb < NB_HIST; ++bb) {
+          cum += (int)hist[bb * 32 + lane];
+          if (cum > K) break;
+        }
+        if (bb < NB_HIST - 1) {
+          const float edge = __int_as_float((kHistBase + bb) << 21) * hR2 * (1.0f + 4.0f * kEps);
+          if (edge < hr2) {
+            hr2 = edge;
+            h_fin = edge;
+            if (nl && ne > 2 * K && ne <= a.ncap) {
+              int w2 = 0;
+              for (int i = 0; i < ne; ++i) {
+                const uint2 e = nl[i];
+                if (e.y >= kCellTag || __uint_as_float(e.y) <= edge) nl[w2++] = e;
+              }
+              ne = w2;
+            }
+          }
+        }
+      };
       const float e_lo_f = member ? lo_f : -1.f, e_hi_f = member ? hi_f : -2.f;
       const float e_d2k_f = member ? d2k_f : -1.f;
       const double e_d2k = member ? d2k : -1.0;
@@ -388,7 +420,14 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                   if (!((a.shortcut >> MODE) & 1)) need = need || sc >= 0;
                   if (!__any_sync(FULL, need)) {
                     if constexpr (MODE == MODE_HIST) {
-                      if (sc >= 0) { hist[sc * 32 + lane] += (unsigned)ncell; seen += ncell; }
+                      if (sc >= 0) {
+                        hist[sc * 32 + lane] += (unsigned)ncell;
+                        seen += ncell;
+                        if (nl) {  // whole cell recorded as one entry
+                          if (ne < a.ncap) nl[ne] = make_uint2((unsigned)s0 | ((unsigned)sidx << 27), kCellTag | (unsigned)ncell);
+                          ++ne;
+                        }
+                      }
                     } else if constexpr (MODE == MODE_BAND) {
                       if (sc > 0) c_below += sc;
                     } else if constexpr (MODE == MODE_COUNT) {
@@ -492,6 +531,10 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                     const int bin = min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
                     atomicAdd(&hist[bin * 32 + lane], 1u);  // no return value: no LDS->STS chain
                     ++seen;
+                    if (nl) {
+                      if (ne < a.ncap) nl[ne] = make_uint2((unsigned)cidx | ((unsigned)sidx << 27), __float_as_uint(F32 ? af : (float)ad));
+                      ++ne;
+                    }
                   }
                 } else if constexpr (MODE == MODE_BAND) {
                   if (!is_self) {
@@ -565,25 +608,21 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                 }
                }
               }
+              if constexpr (MODE == MODE_HIST) {
+                // list recording: shrink as soon as K/2 more were counted, so
+                // that the list stays near K entries
+                if (nl && member && seen > K && seen - seen_shrunk >= (K >> 1)) {
+                  shrink(seen, h_r2);
+                  seen_shrunk = seen;
+                }
+                h_r2d = (double)h_r2;
+              }
             }
             __syncwarp();
           }
           if constexpr (MODE == MODE_HIST) {
-            // Adaptive shrink: once >= K others are counted, the K-th lies at or
-            // below the upper edge of the bin holding the K-th so far; farther
-            // candidates cannot change it, so the lane stops looking beyond.
-            if (member && seen > K) {
-              int cum = 0, bb = 0;
-              for (; bb < NB_HIST; ++bb) {
-                cum += (int)hist[bb * 32 + lane];
-                if (cum > K) break;
-              }
-              if (bb < NB_HIST - 1) {
-                const float edge = __int_as_float((kHistBase + bb) << 21) * hR2 * (1.0f + 4.0f * kEps);
-                h_r2 = fminf(h_r2, edge);
-                h_r2d = (double)h_r2;
-              }
-            }
+            if (member && seen > K) shrink(seen, h_r2);
+            h_r2d = (double)h_r2;
             R2b = fminf(R2b, warp_max(member ? h_r2 : 0.f) * (1.0f + 4.0f * kEps) + 1e-37f);
           }
           nr = 0;
@@ -639,6 +678,13 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
           } else {
             tl = (double)__int_as_float((kHistBase + bb - 1) << 21) * R2d * (1.0 - 8.0 * kEpsD);
             th = (double)__int_as_float((kHistBase + bb) << 21) * R2d * (1.0 + 8.0 * kEpsD);
+          }
+          if (a.nlists) {
+            // the recorded list holds every candidate with d2 <= h_fin (fp32
+            // prefilter, 2^-20 guard): clip the bracket to that
+            th = fmin(th, (double)h_fin * (1.0 - 4.0 * kEpsD));
+            if (th < tl) th = tl;
+            a.ncount[p] = ne;
           }
           a.t_lo[p] = tl;
           a.t_hi[p] = th;

@@ -1,0 +1,580 @@
+// One warp per target: neighbour search, exact K-th selection and density in
+// a single persistent kernel (the default pass).
+//
+// For target i (reference compute_density_pass, density.py:286-413, with the
+// todo loop replaced by a radius that only has to bound the K-th neighbour):
+//   walk   the search tree with the target's own radius R: 32 pre-order nodes
+//          per step (one per lane, skip pointers), every needed cell of the step
+//          streamed at once, 32 candidates per step (one per lane);
+//   count  each accepted candidate into a per-lane-column d2 histogram
+//          (4 bins/octave) and append it to a shared-memory neighbour list;
+//          once more than K are counted the radius shrinks to the upper edge
+//          of the bin holding the K-th (adaptive shrink) and the list is
+//          compacted to the new radius;
+//   grow   fewer than K others within R: R grows and the walk restarts;
+//   select the bin of the K-th gives a bracket [t_lo, t_hi]; exact fp64 d2
+//          (octree.py:211-214 arithmetic) for list entries that may fall in
+//          it, count below, rank inside -> d2_K (h = sqrt(d2_K), density.py:226-245);
+//   sum    rho = sum over list entries within h of m_j W(r/h), self included
+//          (density.py:160-171, 249-261; kernel.py:30-45), fp32 per pair or
+//          fp64 term-for-term (dens64 / fp64 path).
+// Targets the list cannot serve (overflow, bracket edge cases) keep their
+// bracket in ST_NEED_BAND for the walking select/density passes (sph_pass.cu).
+#include "sph_internal.cuh"
+
+namespace sph {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWarps = 4;
+constexpr int kHistOctaves = 12;
+constexpr int kHistBase = (127 - kHistOctaves) << 2;
+constexpr int NB_HIST = kHistOctaves * 4 + 2;
+constexpr int kHistStride = 33;  // padded rows: the column sums are bank-conflict free
+constexpr int kInCap = 64;       // in-bracket entries (aliases the histogram)
+constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
+constexpr double kEpsD = 9.5367431640625e-07;
+constexpr unsigned kNaNf = 0x7fc00000u;
+
+struct alignas(32) D4 { double x, y, z, m; };
+template <bool F32> struct Pos;
+template <> struct Pos<true> { using T = float4; };
+template <> struct Pos<false> { using T = D4; };
+
+constexpr int kStack = 768;  // traversal stack (node ids) per warp
+
+__host__ __device__ constexpr int warp_smem_bytes(int cap) {
+  return NB_HIST * kHistStride * 4 + cap * 8 + 2 * 32 * 4 + kStack * 4;
+}
+
+__device__ __forceinline__ float wmax(float v) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int hist_bin(float x) {  // x = d2 / R^2
+  return min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int cap, int *fallbacks) {
+  using PT = typename Pos<F32>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char *wbase = smem_raw + wib * warp_smem_bytes(cap);
+  unsigned *hist = reinterpret_cast<unsigned *>(wbase);
+  double *inb = reinterpret_cast<double *>(wbase);  // after the histogram is read
+  uint2 *list = reinterpret_cast<uint2 *>(wbase + NB_HIST * kHistStride * 4);
+  int *spfx = reinterpret_cast<int *>(wbase + NB_HIST * kHistStride * 4 + cap * 8);
+  int *sbase = spfx + 32;
+  int *stk = sbase + 32;
+  const PT *__restrict__ pos = reinterpret_cast<const PT *>(a.pos);
+  const float4 *__restrict__ nlo = a.tree.nlo;
+  const float4 *__restrict__ nhi = a.tree.nhi;
+  const int n_nodes = a.tree.n_nodes;
+  const int n = a.n;
+  const int K = a.k;
+  const int center = a.periodic ? 13 : 0;
+  const float boxf = (float)a.box;
+  const bool f32sum = F32 && !a.dens64;
+  const double norm = a.kernel_kind == 0 ? kWc6Norm : kM4Norm;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned long long tests = 0, accepted = 0;
+  int fb_over = 0, fb_bracket = 0;
+
+  const int count = a.list ? *a.list_count : a.static_count;
+  for (;;) {
+    int ti = 0;
+    if (lane == 0) ti = atomicAdd(a.work_counter, 1);
+    ti = __shfl_sync(FULL, ti, 0);
+    if (ti >= count) break;
+    const int p = a.list ? (int)a.list[ti] : ti;
+    if (a.state[p] != ST_NEED_HIST) continue;
+
+    double tx, ty, tz;
+    {
+      const PT t = pos[p];
+      tx = t.x; ty = t.y; tz = t.z;
+    }
+    const float fx = (float)tx, fy = (float)ty, fz = (float)tz;
+    float R = a.radius[p];
+    if (!(R > 0.f)) R = 1e-30f;
+    const float slack0 = F32 ? 0.f : fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))) * 1.2e-7f;
+    // squared per-axis gap from x_i - s*box (s = -1, 0, +1) to the root box
+    float gsq[3][3];
+    {
+      const float4 l4 = nlo[0], h4 = nhi[0];
+      const double t3[3] = {tx, ty, tz};
+      const float lo3[3] = {l4.x, l4.y, l4.z}, hi3[3] = {h4.x, h4.y, h4.z};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int si = 0; si < 3; ++si) {
+          const int sv = si - 1;
+          const float q = (float)(t3[d] - sv * a.box);
+          const float sl = sv ? boxf * 4.8e-7f : slack0;
+          const float g = fmaxf(fmaxf(lo3[d] - q, q - hi3[d]) - sl, 0.f);
+          gsq[d][si] = (a.periodic || sv == 0) ? g * g : INFINITY;
+        }
+      }
+    }
+
+    for (;;) {  // grow loop
+      const float hR2 = R * R;
+      const float h_inv = 1.0f / hR2;
+      float h_r2 = hR2;  // current acceptance radius^2 (shrinks)
+      for (int bb = lane; bb < NB_HIST * kHistStride; bb += 32) hist[bb] = 0u;
+      int seen = 0, seen_shrunk = 0;  // warp-uniform: counted candidates (self included)
+      int ne = 0;                     // warp-uniform: list entries
+      bool over = false;              // list overflowed: no list-based select
+      bool stack_over = false;        // traversal stack overflowed: bundle passes instead
+      __syncwarp();
+
+      // adaptive shrink from the column histogram; compacts the list
+      auto shrink = [&]() {
+        unsigned c0 = 0, c1 = 0;
+#pragma unroll 4
+        for (int c = 0; c < 32; ++c) {
+          c0 += hist[lane * kHistStride + c];
+          if (lane + 32 < NB_HIST) c1 += hist[(lane + 32) * kHistStride + c];
+        }
+        // inclusive prefix over bins 0..31 then 32..NB_HIST-1
+        unsigned s0 = c0, s1 = c1;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v0 = __shfl_up_sync(FULL, s0, o), v1 = __shfl_up_sync(FULL, s1, o);
+          if (lane >= o) { s0 += v0; s1 += v1; }
+        }
+        s1 += __shfl_sync(FULL, s0, 31);
+        const unsigned m0 = __ballot_sync(FULL, (int)s0 > K);
+        const unsigned m1 = __ballot_sync(FULL, (int)s1 > K && lane + 32 < NB_HIST);
+        const int bb = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : NB_HIST);
+        if (bb < NB_HIST - 1) {
+          const float edge = __int_as_float((kHistBase + bb) << 21) * hR2 * (1.0f + 4.0f * kEps);
+          if (edge < h_r2) {
+            h_r2 = edge;
+            if (!over && ne > K) {
+              // in-place warp compaction of the list to the new radius
+              int w = 0;
+              for (int i0 = 0; i0 < ne; i0 += 32) {
+                const int i = i0 + lane;
+                uint2 e = make_uint2(0u, kNaNf);
+                if (i < ne) e = list[i];
+                const bool keep = i < ne && __uint_as_float(e.y) <= edge;
+                const unsigned km = __ballot_sync(FULL, keep);
+                __syncwarp();
+                if (keep) list[w + __popc(km & lt_mask)] = e;
+                w += __popc(km);
+                __syncwarp();
+              }
+              ne = w;
+            }
+          }
+        }
+        seen_shrunk = seen;
+      };
+
+      // periodic images: shifts s in {0,-1,+1}^3, the unshifted one first (its
+      // neighbours shrink the radius early); a shift is searched only if the
+      // root box, seen from x_i - s*box, comes within the current radius
+      const int ns = a.periodic ? 3 : 1;
+      for (int ix = 0; ix < ns; ++ix) {
+      const int sx = ix == 0 ? 0 : (ix == 1 ? -1 : 1);
+      const float gxs = sx == 0 ? gsq[0][1] : (sx < 0 ? gsq[0][0] : gsq[0][2]);
+      if (gxs * (1.0f - 4.0f * kEps) > h_r2) continue;
+      for (int iy = 0; iy < ns; ++iy) {
+      const int sy = iy == 0 ? 0 : (iy == 1 ? -1 : 1);
+      const float gys = sy == 0 ? gsq[1][1] : (sy < 0 ? gsq[1][0] : gsq[1][2]);
+      if ((gxs + gys) * (1.0f - 4.0f * kEps) > h_r2) continue;
+      for (int iz = 0; iz < ns; ++iz) {
+        const int sz = iz == 0 ? 0 : (iz == 1 ? -1 : 1);
+        const float gzs = sz == 0 ? gsq[2][1] : (sz < 0 ? gsq[2][0] : gsq[2][2]);
+        if ((gxs + gys + gzs) * (1.0f - 4.0f * kEps) > h_r2) continue;
+        const int sidx = a.periodic ? (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1) : 0;
+        const bool shifted = (sx | sy | sz) != 0;
+        const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
+        // the target in the tree frame of this shift (x_i - s*box), plus slack
+        const float pqx = sx ? (float)(tx - dsx) : fx, pqy = sy ? (float)(ty - dsy) : fy,
+                    pqz = sz ? (float)(tz - dsz) : fz;
+        const float pslack = shifted ? boxf * 4.8e-7f : slack0;
+        // fp32 image arithmetic: x_j - box exact when it matters (Sterbenz); for a
+        // +box shift the target moves instead (x_i - box)
+        const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
+        const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
+
+        // ---- warp traversal: pop up to 32 nodes (one per lane), test, push the
+        // children of hit internal nodes (child lists), stream the hit cells ----
+        // unshifted: start at the lowest ancestor of the target's cell whose box
+        // holds the whole search sphere (no cell outside it can be within R)
+        int start = 0;
+        if (!shifted && a.tree.parent) {
+          const float rr = sqrtf(h_r2) * (1.0f + 8.0f * kEps) + pslack;
+          int c = a.tree.cellof[p];
+          while (c > 0) {
+            const float4 l4 = nlo[c], h4 = nhi[c];
+            if (l4.x <= pqx - rr && pqx + rr <= h4.x && l4.y <= pqy - rr && pqy + rr <= h4.y && l4.z <= pqz - rr &&
+                pqz + rr <= h4.z)
+              break;
+            c = a.tree.parent[c];
+          }
+          start = c;
+        }
+        int top = 0;
+        if (lane == 0) stk[0] = start;
+        top = 1;
+        __syncwarp();
+        while (top > 0) {
+          const int cnt = min(top, 32);
+          top -= cnt;
+          const bool act = lane < cnt;
+          const int node = act ? stk[top + lane] : 0;
+          __syncwarp();
+          bool hit = false, is_cell = false;
+          int my_start = 0, my_end = 0;
+          int4 k0 = make_int4(-1, -1, -1, -1), k1 = k0;
+          if (act) {
+            const float4 l4 = nlo[node], h4 = nhi[node];
+            is_cell = __float_as_int(l4.w) == node + 1;
+            const float gx = fmaxf(fmaxf(l4.x - pqx, pqx - h4.x) - pslack, 0.f);
+            const float gy = fmaxf(fmaxf(l4.y - pqy, pqy - h4.y) - pslack, 0.f);
+            const float gz = fmaxf(fmaxf(l4.z - pqz, pqz - h4.z) - pslack, 0.f);
+            hit = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= h_r2;
+            if (hit) {
+              if (is_cell) {
+                my_start = __float_as_int(h4.w);
+                my_end = node + 1 < n_nodes ? __float_as_int(nhi[node + 1].w) : n;
+              } else {
+                const int4 *kp = reinterpret_cast<const int4 *>(a.tree.kids) + 2 * node;
+                k0 = kp[0];
+                k1 = kp[1];
+              }
+            }
+          }
+          // push children (in order: the last pushed is popped first)
+          const int nk = (hit && !is_cell) ? (k0.x >= 0) + (k0.y >= 0) + (k0.z >= 0) + (k0.w >= 0) + (k1.x >= 0) +
+                                                 (k1.y >= 0) + (k1.z >= 0) + (k1.w >= 0)
+                                           : 0;
+          int kin = nk;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, kin, o);
+            if (lane >= o) kin += v;
+          }
+          const int ktot = __shfl_sync(FULL, kin, 31);
+          if (top + ktot > kStack) { stack_over = true; break; }
+          if (nk) {
+            int o = top + kin - nk;
+            const int kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              if (kk[c] >= 0) stk[o++] = kk[c];
+          }
+          top += ktot;
+          const bool need = hit && is_cell;
+          const int len = need ? my_end - my_start : 0;
+          int incl = len;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int total = __shfl_sync(FULL, incl, 31);
+          __syncwarp();
+          if (total == 0) continue;
+          spfx[lane] = incl;
+          sbase[lane] = my_start - (incl - len);
+          __syncwarp();
+
+          // ---- stream the window's candidates, 32 per step ----
+          for (int c0 = 0; c0 < total; c0 += 32) {
+            const int s = c0 + lane;
+            bool in = false;
+            int j = 0;
+            float af = 0.f;
+            if (s < total) {
+              int r = 0;
+#pragma unroll
+              for (int step = 16; step; step >>= 1)
+                if (spfx[r + step - 1] <= s) r += step;
+              j = sbase[r] + s;
+              const PT c = pos[j];
+              if constexpr (F32) {
+                float dx, dy, dz;
+                if (shifted) {
+                  dx = (c.x + csx) - tfx; dy = (c.y + csy) - tfy; dz = (c.z + csz) - tfz;
+                } else {
+                  dx = c.x - fx; dy = c.y - fy; dz = c.z - fz;
+                }
+                af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                in = af <= h_r2;
+              } else {
+                double cx = c.x, cy = c.y, cz = c.z;
+                if (shifted) { cx = __dadd_rn(cx, dsx); cy = __dadd_rn(cy, dsy); cz = __dadd_rn(cz, dsz); }
+                const double ad = exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
+                in = ad <= (double)h_r2;
+                af = (float)ad;
+              }
+              if (in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + lane], 1u);
+            }
+            if (lane == 0) tests += (unsigned long long)min(32, total - c0);
+            bool lst = in;
+            int nin = __popc(__ballot_sync(FULL, in));
+            seen += nin;
+            if (!over && ne + nin > cap) {
+              // full list: shrink first (the histogram already holds this step)
+              if (seen > K + 1) {
+                shrink();
+                if (lst && !(af <= h_r2)) lst = false;  // counted, beyond the new radius
+              }
+              if (ne + __popc(__ballot_sync(FULL, lst)) > cap) over = true;
+            }
+            if (!over) {
+              const unsigned lm = __ballot_sync(FULL, lst);
+              if (lst) list[ne + __popc(lm & lt_mask)] = make_uint2((unsigned)j | ((unsigned)sidx << 27), __float_as_uint(af));
+              ne += __popc(lm);
+            }
+          }
+          __syncwarp();
+          if (seen > K + 1 && seen - seen_shrunk >= (K >> 2)) shrink();
+        }
+        if (stack_over) break;
+      }
+      if (stack_over) break;
+      }
+      if (stack_over) break;
+      }
+      __syncwarp();
+      if (stack_over) break;  // leave the target to the bundle passes (state NEED_HIST)
+
+      // ---- counted enough? ----
+      const int others = seen - 1;  // the target itself (d2 = 0)
+      if (others < K) {
+        if (R >= a.rmax) {
+          if (lane == 0) {
+            a.state[p] = ST_UNREACHABLE;
+            a.d2k[p] = INFINITY;
+          }
+          break;
+        }
+        float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.15f : 2.f;
+        f = fminf(fmaxf(f, 1.26f), 2.5f);
+        R = fminf(R * f, a.rmax);
+        continue;
+      }
+
+      // ---- bracket of the K-th from the histogram (bin sums per lane) ----
+      double tl, th;
+      {
+        unsigned c0 = 0, c1 = 0;
+#pragma unroll 4
+        for (int c = 0; c < 32; ++c) {
+          c0 += hist[lane * kHistStride + c];
+          if (lane + 32 < NB_HIST) c1 += hist[(lane + 32) * kHistStride + c];
+        }
+        if (lane == 0) c0 -= 1u;  // self, bin 0
+        unsigned s0 = c0, s1 = c1;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v0 = __shfl_up_sync(FULL, s0, o), v1 = __shfl_up_sync(FULL, s1, o);
+          if (lane >= o) { s0 += v0; s1 += v1; }
+        }
+        s1 += __shfl_sync(FULL, s0, 31);
+        const unsigned m0 = __ballot_sync(FULL, (int)s0 >= K);
+        const unsigned m1 = __ballot_sync(FULL, (int)s1 >= K && lane + 32 < NB_HIST);
+        const int bb = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : NB_HIST - 1);
+        const double R2d = (double)hR2;
+        if (bb == 0) {
+          tl = 0.0;
+          th = (double)__int_as_float(kHistBase << 21) * R2d * (1.0 + 8.0 * kEpsD);
+        } else if (bb >= NB_HIST - 1) {
+          tl = R2d * (1.0 - 8.0 * kEpsD);
+          th = R2d * (1.0 + 8.0 * kEpsD);
+        } else {
+          tl = (double)__int_as_float((kHistBase + bb - 1) << 21) * R2d * (1.0 - 8.0 * kEpsD);
+          th = (double)__int_as_float((kHistBase + bb) << 21) * R2d * (1.0 + 8.0 * kEpsD);
+        }
+        // the list holds every candidate with d2 <= h_r2 (2^-20 guard)
+        th = fmin(th, (double)h_r2 * (1.0 - 4.0 * kEpsD));
+        if (th < tl) th = tl;
+      }
+      __syncwarp();
+
+      auto fallback = [&]() {
+        if (lane == 0) {
+          a.t_lo[p] = tl;
+          a.t_hi[p] = th;
+          a.radius[p] = R;
+          a.state[p] = ST_NEED_BAND;
+        }
+      };
+      if (over) { ++fb_over; fallback(); break; }
+
+      // ---- exact count below the bracket, collect the bracket ----
+      const float lo_f = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
+      const float hi_f = __double2float_ru(th * (1.0 + kEpsD)) + 1e-37f;
+      auto image_d2 = [&](const PT &c, int sidx) {
+        double cx = c.x, cy = c.y, cz = c.z;
+        if (a.periodic && sidx != 13) {
+          const int sx = sidx / 9 - 1, sy = (sidx / 3) % 3 - 1, sz = sidx % 3 - 1;
+          cx = __dadd_rn(cx, sx * a.box); cy = __dadd_rn(cy, sy * a.box); cz = __dadd_rn(cz, sz * a.box);
+        }
+        return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
+      };
+      int below = 0, n_in = 0;
+      for (int i0 = 0; i0 < ne; i0 += 32) {
+        const int i = i0 + lane;
+        bool inb_ = false;
+        double e = 0.0;
+        if (i < ne) {
+          const uint2 le = list[i];
+          const float af = __uint_as_float(le.y);
+          const int j = (int)(le.x & ((1u << 27) - 1u));
+          const int sidx = (int)(le.x >> 27);
+          if (!(j == p && sidx == center)) {
+            if (af < lo_f) {
+              ++below;
+            } else if (af <= hi_f) {
+              e = image_d2(pos[j], sidx);
+              if (e < tl) ++below;
+              else if (e <= th) inb_ = true;
+            }
+          }
+        }
+        const unsigned bm = __ballot_sync(FULL, inb_);
+        if (inb_ && n_in + __popc(bm & lt_mask) < kInCap) inb[n_in + __popc(bm & lt_mask)] = e;
+        n_in += __popc(bm);
+      }
+      __syncwarp();
+      below = (int)__reduce_add_sync(FULL, (unsigned)below);
+      const int r = K - below;  // 1-based rank of the K-th inside the bracket
+      if (n_in > kInCap || r < 1 || r > n_in) { ++fb_bracket; fallback(); break; }
+
+      // ---- the r-th smallest of the bracket ----
+      double v = INFINITY;
+      for (int i = lane; i < n_in; i += 32) {
+        const double ei = inb[i];
+        int less = 0, eq = 0;
+        for (int jj = 0; jj < n_in; ++jj) {
+          const double ej = inb[jj];
+          less += ej < ei;
+          eq += ej == ei;
+        }
+        if (less < r && r <= less + eq) v = ei;
+      }
+      for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+      const double d2k = v;
+
+      // ---- density over the list entries within h ----
+      double rho = 0.0;
+      if (d2k > 0.0) {
+        double accd = 0.0;
+        float accf = 0.f;
+        const double hh = __dsqrt_rn(d2k);
+        const double norm_h3 = __ddiv_rn(norm, __dmul_rn(__dmul_rn(hh, hh), hh));
+        const float d2k_f = __double2float_ru(d2k * (1.0 + kEpsD));
+        const float inv_h = (float)(1.0 / hh);
+        for (int i = lane; i < ne; i += 32) {
+          const uint2 le = list[i];
+          const float af = __uint_as_float(le.y);
+          if (!(af < d2k_f)) continue;
+          ++accepted;
+          const int j = (int)(le.x & ((1u << 27) - 1u));
+          const PT c = pos[j];
+          if (f32sum) {
+            if constexpr (F32) {
+              const float rr = af > 0.f ? af * rsqrtf(af) : 0.f;
+              const float q = rr * inv_h;
+              const float wv = a.kernel_kind == 0 ? wc6_profile_f(q) : m4_profile_f(q);
+              if (q < 1.f) accf = fmaf(c.w, wv, accf);
+            }
+          } else {
+            const double e = image_d2(c, (int)(le.x >> 27));
+            if (e < d2k) {
+              const double r_ = __dsqrt_rn(e);
+              double wv;
+              if (a.kernel_kind == 0) {
+                wv = wc6_lowered(r_, hh, norm_h3);
+              } else {
+                const double q = __ddiv_rn(r_, hh);
+                wv = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+              }
+              double mj;
+              if constexpr (F32) mj = a.mass64[j]; else mj = c.m;
+              accd = __dadd_rn(accd, __dmul_rn(mj, wv));
+            }
+          }
+        }
+        for (int o = 16; o; o >>= 1) {
+          accd += __shfl_xor_sync(FULL, accd, o);
+          accf += __shfl_xor_sync(FULL, accf, o);
+        }
+        rho = f32sum ? __dmul_rn(norm_h3, (double)accf) : accd;
+      }
+      if (lane == 0) {
+        a.d2k[p] = d2k;
+        a.rho[p] = rho;
+        a.radius[p] = R;
+        a.state[p] = ST_FINAL;
+      }
+      break;
+    }
+  }
+  // statistics
+  for (int o = 16; o; o >>= 1) accepted += __shfl_xor_sync(FULL, accepted, o);
+  if (lane == 0) {
+    atomicAdd(&a.stats[0], tests);
+    atomicAdd(&a.stats[1], accepted);
+    if (fallbacks) {
+      if (fb_over) atomicAdd(fallbacks, fb_over);
+      if (fb_bracket) atomicAdd(fallbacks + 1, fb_bracket);
+    }
+  }
+}
+
+// children of each internal node (pre-order indices, -1 padded): k+1, then
+// the skip pointer chain up to the node's own skip
+// and the parent of each node; cellof[i] = the cell holding sorted particle i
+__global__ void k_kids(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi, int n_nodes, int n,
+                       int *__restrict__ kids, int *__restrict__ parent, int *__restrict__ cellof) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_nodes) return;
+  if (k == 0) parent[0] = -1;
+  const int skip = __float_as_int(nlo[k].w);
+  int c = k + 1, i = 0;
+  if (skip != k + 1) {
+    while (c < skip && i < 8) {
+      kids[8 * k + i++] = c;
+      parent[c] = k;
+      c = __float_as_int(nlo[c].w);
+    }
+  } else {
+    const int s0 = __float_as_int(nhi[k].w);
+    const int e0 = k + 1 < n_nodes ? __float_as_int(nhi[k + 1].w) : n;
+    for (int j = s0; j < e0; ++j) cellof[j] = k;
+  }
+  for (; i < 8; ++i) kids[8 * k + i] = -1;
+}
+
+}  // namespace
+
+void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, int *kids, int *parent,
+                 int *cellof) {
+  k_kids<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, nhi, n_nodes, n, kids, parent, cellof);
+}
+
+int target_list_cap(int k) { return std::min(std::max(4 * k, 128), 1024); }
+
+void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms) {
+  const int smem = kWarps * warp_smem_bytes(cap);
+  int bps = 0;
+  if (f32) {
+    cudaFuncSetAttribute(k_target<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_target<true>, kWarps * 32, smem);
+    k_target<true><<<num_sms * std::max(bps, 1), kWarps * 32, smem, s>>>(a, cap, fallbacks);
+  } else {
+    cudaFuncSetAttribute(k_target<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_target<false>, kWarps * 32, smem);
+    k_target<false><<<num_sms * std::max(bps, 1), kWarps * 32, smem, s>>>(a, cap, fallbacks);
+  }
+}
+
+}  // namespace sph
