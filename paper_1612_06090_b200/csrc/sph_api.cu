@@ -84,7 +84,9 @@ struct sph_ctx {
   bool warp = false;   // SPH_WARP=1: the per-target kernel for every target (no bundle pass)
   bool hybrid = true;  // SPH_HYBRID=0: bundle histogram rounds until settled
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
-  int list_mult = 4;   // SPH_LISTCAP: neighbour-list capacity per target in units of K
+  int list_mult = 4;
+  int lshrink = 1;       // SPH_LSHRINK
+  float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
   DevBuf<uint2> nlists;
   DevBuf<int> kids, parent, cellof;
@@ -767,6 +769,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       a.nlists = ctx->nlists.p;
       a.ncount = ctx->ncount.p;
       a.ncap = (int)cap;
+      a.lshrink = ctx->lshrink;
+      a.lcompact = (int)(ctx->lcompact * k);
       use_lists = true;
     } else {
       cudaGetLastError();  // allocation failure: walk-based select/density instead
@@ -789,6 +793,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     t.tree.parent = ctx->parent.p;
     t.tree.cellof = ctx->cellof.p;
     t.list = ctx->list.p;
+    t.ncount = a.ncount;
     SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
     SPH_CK(ctx->qints.ensure(8));
     const int i = ctx->n_kev;
@@ -796,10 +801,19 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ctx->kev_mode[i] = MODE_HIST;
       cudaEventRecord(ctx->kev[2 * i], ctx->stream);
     }
-    launch_target(ctx->stream, compute_f32, t, target_list_cap(k), nullptr, ctx->num_sms);
+    SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+    launch_target(ctx->stream, compute_f32, t, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
     if (i < 64) {
       cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
       ctx->n_kev = i + 1;
+    }
+    if (ctx->debug) {
+      int fbk[2] = {0, 0}, nrem = 0;
+      cudaStreamSynchronize(ctx->stream);
+      cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&nrem, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[sph hybrid] %d targets to the per-target kernel; fall back: %d overflowed lists, %d bracket misses\n",
+              nrem, fbk[0], fbk[1]);
     }
     launches += 2;
     hist_rounds = 2;
@@ -817,6 +831,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   // ---- select (+ density) ----
   if (use_lists) {
     SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+    SPH_CK(cudaMemsetAsync(ctx->qints.p + 7, 0, sizeof(int), ctx->stream));
     const int i = ctx->n_kev;
     if (i < 64) {
       ctx->kev_mode[i] = MODE_BAND;
@@ -984,6 +999,8 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_WARP")) c->warp = v[0] == '1';
   if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
+  if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
+  if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);

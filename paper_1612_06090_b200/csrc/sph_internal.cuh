@@ -132,6 +132,8 @@ struct PassArgs {
   uint2 *nlists;
   int *ncount;              // entries recorded (> ncap: overflowed, list unusable)
   int ncap;
+  int lshrink;              // shrink after every candidate chunk (not only per flush)
+  int lcompact;             // compact the list at a shrink once it holds more entries than this
 };
 
 // arguments of the fused search/select/density kernel (sph_fused.cu)

@@ -20,6 +20,7 @@
 // A target whose list overflowed, or whose bracket does not hold the K-th
 // (fp32 histogram edge cases), stays in ST_NEED_BAND for the walking passes.
 #include "sph_internal.cuh"
+#include <cstdio>
 
 namespace sph {
 namespace {
@@ -36,7 +37,7 @@ template <> struct Pos<true> { using T = float4; };
 template <> struct Pos<false> { using T = D4; };
 
 template <bool F32, int EPL>
-__global__ void __launch_bounds__(kWarps * 32) k_lists(const PassArgs a, int *fallbacks) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_lists(const PassArgs a, int *fallbacks) {
   using PT = typename Pos<F32>::T;
   __shared__ double s_in[kWarps][kInCap];
   __shared__ int s_nin[kWarps];
@@ -154,50 +155,33 @@ __global__ void __launch_bounds__(kWarps * 32) k_lists(const PassArgs a, int *fa
           if (slot < kInCap) inb[slot] = e;
         }
       };
-      bool gat[EPL];
-      double ex[EPL], mw[EPL];
+      float mw[EPL];  // fp32 sums: the entry's mass (gathered once)
       if (slow) {
-#pragma unroll
-        for (int u = 0; u < EPL; ++u) gat[u] = false;
         for_entries([&](bool self, float af, const PT &c, int, int sidx) {
           ++tests;
           if (!(af <= hi_f)) return;
           classify(self, (!self && !(af < lo_f)) ? image_d2(c, sidx) : 0.0, af);
         });
       } else {
-        // fp32 d2 decides all but the entries near the bracket; each entry that
-        // may count for the density (d2 <= t_hi) is gathered here, once, with
-        // its mass and (fp64 sums / bracket) its exact d2
-        PT cg[EPL];
+        // fp32 d2 decides all but the entries near the bracket (exact fp64
+        // there); the fp32 sums gather each candidate mass here, once
+        const float *__restrict__ posf = reinterpret_cast<const float *>(a.pos);
 #pragma unroll
         for (int u = 0; u < EPL; ++u) {
           const float af = __uint_as_float(ev[u].y);
           tests += af == af;
-          gat[u] = af <= hi_f;
-          if (gat[u]) {
-            const int j = (int)(ev[u].x & ((1u << 27) - 1u));
-            cg[u] = pos[j];
-            if constexpr (F32) {
-              if (a.dens64) mw[u] = a.mass64[j];
-            }
-          }
+          mw[u] = 0.f;
+          if (f32sum && af <= hi_f) mw[u] = posf[4 * (size_t)(ev[u].x & ((1u << 27) - 1u)) + 3];
         }
 #pragma unroll
         for (int u = 0; u < EPL; ++u) {
-          if (gat[u]) {
-            const float af = __uint_as_float(ev[u].y);
+          const float af = __uint_as_float(ev[u].y);
+          if (af <= hi_f) {
             const int j = (int)(ev[u].x & ((1u << 27) - 1u));
             const int sidx = (int)(ev[u].x >> 27);
             const bool self = j == p && sidx == center;
-            if constexpr (F32) {
-              if (!a.dens64) mw[u] = (double)cg[u].w;
-            } else {
-              mw[u] = cg[u].m;
-            }
             const bool near = !self && !(af < lo_f);
-            const double e = (near || !f32sum) ? image_d2(cg[u], sidx) : 0.0;
-            ex[u] = e;
-            classify(self, e, af);
+            classify(self, near ? image_d2(pos[j], sidx) : 0.0, af);
           }
         }
       }
@@ -206,7 +190,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_lists(const PassArgs a, int *fa
       const int n_in = s_nin[wib];
       const int r = a.k - below;  // 1-based rank of the K-th inside the bracket
       if (n_in > kInCap) { ++fb_in; continue; }
-      if (r < 1 || r > n_in) { ++fb_r; continue; }
+      if (r < 1 || r > n_in) {
+        ++fb_r;
+        if (lane == 0 && a.dbg && atomicAdd(fallbacks + 3, 1) < 8)
+          printf("[lists miss] p=%d m=%d K=%d below=%d n_in=%d lo=%.9g hi=%.9g\n", p, m, a.k, below, n_in, lo, hi);
+        continue;
+      }
 
       // ---- 2. the r-th smallest of the bracket ----
       double v = INFINITY;
@@ -261,9 +250,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_lists(const PassArgs a, int *fa
 #pragma unroll
           for (int u = 0; u < EPL; ++u) {
             const float af = __uint_as_float(ev[u].y);
-            if (gat[u] && af < d2k_f) {
+            if (af < d2k_f) {
               ++accepted;
-              term(af, ex[u], mw[u]);
+              if (f32sum) {
+                term(af, 0.0, mw[u]);
+              } else {
+                const int j = (int)(ev[u].x & ((1u << 27) - 1u));
+                const PT c = pos[j];
+                term(af, image_d2(c, (int)(ev[u].x >> 27)), mass_of(c, j));
+              }
             }
           }
         }

@@ -250,7 +250,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
           if (edge < hr2) {
             hr2 = edge;
             h_fin = edge;
-            if (nl && ne > 2 * K && ne <= a.ncap) {
+            if (nl && ne > a.lcompact && ne <= a.ncap) {
               int w2 = 0;
               for (int i = 0; i < ne; ++i) {
                 const uint2 e = nl[i];
@@ -611,7 +611,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
               if constexpr (MODE == MODE_HIST) {
                 // list recording: shrink as soon as K/2 more were counted, so
                 // that the list stays near K entries
-                if (nl && member && seen > K && seen - seen_shrunk >= (K >> 1)) {
+                if (nl && a.lshrink && member && seen > K && seen - seen_shrunk >= (K >> 1)) {
                   shrink(seen, h_r2);
                   seen_shrunk = seen;
                 }

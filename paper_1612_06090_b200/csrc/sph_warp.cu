@@ -21,6 +21,7 @@
 // Targets the list cannot serve (overflow, bracket edge cases) keep their
 // bracket in ST_NEED_BAND for the walking select/density passes (sph_pass.cu).
 #include "sph_internal.cuh"
+#include <cstdio>
 
 namespace sph {
 namespace {
@@ -31,7 +32,7 @@ constexpr int kHistOctaves = 12;
 constexpr int kHistBase = (127 - kHistOctaves) << 2;
 constexpr int NB_HIST = kHistOctaves * 4 + 2;
 constexpr int kHistStride = 33;  // padded rows: the column sums are bank-conflict free
-constexpr int kInCap = 64;       // in-bracket entries (aliases the histogram)
+constexpr int kInCap = 256;      // in-bracket entries (aliases the histogram)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
 constexpr unsigned kNaNf = 0x7fc00000u;
@@ -404,6 +405,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
           a.t_hi[p] = th;
           a.radius[p] = R;
           a.state[p] = ST_NEED_BAND;
+          if (a.ncount) a.ncount[p] = 0x7fffffff;  // no recorded list: the walking select
         }
       };
       if (over) { ++fb_over; fallback(); break; }
@@ -446,7 +448,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
       __syncwarp();
       below = (int)__reduce_add_sync(FULL, (unsigned)below);
       const int r = K - below;  // 1-based rank of the K-th inside the bracket
-      if (n_in > kInCap || r < 1 || r > n_in) { ++fb_bracket; fallback(); break; }
+      if (n_in > kInCap || r < 1 || r > n_in) {
+        if (lane == 0 && a.dbg && fallbacks && atomicAdd(fallbacks + 2, 1) < 10)
+          printf("[target miss] p=%d ne=%d seen=%d K=%d below=%d n_in=%d tl=%.9g th=%.9g h_r2=%.9g R2=%.9g\n", p, ne,
+                 seen, K, below, n_in, tl, th, (double)h_r2, (double)hR2);
+        ++fb_bracket;
+        fallback();
+        break;
+      }
 
       // ---- the r-th smallest of the bracket ----
       double v = INFINITY;
