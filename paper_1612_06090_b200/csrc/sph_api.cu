@@ -81,11 +81,12 @@ struct sph_ctx {
   bool debug = false;
   bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
   bool v3 = false;     // SPH_V3=1: walk-once / sweep-narrow kernels (sph_knn.cu, experimental)
-  bool warp = false;   // SPH_WARP=1: the per-target kernel for every target (no bundle pass)
+  bool warp = true;    // SPH_WARP=0: bundle histogram pass first (SPH_HYBRID) or bundle rounds
   bool hybrid = true;  // SPH_HYBRID=0: bundle histogram rounds until settled
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
+  int tshrink = 2;       // SPH_TSHRINK
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
   DevBuf<uint2> nlists;
@@ -366,6 +367,7 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.task_count = ctx->ints.p + 4;
   a.member_cursor = ctx->ints.p + 5;
   a.shortcut = ctx->shortcut;
+  a.tshrink = ctx->tshrink;
   if (ctx->debug && ctx->dbg.ensure(8 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
   return a;
 }
@@ -554,6 +556,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   a.tree.kids = ctx->kids.p;
   a.tree.parent = ctx->parent.p;
   a.tree.cellof = ctx->cellof.p;
+  SPH_CK(ctx->ncount.ensure(n));
+  a.ncount = ctx->ncount.p;
   SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
   {
     const int i = ctx->n_kev;
@@ -582,6 +586,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     for (int i = 0; i < 16; ++i) if (cnt[i]) fprintf(stderr, " %d:%d", i, cnt[i]);
     fprintf(stderr, "\n");
   }
+  // overflowed lists: collect again up to the bracket top
+  SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+  launch_target(ctx->stream, compute_f32, a, target_list_cap(k), nullptr, ctx->num_sms, true);
+  ++launches;
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);
@@ -852,6 +860,17 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
               fbk[0], fbk[1], fbk[2]);
     }
     a.nlists = nullptr;
+    if (ctx->hybrid && ctx->kids.p) {
+      // overflowed lists (bundle pass or per-target kernel): collect up to the bracket top
+      PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
+      t.tree.kids = ctx->kids.p;
+      t.tree.parent = ctx->parent.p;
+      t.tree.cellof = ctx->cellof.p;
+      t.ncount = ctx->ncount.p;
+      SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
+      launch_target(ctx->stream, compute_f32, t, target_list_cap(k), nullptr, ctx->num_sms, true);
+      ++launches;
+    }
   }
   rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
   if (rc) return rc;
@@ -1000,6 +1019,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
+  if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);

@@ -134,6 +134,7 @@ struct PassArgs {
   int ncap;
   int lshrink;              // shrink after every candidate chunk (not only per flush)
   int lcompact;             // compact the list at a shrink once it holds more entries than this
+  int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
 };
 
 // arguments of the fused search/select/density kernel (sph_fused.cu)
@@ -230,7 +231,8 @@ void launch_lists(cudaStream_t s, int f32, const PassArgs &a, int *fallbacks, in
 int lists_max_cap();
 // fused per-target search + select + density (sph_warp.cu)
 int target_list_cap(int k);
-void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms);
+void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,
+                   bool collect = false);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, int *kids, int *parent,
                  int *cellof);
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_lists(const PassArgs a, int 
       m_l = a.ncount[pl];
       if (m_l > a.ncap || m_l > 32 * EPL) {
         ++fb;
+        if (m_l <= 0x7ffffffd) a.ncount[pl] = 0x7fffffff;  // overflowed: the collect pass (sph_warp.cu)
       } else {
         want = true;
         lo_l = a.t_lo[pl];

@@ -22,6 +22,7 @@
 // bracket in ST_NEED_BAND for the walking select/density passes (sph_pass.cu).
 #include "sph_internal.cuh"
 #include <cstdio>
+#include <cstdlib>
 
 namespace sph {
 namespace {
@@ -31,7 +32,7 @@ constexpr int kWarps = 4;
 constexpr int kHistOctaves = 12;
 constexpr int kHistBase = (127 - kHistOctaves) << 2;
 constexpr int NB_HIST = kHistOctaves * 4 + 2;
-constexpr int kHistStride = 33;  // padded rows: the column sums are bank-conflict free
+constexpr int kHistStride = 17;  // words per bin row: 16-bit counters, two lanes per word (odd: conflict-free row sums)
 constexpr int kInCap = 256;      // in-bracket entries (aliases the histogram)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
@@ -42,23 +43,24 @@ template <bool F32> struct Pos;
 template <> struct Pos<true> { using T = float4; };
 template <> struct Pos<false> { using T = D4; };
 
-constexpr int kStack = 768;  // traversal stack (node ids) per warp
+#ifndef SPH_TARGET_MINB
+#define SPH_TARGET_MINB 7
+#endif
+constexpr int kStack = 448;  // traversal stack (node ids) per warp
 
 __host__ __device__ constexpr int warp_smem_bytes(int cap) {
   return NB_HIST * kHistStride * 4 + cap * 8 + 2 * 32 * 4 + kStack * 4;
 }
 
-__device__ __forceinline__ float wmax(float v) {
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
-  return v;
-}
 
 __device__ __forceinline__ int hist_bin(float x) {  // x = d2 / R^2
   return min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
 }
 
-template <bool F32>
-__global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int cap, int *fallbacks) {
+// COLLECT: second instance for the targets whose list overflowed in the main
+// kernel: one walk with the radius of the bracket top t_hi, list only
+template <bool F32, bool COLLECT>
+__global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const PassArgs a, int cap, int *fallbacks) {
   using PT = typename Pos<F32>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -85,13 +87,31 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
   int fb_over = 0, fb_bracket = 0;
 
   const int count = a.list ? *a.list_count : a.static_count;
+  // work in chunks of CH targets per atomic (the collect instance scans sparse
+  // targets: whole warps of them)
+  constexpr int CH = COLLECT ? 32 : 1;
+  unsigned pend = 0u;
+  int cbase = 0;
   for (;;) {
-    int ti = 0;
-    if (lane == 0) ti = atomicAdd(a.work_counter, 1);
-    ti = __shfl_sync(FULL, ti, 0);
-    if (ti >= count) break;
+    if (!pend) {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(a.work_counter, CH);
+      t0 = __shfl_sync(FULL, t0, 0);
+      if (t0 >= count) break;
+      cbase = t0;
+      const int q = t0 + lane;
+      bool want = false;
+      if (lane < CH && q < count) {
+        const int pq = a.list ? (int)a.list[q] : q;
+        if constexpr (COLLECT) want = a.state[pq] == ST_NEED_BAND && a.ncount[pq] == 0x7fffffff;
+        else want = a.state[pq] == ST_NEED_HIST;
+      }
+      pend = __ballot_sync(FULL, want);
+      if (!pend) continue;
+    }
+    const int ti = cbase + __ffs(pend) - 1;
+    pend &= pend - 1u;
     const int p = a.list ? (int)a.list[ti] : ti;
-    if (a.state[p] != ST_NEED_HIST) continue;
 
     double tx, ty, tz;
     {
@@ -122,23 +142,29 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
     }
 
     for (;;) {  // grow loop
-      const float hR2 = R * R;
+      const float hR2 = COLLECT ? (float)(__double2float_ru(a.t_hi[p] * (1.0 + kEpsD)) + 1e-37f) : R * R;
       const float h_inv = 1.0f / hR2;
       float h_r2 = hR2;  // current acceptance radius^2 (shrinks)
-      for (int bb = lane; bb < NB_HIST * kHistStride; bb += 32) hist[bb] = 0u;
+      if (!COLLECT)
+        for (int bb = lane; bb < NB_HIST * kHistStride; bb += 32) hist[bb] = 0u;
       int seen = 0, seen_shrunk = 0;  // warp-uniform: counted candidates (self included)
       int ne = 0;                     // warp-uniform: list entries
       bool over = false;              // list overflowed: no list-based select
       bool stack_over = false;        // traversal stack overflowed: bundle passes instead
+      int cand = 0;                   // candidates streamed (bounds the 16-bit histogram counters)
       __syncwarp();
 
       // adaptive shrink from the column histogram; compacts the list
       auto shrink = [&]() {
         unsigned c0 = 0, c1 = 0;
 #pragma unroll 4
-        for (int c = 0; c < 32; ++c) {
-          c0 += hist[lane * kHistStride + c];
-          if (lane + 32 < NB_HIST) c1 += hist[(lane + 32) * kHistStride + c];
+        for (int c = 0; c < kHistStride - 1; ++c) {
+          const unsigned w0 = hist[lane * kHistStride + c];
+          c0 += (w0 & 0xffffu) + (w0 >> 16);
+          if (lane + 32 < NB_HIST) {
+            const unsigned w1 = hist[(lane + 32) * kHistStride + c];
+            c1 += (w1 & 0xffffu) + (w1 >> 16);
+          }
         }
         // inclusive prefix over bins 0..31 then 32..NB_HIST-1
         unsigned s0 = c0, s1 = c1;
@@ -178,6 +204,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
       // periodic images: shifts s in {0,-1,+1}^3, the unshifted one first (its
       // neighbours shrink the radius early); a shift is searched only if the
       // root box, seen from x_i - s*box, comes within the current radius
+      double tl = 0.0, th = 0.0;
+      if constexpr (COLLECT) {
+        tl = a.t_lo[p];
+        th = a.t_hi[p];
+      }
+      bool grow = false, done_unreach = false;
+      for (int pass = 0; pass < 1; ++pass) {
       const int ns = a.periodic ? 3 : 1;
       for (int ix = 0; ix < ns; ++ix) {
       const int sx = ix == 0 ? 0 : (ix == 1 ? -1 : 1);
@@ -220,57 +253,41 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
           }
           start = c;
         }
+        // the stack holds hit internal nodes; a step expands up to 4 of them,
+        // one child per lane (8 slots each), and tests the children's boxes
         int top = 0;
-        if (lane == 0) stk[0] = start;
-        top = 1;
-        __syncwarp();
-        while (top > 0) {
-          const int cnt = min(top, 32);
-          top -= cnt;
-          const bool act = lane < cnt;
-          const int node = act ? stk[top + lane] : 0;
+        bool first = true;  // the first step tests the start node itself (lane 0)
+        while (first || top > 0) {
+          int node = -1;
+          if (first) {
+            node = lane == 0 ? start : -1;
+            first = false;
+          } else {
+            const int np = min(top, 4);
+            top -= np;
+            const int pi = lane >> 3;
+            const int par = pi < np ? stk[top + pi] : -1;
+            if (par >= 0) node = a.tree.kids[8 * par + (lane & 7)];
+          }
           __syncwarp();
           bool hit = false, is_cell = false;
           int my_start = 0, my_end = 0;
-          int4 k0 = make_int4(-1, -1, -1, -1), k1 = k0;
-          if (act) {
+          if (node >= 0) {
             const float4 l4 = nlo[node], h4 = nhi[node];
             is_cell = __float_as_int(l4.w) == node + 1;
             const float gx = fmaxf(fmaxf(l4.x - pqx, pqx - h4.x) - pslack, 0.f);
             const float gy = fmaxf(fmaxf(l4.y - pqy, pqy - h4.y) - pslack, 0.f);
             const float gz = fmaxf(fmaxf(l4.z - pqz, pqz - h4.z) - pslack, 0.f);
             hit = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= h_r2;
-            if (hit) {
-              if (is_cell) {
-                my_start = __float_as_int(h4.w);
-                my_end = node + 1 < n_nodes ? __float_as_int(nhi[node + 1].w) : n;
-              } else {
-                const int4 *kp = reinterpret_cast<const int4 *>(a.tree.kids) + 2 * node;
-                k0 = kp[0];
-                k1 = kp[1];
-              }
+            if (hit && is_cell) {
+              my_start = __float_as_int(h4.w);
+              my_end = node + 1 < n_nodes ? __float_as_int(nhi[node + 1].w) : n;
             }
           }
-          // push children (in order: the last pushed is popped first)
-          const int nk = (hit && !is_cell) ? (k0.x >= 0) + (k0.y >= 0) + (k0.z >= 0) + (k0.w >= 0) + (k1.x >= 0) +
-                                                 (k1.y >= 0) + (k1.z >= 0) + (k1.w >= 0)
-                                           : 0;
-          int kin = nk;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, kin, o);
-            if (lane >= o) kin += v;
-          }
-          const int ktot = __shfl_sync(FULL, kin, 31);
-          if (top + ktot > kStack) { stack_over = true; break; }
-          if (nk) {
-            int o = top + kin - nk;
-            const int kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              if (kk[c] >= 0) stk[o++] = kk[c];
-          }
-          top += ktot;
+          const unsigned pm = __ballot_sync(FULL, hit && !is_cell);
+          if (top + __popc(pm) > kStack) { stack_over = true; break; }
+          if (hit && !is_cell) stk[top + __popc(pm & lt_mask)] = node;
+          top += __popc(pm);
           const bool need = hit && is_cell;
           const int len = need ? my_end - my_start : 0;
           int incl = len;
@@ -282,6 +299,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
           const int total = __shfl_sync(FULL, incl, 31);
           __syncwarp();
           if (total == 0) continue;
+          cand += total;
+          if (cand > (1 << 20)) { stack_over = true; break; }  // 16-bit counters: bundle passes
           spfx[lane] = incl;
           sbase[lane] = my_start - (incl - len);
           __syncwarp();
@@ -315,7 +334,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
                 in = ad <= (double)h_r2;
                 af = (float)ad;
               }
-              if (in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + lane], 1u);
+              if (!COLLECT && in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
             }
             if (lane == 0) tests += (unsigned long long)min(32, total - c0);
             bool lst = in;
@@ -323,7 +342,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
             seen += nin;
             if (!over && ne + nin > cap) {
               // full list: shrink first (the histogram already holds this step)
-              if (seen > K + 1) {
+              if (!COLLECT && seen > K + 1) {
                 shrink();
                 if (lst && !(af <= h_r2)) lst = false;  // counted, beyond the new radius
               }
@@ -336,7 +355,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
             }
           }
           __syncwarp();
-          if (seen > K + 1 && seen - seen_shrunk >= (K >> 2)) shrink();
+          if (!COLLECT && seen > K + 1 && seen - seen_shrunk >= (K >> a.tshrink)) shrink();
         }
         if (stack_over) break;
       }
@@ -345,7 +364,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
       if (stack_over) break;
       }
       __syncwarp();
-      if (stack_over) break;  // leave the target to the bundle passes (state NEED_HIST)
+      if (stack_over || COLLECT) break;
 
       // ---- counted enough? ----
       const int others = seen - 1;  // the target itself (d2 = 0)
@@ -355,22 +374,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
             a.state[p] = ST_UNREACHABLE;
             a.d2k[p] = INFINITY;
           }
-          break;
+          done_unreach = true;
+        } else {
+          float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.15f : 2.f;
+          f = fminf(fmaxf(f, 1.26f), 2.5f);
+          R = fminf(R * f, a.rmax);
+          grow = true;
         }
-        float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.15f : 2.f;
-        f = fminf(fmaxf(f, 1.26f), 2.5f);
-        R = fminf(R * f, a.rmax);
-        continue;
+        break;
       }
 
       // ---- bracket of the K-th from the histogram (bin sums per lane) ----
-      double tl, th;
       {
         unsigned c0 = 0, c1 = 0;
 #pragma unroll 4
-        for (int c = 0; c < 32; ++c) {
-          c0 += hist[lane * kHistStride + c];
-          if (lane + 32 < NB_HIST) c1 += hist[(lane + 32) * kHistStride + c];
+        for (int c = 0; c < kHistStride - 1; ++c) {
+          const unsigned w0 = hist[lane * kHistStride + c];
+          c0 += (w0 & 0xffffu) + (w0 >> 16);
+          if (lane + 32 < NB_HIST) {
+            const unsigned w1 = hist[(lane + 32) * kHistStride + c];
+            c1 += (w1 & 0xffffu) + (w1 >> 16);
+          }
         }
         if (lane == 0) c0 -= 1u;  // self, bin 0
         unsigned s0 = c0, s1 = c1;
@@ -398,6 +422,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
         if (th < tl) th = tl;
       }
       __syncwarp();
+      }  // pass loop
+      if (stack_over) break;  // leave the target to the bundle passes (state NEED_HIST)
+      if (done_unreach) break;
+      if (grow) continue;
 
       auto fallback = [&]() {
         if (lane == 0) {
@@ -405,7 +433,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_target(const PassArgs a, int ca
           a.t_hi[p] = th;
           a.radius[p] = R;
           a.state[p] = ST_NEED_BAND;
-          if (a.ncount) a.ncount[p] = 0x7fffffff;  // no recorded list: the walking select
+          // no usable list: the collect instance next, then the walking select
+          if (a.ncount) a.ncount[p] = COLLECT ? 0x7ffffffe : 0x7fffffff;
         }
       };
       if (over) { ++fb_over; fallback(); break; }
@@ -570,19 +599,27 @@ void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nod
   k_kids<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, nhi, n_nodes, n, kids, parent, cellof);
 }
 
-int target_list_cap(int k) { return std::min(std::max(4 * k, 128), 1024); }
+int target_list_cap(int k) {
+  static const int mult = getenv("SPH_TLISTCAP") ? atoi(getenv("SPH_TLISTCAP")) : 3;
+  return std::min(std::max(mult * k, 128), 1024);
+}
 
-void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms) {
+template <bool F32, bool COLLECT>
+void launch_target_t(cudaStream_t s, const PassArgs &a, int cap, int *fallbacks, int num_sms) {
   const int smem = kWarps * warp_smem_bytes(cap);
   int bps = 0;
+  cudaFuncSetAttribute(k_target<F32, COLLECT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_target<F32, COLLECT>, kWarps * 32, smem);
+  k_target<F32, COLLECT><<<num_sms * std::max(bps, 1), kWarps * 32, smem, s>>>(a, cap, fallbacks);
+}
+
+void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms, bool collect) {
   if (f32) {
-    cudaFuncSetAttribute(k_target<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_target<true>, kWarps * 32, smem);
-    k_target<true><<<num_sms * std::max(bps, 1), kWarps * 32, smem, s>>>(a, cap, fallbacks);
+    if (collect) launch_target_t<true, true>(s, a, cap, fallbacks, num_sms);
+    else launch_target_t<true, false>(s, a, cap, fallbacks, num_sms);
   } else {
-    cudaFuncSetAttribute(k_target<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_target<false>, kWarps * 32, smem);
-    k_target<false><<<num_sms * std::max(bps, 1), kWarps * 32, smem, s>>>(a, cap, fallbacks);
+    if (collect) launch_target_t<false, true>(s, a, cap, fallbacks, num_sms);
+    else launch_target_t<false, false>(s, a, cap, fallbacks, num_sms);
   }
 }
 
