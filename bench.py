@@ -306,11 +306,11 @@ def run_ours(args):
     total_particles = float(n_total.item())
     value = total_particles * k / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (the fused neighbour kernel) ----
+    # ---- roofline of the dominant kernel (k_target: per-target search + select + density) ----
     peak_ffma = float(L.sph_fp32_peak(ctx))
     t_k = kern["search"] + kern["select"] + kern["density"]
     ops = 6.0 * tests + 10.0 * accepted
-    dom = "fused"
+    dom = "k_target"
     achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
     peak = peak_ffma / 1e12
     traffic = None
@@ -328,7 +328,7 @@ def run_ours(args):
             "converged_particles_per_s": total_particles / (ms_max * 1e-3),
             "gpu_launches": launches // args.steps,
             "clocks": clk,
-            "roofline": {"bound": "fp32", "kernel": "k_fused (search+select+density)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "fp32", "kernel": "k_target (per-target search + exact select + density; + fallbacks)", "achieved": achieved, "peak": peak,
                          "unit": "Tops/s (fp32-pipe ops)", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
                          "peak_source": "measured FFMA issue rate on this B200 (sph_fp32_peak); MEASURED_PEAKS.json "

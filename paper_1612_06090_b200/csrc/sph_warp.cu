@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           __syncwarp();
           if (total == 0) continue;
           cand += total;
+          tests += (unsigned)total;
           if (cand > (1 << 20)) { stack_over = true; break; }  // 16-bit counters: bundle passes
           spfx[lane] = incl;
           sbase[lane] = my_start - (incl - len);
@@ -319,12 +320,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               j = sbase[r] + s;
               const PT c = pos[j];
               if constexpr (F32) {
-                float dx, dy, dz;
-                if (shifted) {
-                  dx = (c.x + csx) - tfx; dy = (c.y + csy) - tfy; dz = (c.z + csz) - tfz;
-                } else {
-                  dx = c.x - fx; dy = c.y - fy; dz = c.z - fz;
-                }
+                // unshifted: csx = 0 and tfx = fx, so this is c.x - fx exactly
+                const float dx = (c.x + csx) - tfx, dy = (c.y + csy) - tfy, dz = (c.z + csz) - tfz;
                 af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 in = af <= h_r2;
               } else {
@@ -336,7 +333,6 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               }
               if (!COLLECT && in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
             }
-            if (lane == 0) tests += (unsigned long long)min(32, total - c0);
             bool lst = in;
             int nin = __popc(__ballot_sync(FULL, in));
             seen += nin;
