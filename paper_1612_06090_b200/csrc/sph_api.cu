@@ -588,8 +588,15 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   // overflowed lists: collect again up to the bracket top
   SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-  launch_target(ctx->stream, compute_f32, a, target_list_cap(k), nullptr, ctx->num_sms, true);
+  SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+  launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms, true);
   ++launches;
+  if (ctx->debug) {
+    int fbk[2] = {0, 0};
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[sph collect] still to the walking select: %d overflowed lists, %d bracket misses\n", fbk[0], fbk[1]);
+  }
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);

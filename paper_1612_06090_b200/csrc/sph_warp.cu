@@ -205,9 +205,12 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       // neighbours shrink the radius early); a shift is searched only if the
       // root box, seen from x_i - s*box, comes within the current radius
       double tl = 0.0, th = 0.0;
+      float lo_c = -1.f;  // collect: candidates below the bracket are counted, not listed
+      int cbelow = 0;
       if constexpr (COLLECT) {
         tl = a.t_lo[p];
         th = a.t_hi[p];
+        lo_c = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
       }
       bool grow = false, done_unreach = false;
       for (int pass = 0; pass < 1; ++pass) {
@@ -334,6 +337,12 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               if (!COLLECT && in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
             }
             bool lst = in;
+            if constexpr (COLLECT) {
+              if (lst && af < lo_c && !(j == p && sidx == center)) {
+                ++cbelow;
+                lst = false;
+              }
+            }
             int nin = __popc(__ballot_sync(FULL, in));
             seen += nin;
             if (!over && ne + nin > cap) {
@@ -446,7 +455,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         }
         return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
       };
-      int below = 0, n_in = 0;
+      int below = cbelow, n_in = 0;
       for (int i0 = 0; i0 < ne; i0 += 32) {
         const int i = i0 + lane;
         bool inb_ = false;
@@ -473,6 +482,12 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       __syncwarp();
       below = (int)__reduce_add_sync(FULL, (unsigned)below);
       const int r = K - below;  // 1-based rank of the K-th inside the bracket
+      if (!COLLECT && n_in <= kInCap && r > n_in && R < a.rmax) {
+        // the K-th lies above the (clipped) list radius, at the very edge of
+        // R: search again with a slightly larger radius
+        R = fminf(R * 1.26f, a.rmax);
+        continue;
+      }
       if (n_in > kInCap || r < 1 || r > n_in) {
         if (lane == 0 && a.dbg && fallbacks && atomicAdd(fallbacks + 2, 1) < 10)
           printf("[target miss] p=%d ne=%d seen=%d K=%d below=%d n_in=%d tl=%.9g th=%.9g h_r2=%.9g R2=%.9g\n", p, ne,
@@ -496,6 +511,14 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       }
       for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
       const double d2k = v;
+      if constexpr (COLLECT) {
+        // the list held only the bracket: the density pass (sph_pass.cu) sums rho
+        if (lane == 0) {
+          a.d2k[p] = d2k;
+          a.state[p] = ST_DONE;
+        }
+        break;
+      }
 
       // ---- density over the list entries within h ----
       double rho = 0.0;
