@@ -546,8 +546,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-  SPH_CK(ctx->qints.ensure(8));
-  SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
+  SPH_CK(ctx->qints.ensure(16));
+  SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 16 * sizeof(int), ctx->stream));
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
   SPH_CK(ctx->kids.ensure(8 * (size_t)n_nodes));
   SPH_CK(ctx->parent.ensure(n_nodes));
@@ -574,10 +574,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   ++launches;
   hist_rounds = 1;
   if (ctx->debug) {
-    int fbk[2] = {0, 0};
+    int fbk[4] = {0, 0, 0, 0};
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses\n", fbk[0], fbk[1]);
+    fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses; %d walks\n", fbk[0], fbk[1], fbk[3]);
     std::vector<uint8_t> hs(n);
     cudaMemcpy(hs.data(), ctx->state.p, n, cudaMemcpyDeviceToHost);
     int cnt[16] = {0};
@@ -624,7 +624,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     SPH_CK(ctx->owner.ensure(n));
     SPH_CK(ctx->v3scratch.ensure(v3_scratch_ints(ctx->num_sms)));
     if (ctx->lpool.ensure(std::min(list_cap, (size_t)INT32_MAX / 2)) != cudaSuccess) SPH_CK(ctx->lpool.ensure(1 << 22));
-    SPH_CK(ctx->qints.ensure(8));
+    SPH_CK(ctx->qints.ensure(16));
     cudaStream_t s = ctx->stream;
     k_init_state<<<nblk(n), kTB, 0, s>>>(n, n_targets, ctx->perm.p, ctx->state.p);
     k_iota<<<nblk(n), kTB, 0, s>>>(n, ctx->iota.p);
@@ -735,7 +735,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   {
     const int item_cap = 2 * n + 65536, pool_cap = 4 * n + 65536;
     if (ctx->items.ensure(item_cap) == cudaSuccess && ctx->pool.ensure(pool_cap) == cudaSuccess &&
-        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(8) == cudaSuccess) {
+        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(16) == cudaSuccess) {
       k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
       SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
       PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
@@ -780,7 +780,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (ctx->lists && ctx->list_mult > 0 && n <= (1 << 27)) {
     const size_t cap = std::min((size_t)ctx->list_mult * (size_t)k, (size_t)lists_max_cap());
     if (ctx->nlists.ensure(cap * (size_t)n) == cudaSuccess && ctx->ncount.ensure(n) == cudaSuccess &&
-        ctx->qints.ensure(8) == cudaSuccess) {
+        ctx->qints.ensure(16) == cudaSuccess) {
       a.nlists = ctx->nlists.p;
       a.ncount = ctx->ncount.p;
       a.ncap = (int)cap;
@@ -810,7 +810,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     t.list = ctx->list.p;
     t.ncount = a.ncount;
     SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-    SPH_CK(ctx->qints.ensure(8));
+    SPH_CK(ctx->qints.ensure(16));
     const int i = ctx->n_kev;
     if (i < 64) {
       ctx->kev_mode[i] = MODE_HIST;

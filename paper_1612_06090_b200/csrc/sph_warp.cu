@@ -49,7 +49,7 @@ template <> struct Pos<false> { using T = D4; };
 constexpr int kStack = 448;  // traversal stack (node ids) per warp
 
 __host__ __device__ constexpr int warp_smem_bytes(int cap) {
-  return NB_HIST * kHistStride * 4 + cap * 8 + 2 * 32 * 4 + kStack * 4;
+  return (32 + NB_HIST * kHistStride * 4 + cap * 8 + 2 * 32 * 4 + kStack * 4 + 15) & ~15;
 }
 
 
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char *wbase = smem_raw + wib * warp_smem_bytes(cap);
+  float4 *simg = reinterpret_cast<float4 *>(smem_raw + wib * warp_smem_bytes(cap));  // image offsets of the shift
+  unsigned char *wbase = smem_raw + wib * warp_smem_bytes(cap) + 32;
   unsigned *hist = reinterpret_cast<unsigned *>(wbase);
   double *inb = reinterpret_cast<double *>(wbase);  // after the histogram is read
   uint2 *list = reinterpret_cast<uint2 *>(wbase + NB_HIST * kHistStride * 4);
@@ -236,8 +237,13 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         const float pslack = shifted ? boxf * 4.8e-7f : slack0;
         // fp32 image arithmetic: x_j - box exact when it matters (Sterbenz); for a
         // +box shift the target moves instead (x_i - box)
-        const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
-        const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
+        // kept in shared memory: the candidate loop reads them instead of
+        // re-deriving them from the shift under register pressure
+        if (lane == 0) {
+          simg[0] = make_float4(sx < 0 ? -boxf : 0.f, sy < 0 ? -boxf : 0.f, sz < 0 ? -boxf : 0.f, 0.f);
+          simg[1] = make_float4(sx > 0 ? fx - boxf : fx, sy > 0 ? fy - boxf : fy, sz > 0 ? fz - boxf : fz, 0.f);
+        }
+        __syncwarp();
 
         // ---- warp traversal: pop up to 32 nodes (one per lane), test, push the
         // children of hit internal nodes (child lists), stream the hit cells ----
@@ -323,8 +329,9 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               j = sbase[r] + s;
               const PT c = pos[j];
               if constexpr (F32) {
-                // unshifted: csx = 0 and tfx = fx, so this is c.x - fx exactly
-                const float dx = (c.x + csx) - tfx, dy = (c.y + csy) - tfy, dz = (c.z + csz) - tfz;
+                // unshifted: cs = 0 and tf = the target, so this is c.x - fx exactly
+                const float4 cs = simg[0], tf = simg[1];
+                const float dx = (c.x + cs.x) - tf.x, dy = (c.y + cs.y) - tf.y, dz = (c.z + cs.z) - tf.z;
                 af = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 in = af <= h_r2;
               } else {
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       if (stack_over) break;
       }
       __syncwarp();
+      if (a.dbg && fallbacks && lane == 0) atomicAdd(fallbacks + 3, 1);  // walks (debug)
       if (stack_over || COLLECT) break;
 
       // ---- counted enough? ----

@@ -1,0 +1,44 @@
+"""Every pipeline of the library against the CPU oracle.
+
+The default pass is the per-target kernel; its fallbacks (collect instance for
+overflowed neighbour lists, walking select/density kernels) only run on a
+few targets of large inputs, so they are forced here with a small list
+capacity.  The bundle pipelines (``SPH_WARP=0``: hybrid, bundle rounds with
+recorded lists, pure walking passes) stay selectable and are checked the
+same way.  Each configuration runs in a fresh process because the pipeline
+switches are read when the library context is created.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CONFIGS = {
+    "per_target": {},
+    "per_target_small_lists": {"SPH_TLISTCAP": "1"},
+    "hybrid_bundle_then_per_target": {"SPH_WARP": "0", "SPH_HYBRID": "1"},
+    "hybrid_small_lists": {"SPH_WARP": "0", "SPH_HYBRID": "1", "SPH_LISTCAP": "1", "SPH_TLISTCAP": "1"},
+    "bundle_rounds_with_lists": {"SPH_WARP": "0", "SPH_HYBRID": "0"},
+    "bundle_rounds_walking_select": {"SPH_WARP": "0", "SPH_HYBRID": "0", "SPH_LISTS": "0"},
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(CONFIGS))
+def test_pipeline_matches_oracle(cfg):
+    env = dict(os.environ)
+    env.update(CONFIGS[cfg])
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_path_worker.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, v in res.items():
+        assert v["h_exact"], (cfg, name)
+        assert v["todo_exact"], (cfg, name)
+        tol = 1e-4 if "_f32_" in name else 1e-12
+        assert v["rho_rel"] <= tol, (cfg, name, v["rho_rel"])
