@@ -20,6 +20,8 @@
  *   sph_fnv1a64           <- snapshot.checksum64 / bench.density_checksum
  *                                                              snapshot.py:70-82,
  *                                                              bench.py:48-50
+ *   sph_uniform_box_device <- workload.generate(UNIFORM_BOX) positions
+ *                                                              workload.py:42-84
  * Status codes map to the reference's exceptions (density.py:69-74, 375-379,
  * 353-357; ValueError for invalid arguments, density.py:297-301).
  */
@@ -135,6 +137,15 @@ double sph_fp32_peak(sph_ctx *ctx);
 
 /* FNV-1a-64 over a byte buffer (host; the reference checksum64) */
 uint64_t sph_fnv1a64(const uint8_t *data, size_t len);
+
+/* On-device input path: the reference's UniformBox positions
+ * generated straight into device SoA arrays (fp64), bit-exact with
+ * generate(WorkloadSpec(UNIFORM_BOX, n, seed)) (workload.py:77-84, splitmix64
+ * draws workload.py:42-60): draw t = 3i + axis of particle i is
+ * mix(seed + (t+1) * 0x9E3779B97F4A7C15) >> 11, times 2^-53, times box
+ * (values at box clamp to nextafter(box, 0)).  Runs on the context's stream. */
+int sph_uniform_box_device(sph_ctx *ctx, int64_t n, uint64_t seed, double box, double *d_x, double *d_y,
+                           double *d_z);
 
 #ifdef __cplusplus
 }

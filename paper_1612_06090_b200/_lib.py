@@ -26,7 +26,7 @@ MAX_TODO = 128
 EXPORTED_SYMBOLS = (
     "sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_device_count",
     "sph_density_pass", "sph_density_pass_device", "sph_sort_perm",
-    "sph_neighbor_counts", "sph_fnv1a64", "sph_ctx_stream", "sph_fp32_peak",
+    "sph_neighbor_counts", "sph_fnv1a64", "sph_ctx_stream", "sph_fp32_peak", "sph_uniform_box_device",
 )
 
 
@@ -100,6 +100,7 @@ def load():
         L.sph_ctx_stream.restype = vp
         L.sph_fnv1a64.argtypes = [vp, ctypes.c_size_t]
         L.sph_fnv1a64.restype = ctypes.c_uint64
+        L.sph_uniform_box_device.argtypes = [vp, i64, ctypes.c_uint64, ctypes.c_double, vp, vp, vp]
         _lib = L
         return L
 

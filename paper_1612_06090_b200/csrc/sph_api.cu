@@ -1064,6 +1064,42 @@ uint64_t sph_fnv1a64(const uint8_t *data, size_t len) {
   return h;
 }
 
+namespace {
+// splitmix64 UniformBox draws (reference workload.py:42-60, 77-84)
+__global__ void k_uniform_box(int64_t n, uint64_t seed, double box, double *x, double *y, double *z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const uint64_t t = (uint64_t)(3 * i + a) + 1ull;
+    uint64_t s = seed + t * 0x9E3779B97F4A7C15ull;
+    s = (s ^ (s >> 30)) * 0xBF58476D1CE4E5B9ull;
+    s = (s ^ (s >> 27)) * 0x94D049BB133111EBull;
+    s = s ^ (s >> 31);
+    const double u = __dmul_rn(__ull2double_rn(s >> 11), 0x1p-53);
+    double w = __dmul_rn(u, box);
+    if (w >= box) w = nextafter(box, 0.0);
+    v[a] = w;
+  }
+  x[i] = v[0];
+  y[i] = v[1];
+  z[i] = v[2];
+}
+}  // namespace
+
+int sph_uniform_box_device(sph_ctx *ctx, int64_t n, uint64_t seed, double box, double *d_x, double *d_y,
+                           double *d_z) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || !(box > 0.0) || (n > 0 && (!d_x || !d_y || !d_z))) return fail(ctx, SPH_INVALID, "invalid uniform box request");
+  if (n == 0) return SPH_OK;
+  cudaSetDevice(ctx->device);
+  k_uniform_box<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(n, seed, box, d_x, d_y, d_z);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SPH_CUDA_ERROR, std::string("k_uniform_box: ") + cudaGetErrorString(e));
+  return SPH_OK;
+}
+
 double sph_fp32_peak(sph_ctx *ctx) {
   if (!ctx) return 0.0;
   cudaSetDevice(ctx->device);

@@ -53,6 +53,27 @@ def uniform_box(n: int, seed: int, box: float = 1.0) -> np.ndarray:
     return v
 
 
+def uniform_box_device(n: int, seed: int, box: float = 1.0, device: int = 0):
+    """``uniform_box`` generated on the GPU (C ABI ``sph_uniform_box_device``):
+    three fp64 torch tensors (x, y, z) on ``cuda:device``, bit-exact with
+    ``uniform_box`` (the on-device input path)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    L = _lib.load()
+    ctx = _lib.context(device)
+    out = [torch.empty(n, dtype=torch.float64, device=f"cuda:{device}") for _ in range(3)]
+    rc = L.sph_uniform_box_device(ctx, n, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), float(box),
+                                  *[ctypes.c_void_p(t.data_ptr()) for t in out])
+    if rc != _lib.SPH_OK:
+        raise RuntimeError(f"sph_uniform_box_device failed ({rc}): {_lib.last_error(ctx)}")
+    torch.cuda.ExternalStream(_lib.stream_handle(ctx), device=f"cuda:{device}").synchronize()
+    return tuple(out)
+
+
 def nfw_enclosed(x):
     return np.log1p(x) - x / (1.0 + x)
 

@@ -249,3 +249,40 @@ def test_k128_single_halo_against_oracle():
     assert np.array_equal(h, want.h)
     assert _rel(rho, want.rho) <= RTOL_F32
     assert np.array_equal(st.todo_sizes, want.todo_sizes)
+
+
+def test_uniform_box_generated_on_device_bit_exact():
+    """On-device input path: the reference UniformBox stream generated by the
+    GPU equals the host restatement (itself pinned to the reference)."""
+    n, seed = 100003, 12345
+    x, y, z = workload.uniform_box_device(n, seed, 2.5)
+    want = workload.uniform_box(n, seed, 2.5)
+    got = np.stack([x.cpu().numpy(), y.cpu().numpy(), z.cpu().numpy()], axis=1)
+    assert np.array_equal(got, want)
+    # and it feeds the device-resident pass: config 1 with no host input at all
+    import ctypes
+
+    import torch
+
+    from paper_1612_06090_b200 import _lib
+    g = golden("c1_uniform32k")
+    n, k = int(g["n"]), int(g["k"])
+    x, y, z = workload.uniform_box_device(n, int(g["seed"]), float(g["box"]))
+    dev = x.device
+    m = torch.full((n,), float(g["mass"]), dtype=torch.float64, device=dev)
+    h = torch.full((n,), float(g["h0"]), dtype=torch.float64, device=dev)
+    rho = torch.empty(n, dtype=torch.float64, device=dev)
+    fl = torch.empty(n, dtype=torch.uint8, device=dev)
+    L = _lib.load()
+    ctx = _lib.context(dev.index or 0)
+    prm = _lib.SphParams(n=n, k=k, max_iterations=100, precision=_lib.PRECISION["f64"], periodic=0,
+                         box=0.0, kernel=0, reserved=0)
+    st = _lib.SphStats()
+    vp = ctypes.c_void_p
+    rc = L.sph_density_pass_device(ctx, prm, vp(x.data_ptr()), vp(y.data_ptr()), vp(z.data_ptr()), vp(m.data_ptr()),
+                                   vp(h.data_ptr()), vp(rho.data_ptr()), vp(fl.data_ptr()), st)
+    assert rc == _lib.SPH_OK, _lib.last_error(ctx)
+    torch.cuda.ExternalStream(_lib.stream_handle(ctx), device=dev).synchronize()
+    assert array_digest(h.cpu().numpy()) == str(g["h_digest"])
+    idx = g["sample_idx"]
+    assert _rel(rho.cpu().numpy()[idx], g["sample_rho"]) <= RTOL_F64
