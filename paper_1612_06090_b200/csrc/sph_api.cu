@@ -90,7 +90,10 @@ struct sph_ctx {
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
   DevBuf<uint2> nlists;
-  DevBuf<int> kids, parent, cellof;
+  DevBuf<float4> crec;
+  DevBuf<int4> anc4;
+  DevBuf<int> parent, cellof;
+  bool crec_ready = false;
   DevBuf<int> ncount;
   bool v3band = false; // SPH_V3BAND=1: select from the recorded lists (else k_pass BAND tasks)
   int last_legacy = 0;
@@ -472,6 +475,29 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
   return SPH_OK;
 }
 
+// child records / ancestors / cell map for the per-target kernel (sph_warp.cu)
+int prepare_target_tree(sph_ctx *ctx, int n, int n_nodes, PassArgs &a) {
+  SPH_CK(ctx->crec.ensure(16 * ((size_t)n_nodes + 1)));
+  SPH_CK(ctx->anc4.ensure(n_nodes));
+  SPH_CK(ctx->parent.ensure(n_nodes));
+  SPH_CK(ctx->cellof.ensure(n));
+  launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->crec.p, ctx->parent.p, ctx->anc4.p, ctx->cellof.p);
+  SPH_CK(cudaGetLastError());
+  a.tree.crec = ctx->crec.p;
+  a.tree.anc4 = ctx->anc4.p;
+  a.tree.cellof = ctx->cellof.p;
+  a.tree.root_start = n_nodes == 1 ? n_nodes : 0;  // a single-cell root: start from the virtual node
+  ctx->crec_ready = true;
+  return SPH_OK;
+}
+
+void use_target_tree(const sph_ctx *ctx, int n_nodes, PassArgs &a) {
+  a.tree.crec = ctx->crec.p;
+  a.tree.anc4 = ctx->anc4.p;
+  a.tree.cellof = ctx->cellof.p;
+  a.tree.root_start = n_nodes == 1 ? n_nodes : 0;
+}
+
 int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const void *y, const void *z,
                      const double *mass, const double *h0, double *h_out, double *rho_out, uint8_t *flags_out,
                      sph_stats *st, Timer &tm) {
@@ -480,6 +506,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const int k = prm->k;
   const int max_it = prm->max_iterations;
   int launches = 0;
+  ctx->crec_ready = false;
   ctx->n_kev = 0;
   { int rc0 = ensure_common(ctx, n, max_it); if (rc0) return rc0; }
   SPH_CK(ctx->t_lo.ensure(n));
@@ -549,13 +576,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(ctx->qints.ensure(16));
   SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 16 * sizeof(int), ctx->stream));
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  SPH_CK(ctx->kids.ensure(8 * (size_t)n_nodes));
-  SPH_CK(ctx->parent.ensure(n_nodes));
-  SPH_CK(ctx->cellof.ensure(n));
-  launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->kids.p, ctx->parent.p, ctx->cellof.p);
-  a.tree.kids = ctx->kids.p;
-  a.tree.parent = ctx->parent.p;
-  a.tree.cellof = ctx->cellof.p;
+  rc = prepare_target_tree(ctx, n, n_nodes, a);
+  if (rc) return rc;
   SPH_CK(ctx->ncount.ensure(n));
   a.ncount = ctx->ncount.p;
   SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
@@ -800,13 +822,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
                   ctx->cub_temp.p, ctx->cub_bytes);
     launches += 2;
     PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
-    SPH_CK(ctx->kids.ensure(8 * (size_t)n_nodes));
-    SPH_CK(ctx->parent.ensure(n_nodes));
-    SPH_CK(ctx->cellof.ensure(n));
-    launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->kids.p, ctx->parent.p, ctx->cellof.p);
-    t.tree.kids = ctx->kids.p;
-    t.tree.parent = ctx->parent.p;
-    t.tree.cellof = ctx->cellof.p;
+    rc = prepare_target_tree(ctx, n, n_nodes, t);
+    if (rc) return rc;
     t.list = ctx->list.p;
     t.ncount = a.ncount;
     SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
@@ -867,12 +884,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
               fbk[0], fbk[1], fbk[2]);
     }
     a.nlists = nullptr;
-    if (ctx->hybrid && ctx->kids.p) {
+    if (ctx->hybrid && ctx->crec_ready) {
       // overflowed lists (bundle pass or per-target kernel): collect up to the bracket top
       PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
-      t.tree.kids = ctx->kids.p;
-      t.tree.parent = ctx->parent.p;
-      t.tree.cellof = ctx->cellof.p;
+      use_target_tree(ctx, n_nodes, t);
       t.ncount = ctx->ncount.p;
       SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
       launch_target(ctx->stream, compute_f32, t, target_list_cap(k), nullptr, ctx->num_sms, true);
@@ -1046,7 +1061,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->ncount.release(); c->kids.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -9,7 +9,10 @@ namespace sph {
 
 constexpr int kMaxLevel = 21;        // 63-bit Morton keys: 21 octree levels
 constexpr int kLeafCap = 8;          // reference leaf capacity (octree.py:30)
-constexpr int kCellCap = 32;         // search cell capacity (one warp of candidates)
+#ifndef SPH_CELL_CAP
+#define SPH_CELL_CAP 32
+#endif
+constexpr int kCellCap = SPH_CELL_CAP;  // search cell capacity (<= 32: one warp of candidates)
 constexpr double kGrowth = 1.2599210498948732;  // 2.0 ** (1.0 / 3.0), density.py:53
 constexpr double kWc6Norm = 1365.0 / (64.0 * 3.14159265358979323846);  // kernel.py:17
 constexpr double kM4Norm = 8.0 / 3.14159265358979323846;              // M4 (extension)
@@ -90,9 +93,10 @@ struct TreeView {
   const float4 *nlo;
   const float4 *nhi;
   const int *nsize;   // particles in the node's subtree
-  const int *kids;    // 8 child node ids per node (-1 padded), for the per-target traversal
-  const int *parent;  // parent node id (-1 for the root)
-  const int *cellof;  // cell holding each sorted particle
+  const float4 *crec;  // per-target traversal: 8 child records {box lo, code} {box hi, end} per node (+ virtual root)
+  const int4 *anc4;    // first four ancestors of each node
+  const int *cellof;   // cell holding each sorted particle
+  int root_start;      // node whose children the unshifted-fallback / shifted walks expand (0, or the virtual node)
   int n_nodes;
 };
 
@@ -233,8 +237,8 @@ int lists_max_cap();
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,
                    bool collect = false);
-void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, int *kids, int *parent,
-                 int *cellof);
+void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
+                 int4 *anc4, int *cellof);
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
 size_t select_temp_needed(int n);

@@ -108,28 +108,29 @@ __global__ void k_keys(int n, const PosT *__restrict__ x, const PosT *__restrict
 // level = floor(M/3) + 1 (0 when no full window exists).
 __global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uint8_t *__restrict__ lvl8,
                          uint8_t *__restrict__ lvl32, int *deep_count, uint32_t *deep_list) {
-  __shared__ unsigned long long sk[kTB + 64];
-  __shared__ int w8[kTB + 32], w32[kTB + 32];
+  constexpr int H = kCellCap > 32 ? kCellCap : 32;  // window halo
+  __shared__ unsigned long long sk[kTB + 2 * H];
+  __shared__ int w8[kTB + H], w32[kTB + H];
   const int b0 = blockIdx.x * kTB;
-  for (int t = threadIdx.x; t < kTB + 64; t += kTB) {
-    int q = b0 - 32 + t;
+  for (int t = threadIdx.x; t < kTB + 2 * H; t += kTB) {
+    int q = b0 - H + t;
     sk[t] = (q >= 0 && q < n) ? keys[q] : 0ull;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < kTB + 32; t += kTB) {
-    int s = b0 - 32 + t;  // window start
+  for (int t = threadIdx.x; t < kTB + H; t += kTB) {
+    int s = b0 - H + t;  // window start
     w8[t] = (s >= 0 && s + 8 <= n - 1) ? key_cpl(sk[t], sk[t + 8]) : -1;
-    w32[t] = (s >= 0 && s + 32 <= n - 1) ? key_cpl(sk[t], sk[t + 32]) : -1;
+    w32[t] = (s >= 0 && s + kCellCap <= n - 1) ? key_cpl(sk[t], sk[t + kCellCap]) : -1;
   }
   __syncthreads();
   const int p = b0 + threadIdx.x;
   if (p >= n) return;
-  const int tp = threadIdx.x + 32;  // index of window starting at p
+  const int tp = threadIdx.x + H;  // index of window starting at p
   int m8 = -1, m32 = -1;
 #pragma unroll
   for (int d = 0; d <= 8; ++d) m8 = max(m8, w8[tp - d]);
 #pragma unroll 8
-  for (int d = 0; d <= 32; ++d) m32 = max(m32, w32[tp - d]);
+  for (int d = 0; d <= kCellCap; ++d) m32 = max(m32, w32[tp - d]);
   int l8 = m8 < 0 ? 0 : m8 / 3 + 1;
   int l32 = m32 < 0 ? 0 : m32 / 3 + 1;
   if (l8 > kMaxLevel) {

@@ -249,48 +249,46 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         // children of hit internal nodes (child lists), stream the hit cells ----
         // unshifted: start at the lowest ancestor of the target's cell whose box
         // holds the whole search sphere (no cell outside it can be within R)
-        int start = 0;
-        if (!shifted && a.tree.parent) {
+        int start = a.tree.root_start;
+        if (!shifted) {
+          const int4 an = a.tree.anc4[a.tree.cellof[p]];
           const float rr = sqrtf(h_r2) * (1.0f + 8.0f * kEps) + pslack;
-          int c = a.tree.cellof[p];
-          while (c > 0) {
-            const float4 l4 = nlo[c], h4 = nhi[c];
-            if (l4.x <= pqx - rr && pqx + rr <= h4.x && l4.y <= pqy - rr && pqy + rr <= h4.y && l4.z <= pqz - rr &&
-                pqz + rr <= h4.z)
-              break;
-            c = a.tree.parent[c];
+          const int my_anc = lane == 0 ? an.x : lane == 1 ? an.y : lane == 2 ? an.z : lane == 3 ? an.w : -1;
+          bool holds = false;
+          if (my_anc >= 0) {
+            const float4 l4 = nlo[my_anc], h4 = nhi[my_anc];
+            holds = l4.x <= pqx - rr && pqx + rr <= h4.x && l4.y <= pqy - rr && pqy + rr <= h4.y &&
+                    l4.z <= pqz - rr && pqz + rr <= h4.z;
           }
-          start = c;
+          const unsigned hm = __ballot_sync(FULL, holds);
+          if (hm) start = __shfl_sync(FULL, my_anc, __ffs(hm) - 1);
         }
         // the stack holds hit internal nodes; a step expands up to 4 of them,
-        // one child per lane (8 slots each), and tests the children's boxes
-        int top = 0;
-        bool first = true;  // the first step tests the start node itself (lane 0)
-        while (first || top > 0) {
-          int node = -1;
-          if (first) {
-            node = lane == 0 ? start : -1;
-            first = false;
-          } else {
-            const int np = min(top, 4);
-            top -= np;
-            const int pi = lane >> 3;
-            const int par = pi < np ? stk[top + pi] : -1;
-            if (par >= 0) node = a.tree.kids[8 * par + (lane & 7)];
-          }
+        // one child record per lane (8 slots each: box + node id or cell range)
+        if (lane == 0) stk[0] = start;
+        int top = 1;
+        __syncwarp();
+        while (top > 0) {
+          const int np = min(top, 4);
+          top -= np;
+          const int pi = lane >> 3;
+          const int par = pi < np ? stk[top + pi] : -1;
           __syncwarp();
           bool hit = false, is_cell = false;
-          int my_start = 0, my_end = 0;
-          if (node >= 0) {
-            const float4 l4 = nlo[node], h4 = nhi[node];
-            is_cell = __float_as_int(l4.w) == node + 1;
+          int node = -1, my_start = 0, my_end = 0;
+          if (par >= 0) {
+            const float4 *rec = a.tree.crec + 16 * (size_t)par + 2 * (lane & 7);
+            const float4 l4 = rec[0], h4 = rec[1];
+            const int code = __float_as_int(l4.w);
+            is_cell = code < 0;
+            node = code;
             const float gx = fmaxf(fmaxf(l4.x - pqx, pqx - h4.x) - pslack, 0.f);
             const float gy = fmaxf(fmaxf(l4.y - pqy, pqy - h4.y) - pslack, 0.f);
             const float gz = fmaxf(fmaxf(l4.z - pqz, pqz - h4.z) - pslack, 0.f);
             hit = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= h_r2;
             if (hit && is_cell) {
-              my_start = __float_as_int(h4.w);
-              my_end = node + 1 < n_nodes ? __float_as_int(nhi[node + 1].w) : n;
+              my_start = ~code;
+              my_end = __float_as_int(h4.w);
             }
           }
           const unsigned pm = __ballot_sync(FULL, hit && !is_cell);
@@ -595,35 +593,80 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   }
 }
 
-// children of each internal node (pre-order indices, -1 padded): k+1, then
-// the skip pointer chain up to the node's own skip
-// and the parent of each node; cellof[i] = the cell holding sorted particle i
+// Child records for the per-target traversal: for every internal node k (and
+// a virtual node V = n_nodes whose only child is the root) 8 slots of
+// {child box lo, code} {child box hi, end}: code >= 0 is an internal child's
+// node id, code < 0 a cell holding particles [~code, end); absent slots have an
+// empty box (never hit).  Also the parent of each node and the cell of each
+// sorted particle.
+__device__ __forceinline__ void child_record(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi,
+                                             int n_nodes, int n, int c, float4 &lo, float4 &hi) {
+  lo = nlo[c];
+  hi = nhi[c];
+  const bool cell = __float_as_int(lo.w) == c + 1;
+  const int start = __float_as_int(hi.w);
+  const int end = c + 1 < n_nodes ? __float_as_int(nhi[c + 1].w) : n;
+  lo.w = __int_as_float(cell ? ~start : c);
+  hi.w = __int_as_float(cell ? end : 0);
+}
+
 __global__ void k_kids(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi, int n_nodes, int n,
-                       int *__restrict__ kids, int *__restrict__ parent, int *__restrict__ cellof) {
+                       float4 *__restrict__ crec, int *__restrict__ parent, int *__restrict__ cellof) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > n_nodes) return;
+  const float4 empty_lo = make_float4(INFINITY, INFINITY, INFINITY, __int_as_float(INT_MIN));
+  const float4 empty_hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+  float4 *rec = crec + 16 * (size_t)k;
+  int i = 0;
+  if (k == n_nodes) {  // virtual node above the root
+    float4 lo, hi;
+    child_record(nlo, nhi, n_nodes, n, 0, lo, hi);
+    rec[0] = lo;
+    rec[1] = hi;
+    i = 1;
+  } else {
+    if (k == 0) parent[0] = -1;
+    const int skip = __float_as_int(nlo[k].w);
+    if (skip != k + 1) {
+      int c = k + 1;
+      while (c < skip && i < 8) {
+        float4 lo, hi;
+        child_record(nlo, nhi, n_nodes, n, c, lo, hi);
+        rec[2 * i] = lo;
+        rec[2 * i + 1] = hi;
+        ++i;
+        parent[c] = k;
+        c = __float_as_int(nlo[c].w);
+      }
+    } else {
+      const int s0 = __float_as_int(nhi[k].w);
+      const int e0 = k + 1 < n_nodes ? __float_as_int(nhi[k + 1].w) : n;
+      for (int j = s0; j < e0; ++j) cellof[j] = k;
+    }
+  }
+  for (; i < 8; ++i) {
+    rec[2 * i] = empty_lo;
+    rec[2 * i + 1] = empty_hi;
+  }
+}
+
+// the first four ancestors of every node (-1 above the root)
+__global__ void k_anc(const int *__restrict__ parent, int n_nodes, int4 *__restrict__ anc4) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_nodes) return;
-  if (k == 0) parent[0] = -1;
-  const int skip = __float_as_int(nlo[k].w);
-  int c = k + 1, i = 0;
-  if (skip != k + 1) {
-    while (c < skip && i < 8) {
-      kids[8 * k + i++] = c;
-      parent[c] = k;
-      c = __float_as_int(nlo[c].w);
-    }
-  } else {
-    const int s0 = __float_as_int(nhi[k].w);
-    const int e0 = k + 1 < n_nodes ? __float_as_int(nhi[k + 1].w) : n;
-    for (int j = s0; j < e0; ++j) cellof[j] = k;
-  }
-  for (; i < 8; ++i) kids[8 * k + i] = -1;
+  const int a1 = parent[k];
+  const int a2 = a1 >= 0 ? parent[a1] : -1;
+  const int a3 = a2 >= 0 ? parent[a2] : -1;
+  const int a4 = a3 >= 0 ? parent[a3] : -1;
+  anc4[k] = make_int4(a1, a2, a3, a4);
 }
 
 }  // namespace
 
-void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, int *kids, int *parent,
-                 int *cellof) {
-  k_kids<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, nhi, n_nodes, n, kids, parent, cellof);
+void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
+                 int4 *anc4, int *cellof) {
+  k_kids<<<(n_nodes + 1 + 255) / 256, 256, 0, s>>>(nlo, nhi, n_nodes, n, crec, parent, cellof);
+  k_anc<<<(n_nodes + 255) / 256, 256, 0, s>>>(parent, n_nodes, anc4);
 }
 
 int target_list_cap(int k) {
