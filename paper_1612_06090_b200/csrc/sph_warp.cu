@@ -309,22 +309,30 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           cand += total;
           tests += (unsigned)total;
           if (cand > (1 << 20)) { stack_over = true; break; }  // 16-bit counters: bundle passes
-          spfx[lane] = incl;
-          sbase[lane] = my_start - (incl - len);
+          // needed cells compacted (all ranges non-empty, so their stream ends
+          // are distinct): lane r holds the end of cell r in the stream
+          const unsigned nm = __ballot_sync(FULL, need);
+          if (need) {
+            const int ci = __popc(nm & lt_mask);
+            spfx[ci] = incl;
+            sbase[ci] = my_start - (incl - len);
+          }
           __syncwarp();
+          const int cend = lane < __popc(nm) ? spfx[lane] : 0x7fffffff;
 
-          // ---- stream the window's candidates, 32 per step ----
+          // ---- stream the step's candidates, 32 per chunk ----
           for (int c0 = 0; c0 < total; c0 += 32) {
             const int s = c0 + lane;
             bool in = false;
             int j = 0;
             float af = 0.f;
+            // owner of stream slot s = #{cells whose end <= s}: the cells ending
+            // before the chunk plus a bit mask of the ends inside it
+            const unsigned ev = (cend > c0 && cend <= c0 + 31) ? 1u << (cend - c0 - 1) : 0u;
+            const unsigned emask = __reduce_or_sync(FULL, ev);
+            const int owner = __popc(__ballot_sync(FULL, cend <= c0)) + __popc(emask & lt_mask);
             if (s < total) {
-              int r = 0;
-#pragma unroll
-              for (int step = 16; step; step >>= 1)
-                if (spfx[r + step - 1] <= s) r += step;
-              j = sbase[r] + s;
+              j = sbase[owner] + s;
               const PT c = pos[j];
               if constexpr (F32) {
                 // unshifted: cs = 0 and tf = the target, so this is c.x - fx exactly
