@@ -608,33 +608,45 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     for (int i = 0; i < 16; ++i) if (cnt[i]) fprintf(stderr, " %d:%d", i, cnt[i]);
     fprintf(stderr, "\n");
   }
-  // overflowed lists: collect again up to the bracket top
-  SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-  SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
-  launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms, true);
-  ++launches;
-  if (ctx->debug) {
-    int fbk[2] = {0, 0};
-    cudaStreamSynchronize(ctx->stream);
-    cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[sph collect] still to the walking select: %d overflowed lists, %d bracket misses\n", fbk[0], fbk[1]);
+  // fallback counters of the main kernel: [5] overflowed lists [6] bracket
+  // misses [9] stack overflows (one small read; the empty fallback launches are skipped)
+  int q[16];
+  SPH_CK(cudaMemcpyAsync(q, ctx->qints.p, sizeof(q), cudaMemcpyDeviceToHost, ctx->stream));
+  SPH_CK(cudaStreamSynchronize(ctx->stream));
+  int coll_left = 0;
+  if (q[5] + q[6] > 0) {
+    // overflowed lists: the collect instance (bracket list, then the density list)
+    SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+    launch_target(ctx->stream, compute_f32, a, 1024, ctx->qints.p + 10, ctx->num_sms, true);
+    ++launches;
+    int q2[5];
+    SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 10, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));
+    SPH_CK(cudaStreamSynchronize(ctx->stream));
+    coll_left = q2[0] + q2[1] + q2[4];
+    if (ctx->debug)
+      fprintf(stderr, "[sph collect] %d targets; still to the walking select: %d overflowed, %d bracket misses, %d stack\n",
+              q[5] + q[6], q2[0], q2[1], q2[4]);
   }
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);
-  // targets the stack could not serve: the bundle search passes
-  {
+  if (q[9] > 0) {
+    // targets the stack could not serve: the bundle search passes
     int hr = 0;
     rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hr);
     if (rc) return rc;
     hist_rounds += hr;
   }
-  // targets the lists could not serve: walking select + density
-  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
-  if (rc) return rc;
-  tm.mark(4);
-  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
-  ++launches;
+  if (q[9] > 0 || coll_left > 0) {
+    // targets no list could serve: walking select + density
+    rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
+    if (rc) return rc;
+    tm.mark(4);
+    timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
+    ++launches;
+  } else {
+    tm.mark(4);
+  }
   tm.mark(5);
   } else if (ctx->v3) {
   // ---- "walk once, sweep narrow": k_form groups, one recorded walk per group ----
@@ -890,7 +902,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       use_target_tree(ctx, n_nodes, t);
       t.ncount = ctx->ncount.p;
       SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-      launch_target(ctx->stream, compute_f32, t, target_list_cap(k), nullptr, ctx->num_sms, true);
+      launch_target(ctx->stream, compute_f32, t, 1024, nullptr, ctx->num_sms, true);
       ++launches;
     }
   }

@@ -33,7 +33,8 @@ constexpr int kHistOctaves = 12;
 constexpr int kHistBase = (127 - kHistOctaves) << 2;
 constexpr int NB_HIST = kHistOctaves * 4 + 2;
 constexpr int kHistStride = 17;  // words per bin row: 16-bit counters, two lanes per word (odd: conflict-free row sums)
-constexpr int kInCap = 256;      // in-bracket entries (aliases the histogram)
+constexpr int kInCapMain = 256;     // in-bracket entries (alias the histogram, 3.4 KB)
+constexpr int kInCapCollect = 416;  // the collect instance has no histogram to keep
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
 constexpr unsigned kNaNf = 0x7fc00000u;
@@ -84,8 +85,9 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   const bool f32sum = F32 && !a.dens64;
   const double norm = a.kernel_kind == 0 ? kWc6Norm : kM4Norm;
   const unsigned lt_mask = (1u << lane) - 1u;
+  constexpr int kInCap = COLLECT ? kInCapCollect : kInCapMain;
   unsigned long long tests = 0, accepted = 0;
-  int fb_over = 0, fb_bracket = 0;
+  int fb_over = 0, fb_bracket = 0, fb_stack = 0;
 
   const int count = a.list ? *a.list_count : a.static_count;
   // work in chunks of CH targets per atomic (the collect instance scans sparse
@@ -142,8 +144,13 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       }
     }
 
+    // collect instance: phase 0 lists the bracket (counting what lies below it),
+    // phase 1 lists everything within the selected h for the density
+    int cphase = 0;
+    double d2k_c = 0.0;
     for (;;) {  // grow loop
-      const float hR2 = COLLECT ? (float)(__double2float_ru(a.t_hi[p] * (1.0 + kEpsD)) + 1e-37f) : R * R;
+      const float hR2 = COLLECT ? (float)(__double2float_ru((cphase ? d2k_c : a.t_hi[p]) * (1.0 + kEpsD)) + 1e-37f)
+                                : R * R;
       const float h_inv = 1.0f / hR2;
       float h_r2 = hR2;  // current acceptance radius^2 (shrinks)
       if (!COLLECT)
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
             }
             bool lst = in;
             if constexpr (COLLECT) {
-              if (lst && af < lo_c && !(j == p && sidx == center)) {
+              if (cphase == 0 && lst && af < lo_c && !(j == p && sidx == center)) {
                 ++cbelow;
                 lst = false;
               }
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       }
       __syncwarp();
       }  // pass loop
-      if (stack_over) break;  // leave the target to the bundle passes (state NEED_HIST)
+      if (stack_over) { ++fb_stack; break; }  // the bundle passes take it (state unchanged)
       if (done_unreach) break;
       if (grow) continue;
 
@@ -458,9 +465,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       };
       if (over) { ++fb_over; fallback(); break; }
 
-      // ---- exact count below the bracket, collect the bracket ----
-      const float lo_f = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
-      const float hi_f = __double2float_ru(th * (1.0 + kEpsD)) + 1e-37f;
+      double d2k;
       auto image_d2 = [&](const PT &c, int sidx) {
         double cx = c.x, cy = c.y, cz = c.z;
         if (a.periodic && sidx != 13) {
@@ -469,69 +474,76 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         }
         return exact_d2(__dsub_rn(cx, tx), __dsub_rn(cy, ty), __dsub_rn(cz, tz));
       };
-      int below = cbelow, n_in = 0;
-      for (int i0 = 0; i0 < ne; i0 += 32) {
-        const int i = i0 + lane;
-        bool inb_ = false;
-        double e = 0.0;
-        if (i < ne) {
-          const uint2 le = list[i];
-          const float af = __uint_as_float(le.y);
-          const int j = (int)(le.x & ((1u << 27) - 1u));
-          const int sidx = (int)(le.x >> 27);
-          if (!(j == p && sidx == center)) {
-            if (af < lo_f) {
-              ++below;
-            } else if (af <= hi_f) {
-              e = image_d2(pos[j], sidx);
-              if (e < tl) ++below;
-              else if (e <= th) inb_ = true;
+      if (COLLECT && cphase == 1) {
+        d2k = d2k_c;
+      } else {
+        // ---- exact count below the bracket, collect the bracket ----
+        const float lo_f = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
+        const float hi_f = __double2float_ru(th * (1.0 + kEpsD)) + 1e-37f;
+        int below = cbelow, n_in = 0;
+        for (int i0 = 0; i0 < ne; i0 += 32) {
+          const int i = i0 + lane;
+          bool inb_ = false;
+          double e = 0.0;
+          if (i < ne) {
+            const uint2 le = list[i];
+            const float af = __uint_as_float(le.y);
+            const int j = (int)(le.x & ((1u << 27) - 1u));
+            const int sidx = (int)(le.x >> 27);
+            if (!(j == p && sidx == center)) {
+              if (af < lo_f) {
+                ++below;
+              } else if (af <= hi_f) {
+                e = image_d2(pos[j], sidx);
+                if (e < tl) ++below;
+                else if (e <= th) inb_ = true;
+              }
             }
           }
+          const unsigned bm = __ballot_sync(FULL, inb_);
+          if (inb_ && n_in + __popc(bm & lt_mask) < kInCap) inb[n_in + __popc(bm & lt_mask)] = e;  // see kInCap
+          n_in += __popc(bm);
         }
-        const unsigned bm = __ballot_sync(FULL, inb_);
-        if (inb_ && n_in + __popc(bm & lt_mask) < kInCap) inb[n_in + __popc(bm & lt_mask)] = e;
-        n_in += __popc(bm);
-      }
-      __syncwarp();
-      below = (int)__reduce_add_sync(FULL, (unsigned)below);
-      const int r = K - below;  // 1-based rank of the K-th inside the bracket
-      if (!COLLECT && n_in <= kInCap && r > n_in && R < a.rmax) {
-        // the K-th lies above the (clipped) list radius, at the very edge of
-        // R: search again with a slightly larger radius
-        R = fminf(R * 1.26f, a.rmax);
-        continue;
-      }
-      if (n_in > kInCap || r < 1 || r > n_in) {
-        if (lane == 0 && a.dbg && fallbacks && atomicAdd(fallbacks + 2, 1) < 10)
-          printf("[target miss] p=%d ne=%d seen=%d K=%d below=%d n_in=%d tl=%.9g th=%.9g h_r2=%.9g R2=%.9g\n", p, ne,
-                 seen, K, below, n_in, tl, th, (double)h_r2, (double)hR2);
-        ++fb_bracket;
-        fallback();
-        break;
-      }
+        __syncwarp();
+        below = (int)__reduce_add_sync(FULL, (unsigned)below);
+        const int r = K - below;  // 1-based rank of the K-th inside the bracket
+        if (!COLLECT && n_in <= kInCap && r > n_in && R < a.rmax) {
+          // the K-th lies above the (clipped) list radius, at the very edge of
+          // R: search again with a slightly larger radius
+          R = fminf(R * 1.26f, a.rmax);
+          continue;
+        }
+        if (n_in > kInCap || r < 1 || r > n_in) {
+          if (lane == 0 && a.dbg && fallbacks && atomicAdd(fallbacks + 2, 1) < 10)
+            printf("[target miss] p=%d ne=%d seen=%d K=%d below=%d n_in=%d tl=%.9g th=%.9g h_r2=%.9g R2=%.9g\n", p, ne,
+                   seen, K, below, n_in, tl, th, (double)h_r2, (double)hR2);
+          ++fb_bracket;
+          fallback();
+          break;
+        }
 
-      // ---- the r-th smallest of the bracket ----
-      double v = INFINITY;
-      for (int i = lane; i < n_in; i += 32) {
-        const double ei = inb[i];
-        int less = 0, eq = 0;
-        for (int jj = 0; jj < n_in; ++jj) {
-          const double ej = inb[jj];
-          less += ej < ei;
-          eq += ej == ei;
+        // ---- the r-th smallest of the bracket ----
+        double v = INFINITY;
+        for (int i = lane; i < n_in; i += 32) {
+          const double ei = inb[i];
+          int less = 0, eq = 0;
+          for (int jj = 0; jj < n_in; ++jj) {
+            const double ej = inb[jj];
+            less += ej < ei;
+            eq += ej == ei;
+          }
+          if (less < r && r <= less + eq) v = ei;
         }
-        if (less < r && r <= less + eq) v = ei;
-      }
-      for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
-      const double d2k = v;
-      if constexpr (COLLECT) {
-        // the list held only the bracket: the density pass (sph_pass.cu) sums rho
-        if (lane == 0) {
-          a.d2k[p] = d2k;
-          a.state[p] = ST_DONE;
+        for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+        d2k = v;
+
+        if constexpr (COLLECT) {
+          if (d2k > 0.0) {  // phase 1: everything within h, for the density sum
+            d2k_c = d2k;
+            cphase = 1;
+            continue;
+          }
         }
-        break;
       }
 
       // ---- density over the list entries within h ----
@@ -597,6 +609,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
     if (fallbacks) {
       if (fb_over) atomicAdd(fallbacks, fb_over);
       if (fb_bracket) atomicAdd(fallbacks + 1, fb_bracket);
+      if (fb_stack) atomicAdd(fallbacks + 4, fb_stack);
     }
   }
 }
