@@ -580,6 +580,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (rc) return rc;
   SPH_CK(ctx->ncount.ensure(n));
   a.ncount = ctx->ncount.p;
+  a.fb_list = ctx->list.p;          // compacted targets for the collect instance
+  a.fb_count = ctx->qints.p + 15;
   SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
   {
     const int i = ctx->n_kev;
@@ -617,7 +619,11 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (q[5] + q[6] > 0) {
     // overflowed lists: the collect instance (bracket list, then the density list)
     SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-    launch_target(ctx->stream, compute_f32, a, 1024, ctx->qints.p + 10, ctx->num_sms, true);
+    PassArgs c = a;
+    c.list = ctx->list.p;
+    c.list_count = ctx->qints.p + 15;
+    c.fb_list = nullptr;
+    launch_target(ctx->stream, compute_f32, c, 1024, ctx->qints.p + 10, ctx->num_sms, true);
     ++launches;
     int q2[5];
     SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 10, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   const int count = a.list ? *a.list_count : a.static_count;
   // work in chunks of CH targets per atomic (the collect instance scans sparse
   // targets: whole warps of them)
-  constexpr int CH = COLLECT ? 32 : 1;
+  const int CH = (COLLECT && !a.list) ? 32 : 1;  // a compacted list: one target per grab
   unsigned pend = 0u;
   int cbase = 0;
   for (;;) {
@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           a.state[p] = ST_NEED_BAND;
           // no usable list: the collect instance next, then the walking select
           if (a.ncount) a.ncount[p] = COLLECT ? 0x7ffffffe : 0x7fffffff;
+          if (!COLLECT && a.fb_list) a.fb_list[atomicAdd(a.fb_count, 1)] = (uint32_t)p;
         }
       };
       if (over) { ++fb_over; fallback(); break; }
