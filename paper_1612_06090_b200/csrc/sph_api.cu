@@ -94,6 +94,7 @@ struct sph_ctx {
   DevBuf<int4> anc4;
   DevBuf<int> parent, cellof;
   bool crec_ready = false;
+  int tb_emit_r0 = 1;    // did the last tree build compute R0 (k_node_emit)?
   DevBuf<int> ncount;
   bool v3band = false; // SPH_V3BAND=1: select from the recorded lists (else k_pass BAND tasks)
   int last_legacy = 0;
@@ -292,6 +293,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.bbox_ord = ctx->bbox_ord.p;
   tb.r0_scale = ctx->r0_scale;
   tb.c0_scale = ctx->c0_scale;
+  tb.emit_r0 = 1;
   return tb;
 }
 
@@ -311,6 +313,9 @@ int stage_root(sph_ctx *ctx, int n, int precision, const void *x, const void *y,
 int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *x, const void *y, const void *z,
                const double *mass, int k, float rmax, int *n_nodes, int *launches, bool search_tree) {
   TreeBuffers tb = tree_buffers(ctx);
+  // the per-target path derives R0 from the node sizes (k_r0) instead
+  tb.emit_r0 = (ctx->warp && !ctx->fused && n <= (1 << 27)) ? 0 : 1;
+  ctx->tb_emit_r0 = tb.emit_r0;
   const int in32 = precision == SPH_PRECISION_F32 ? 1 : 0;
   tree_build(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, launches);
   if (search_tree) tree_build_search(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, rmax, launches);
@@ -482,6 +487,17 @@ int prepare_target_tree(sph_ctx *ctx, int n, int n_nodes, PassArgs &a) {
   SPH_CK(ctx->parent.ensure(n_nodes));
   SPH_CK(ctx->cellof.ensure(n));
   launch_kids(ctx->stream, ctx->nlo.p, ctx->nhi.p, n_nodes, n, ctx->crec.p, ctx->parent.p, ctx->anc4.p, ctx->cellof.p);
+  if (!ctx->tb_emit_r0) {
+    float root_side = 0.f;  // only used when the root is a single cell: its tight extent
+    if (n_nodes == 1) {
+      float4 l, h;
+      cudaMemcpy(&l, ctx->nlo.p, sizeof(l), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&h, ctx->nhi.p, sizeof(h), cudaMemcpyDeviceToHost);
+      root_side = std::max(h.x - l.x, std::max(h.y - l.y, h.z - l.z));
+    }
+    launch_r0(ctx->stream, ctx->nlo.p, ctx->nhi.p, ctx->nsize.p, ctx->parent.p, n_nodes, n, a.k, ctx->r0_scale,
+              a.rmax, root_side, ctx->r0.p);
+  }
   SPH_CK(cudaGetLastError());
   a.tree.crec = ctx->crec.p;
   a.tree.anc4 = ctx->anc4.p;

@@ -215,6 +215,7 @@ struct TreeBuffers {
   unsigned long long *bbox_ord;         // 6 ordered-int accumulators
   float r0_scale;                       // initial radius = r0_scale * density estimate
   float c0_scale;                       // ... capped by c0_scale * the cell's own tight-box estimate
+  int emit_r0;                          // 0: R0 comes from k_r0 (per-target path) instead of k_node_emit
 };
 
 int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int compute_f32,
@@ -241,6 +242,9 @@ void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fal
                    bool collect = false);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof);
+// per-cell initial search radius from the node sizes and the parent chain
+void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *nsize, const int *parent, int n_nodes,
+               int n, int k, float r0_scale, float rmax, float root_side, float *r0);
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
 size_t select_temp_needed(int n);

@@ -269,7 +269,7 @@ __device__ __forceinline__ float f_ru(double v) { return __double2float_ru(v); }
 template <bool F32>
 __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl32,
                             const int *__restrict__ noff, const RootInfo *__restrict__ root,
-                            const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale, float c0_scale,
+                            const void *__restrict__ pos_sorted, int k, float rmax, float r0_scale, float c0_scale, int emit_r0,
                             float4 *__restrict__ nlo, float4 *__restrict__ nhi, int *__restrict__ nsize,
                             float *__restrict__ r0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -323,6 +323,12 @@ __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, 
       }
       lo = make_float4(mn[0], mn[1], mn[2], __int_as_float(skip));
       hi = make_float4(mx[0], mx[1], mx[2], __int_as_float(p));
+      if (!emit_r0) {  // the per-target path computes R0 from the node sizes (k_r0)
+        nlo[node] = lo;
+        nhi[node] = hi;
+        nsize[node] = end - p;
+        continue;
+      }
       // Initial search radius.  Density estimates from the smallest ancestors
       // holding >= K/2 and >= 2K particles; the smaller of the two (an
       // under-estimate costs one cheap retry, an over-estimate costs a large
@@ -450,10 +456,10 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   size_t tbytes = tb.cub_temp_bytes;
   cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
   if (compute_f32)
-    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale,
+    k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale, tb.emit_r0,
                                               tb.nlo, tb.nhi, tb.nsize, tb.r0);
   else
-    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale,
+    k_node_emit<false><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale, tb.emit_r0,
                                                tb.nlo, tb.nhi, tb.nsize, tb.r0);
   *launches += 3;
   return 0;

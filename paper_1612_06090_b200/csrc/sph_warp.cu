@@ -683,7 +683,44 @@ __global__ void k_anc(const int *__restrict__ parent, int n_nodes, int4 *__restr
   anc4[k] = make_int4(a1, a2, a3, a4);
 }
 
+// Initial search radius per cell (the per-target path): density estimates
+// from the smallest ancestors (cell included) holding >= K/2 and >= 2K
+// particles, the smaller of the two times r0_scale, capped by sqrt(3) x the
+// side of the smallest ancestor holding >= K+1 (it surely contains K others).
+__global__ void k_r0(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi, const int *__restrict__ nsize,
+                     const int *__restrict__ parent, int n_nodes, int n, int k, float r0_scale, float rmax,
+                     float root_side, float *__restrict__ r0) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_nodes || __float_as_int(nlo[c].w) != c + 1) return;
+  const int a0 = parent[c];
+  double side = a0 >= 0 ? 0.5 * ((double)nhi[a0].x - (double)nlo[a0].x) : root_side;  // the cell's cube
+  int cnt = nsize[c];
+  int a = a0;
+  double est_a = 0.0, est_b = 0.0, bound = 0.0;
+  for (;;) {
+    const double est = side * cbrt(3.0 * k / (4.0 * 3.14159265358979323846 * (double)max(cnt, 1)));
+    const bool top = a < 0;
+    if (est_a == 0.0 && (cnt >= (k + 1) / 2 || top)) est_a = est;
+    if (bound == 0.0 && (cnt >= k + 1 || top)) bound = 1.7320508075688772 * side * (1.0 + 1e-6);
+    if (cnt >= 2 * k || top) { est_b = est; break; }
+    cnt = nsize[a];
+    side = (double)nhi[a].x - (double)nlo[a].x;  // the ancestor's (padded) cube
+    a = parent[a];
+  }
+  float R = (float)fmin(r0_scale * fmin(est_a, est_b), bound);
+  if (!(R > 0.f)) R = rmax;
+  R = fminf(R, rmax);
+  const int s0 = __float_as_int(nhi[c].w);
+  const int e0 = c + 1 < n_nodes ? __float_as_int(nhi[c + 1].w) : n;
+  for (int q = s0; q < e0; ++q) r0[q] = R;
+}
+
 }  // namespace
+
+void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *nsize, const int *parent, int n_nodes,
+               int n, int k, float r0_scale, float rmax, float root_side, float *r0) {
+  k_r0<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, nhi, nsize, parent, n_nodes, n, k, r0_scale, rmax, root_side, r0);
+}
 
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof) {
