@@ -110,7 +110,7 @@ struct sph_ctx {
   DevBuf<int> qints;
   float sub_d = 2.0f;
   float sub_d_retry = 2.0f;  // task extent of retry rounds (SPH_SUBD_RETRY)
-  float r0_scale = 1.1f;
+  float r0_scale = 1.15f;
   float c0_scale = 1e30f;  // SPH_C0SCALE: cap R0 by c0 x the cell's tight-box estimate (off by default)
   int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
   size_t cub_bytes = 0;
