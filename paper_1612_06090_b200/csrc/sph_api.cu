@@ -86,6 +86,9 @@ struct sph_ctx {
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
+  int seed_stride = 4;   // SPH_SEED: per-target pass seeds (0/1 = off)
+  float seed_margin = 1.1f;  // SPH_SEEDM
+  DevBuf<uint32_t> seeds;
   int tshrink = 2;       // SPH_TSHRINK
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
@@ -154,6 +157,26 @@ __global__ void k_append_sgs(const int2 *tasks, const int *count, int4 *sgs, int
 __global__ void k_state_map(int n, uint8_t *state, uint8_t from, uint8_t to) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && state[i] == from) state[i] = to;
+}
+
+// seed targets for the per-target pass: every stride-th sorted position
+__global__ void k_seed_list(int ns, int stride, uint32_t *seeds, int *count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *count = ns;
+  if (i < ns) seeds[i] = (uint32_t)(i * stride);
+}
+
+// initial radius of the non-seed targets: margin x the larger converged h of
+// the two seeds around them (their own estimate when neither seed converged)
+__global__ void k_seed_radius(int n, int stride, const uint8_t *__restrict__ state, const double *__restrict__ d2k,
+                              float margin, float rmax, float *__restrict__ r0) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || p % stride == 0 || state[p] != ST_NEED_HIST) return;
+  const int s0 = p - p % stride, s1 = s0 + stride;
+  double h = 0.0;
+  if (state[s0] == ST_FINAL) h = d2k[s0];
+  if (s1 < n && state[s1] == ST_FINAL) h = fmax(h, d2k[s1]);
+  if (h > 0.0) r0[p] = fminf((float)sqrt(h) * margin, rmax);
 }
 
 __global__ void k_iota(int n, uint32_t *a) {
@@ -604,6 +627,22 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     if (i < 64) {
       ctx->kev_mode[i] = MODE_HIST;
       cudaEventRecord(ctx->kev[2 * i], ctx->stream);
+    }
+    if (ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
+      // seeds first (every seed_stride-th sorted position), then every other
+      // target starts from its neighbouring seeds' converged h (sorted
+      // neighbours are spatial neighbours): fewer regrows, tighter radii
+      const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
+      SPH_CK(ctx->seeds.ensure(ns));
+      k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
+      PassArgs sa = a;
+      sa.list = ctx->seeds.p;
+      sa.list_count = ctx->qints.p + 14;
+      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+      k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, ctx->state.p, ctx->d2k.p, ctx->seed_margin,
+                                                      rmax, ctx->r0.p);
+      SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+      launches += 3;
     }
     launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
     if (i < 64) {
@@ -1075,6 +1114,8 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
+  if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
+  if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
@@ -1095,7 +1136,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
