@@ -32,7 +32,14 @@ constexpr int kWarps = 4;
 constexpr int kHistOctaves = 12;
 constexpr int kHistBase = (127 - kHistOctaves) << 2;
 constexpr int NB_HIST = kHistOctaves * 4 + 2;
-constexpr int kHistStride = 17;  // words per bin row: 16-bit counters, two lanes per word (odd: conflict-free row sums)
+#ifndef SPH_HIST_ROW
+#define SPH_HIST_ROW 1
+#endif
+// SPH_HIST_ROW: one 32-bit counter per bin, updated with shared atomics (the
+// sums the shrink needs are then two loads per lane); else 16-bit per-lane
+// columns, two lanes per word, odd row stride (conflict-free column sums)
+constexpr int kHistStride = SPH_HIST_ROW ? 1 : 17;
+constexpr int kHistRegion = SPH_HIST_ROW ? 3328 : NB_HIST * 17 * 4;  // also holds the bracket doubles
 constexpr int kInCapMain = 256;     // in-bracket entries (alias the histogram, 3.4 KB)
 constexpr int kInCapCollect = 416;  // the collect instance has no histogram to keep
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
@@ -50,7 +57,7 @@ template <> struct Pos<false> { using T = D4; };
 constexpr int kStack = 448;  // traversal stack (node ids) per warp
 
 __host__ __device__ constexpr int warp_smem_bytes(int cap) {
-  return (32 + NB_HIST * kHistStride * 4 + cap * 8 + 2 * 32 * 4 + kStack * 4 + 15) & ~15;
+  return (32 + kHistRegion + cap * 8 + 2 * 32 * 4 + kStack * 4 + 15) & ~15;
 }
 
 
@@ -70,8 +77,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   unsigned char *wbase = smem_raw + wib * warp_smem_bytes(cap) + 32;
   unsigned *hist = reinterpret_cast<unsigned *>(wbase);
   double *inb = reinterpret_cast<double *>(wbase);  // after the histogram is read
-  uint2 *list = reinterpret_cast<uint2 *>(wbase + NB_HIST * kHistStride * 4);
-  int *spfx = reinterpret_cast<int *>(wbase + NB_HIST * kHistStride * 4 + cap * 8);
+  uint2 *list = reinterpret_cast<uint2 *>(wbase + kHistRegion);
+  int *spfx = reinterpret_cast<int *>(wbase + kHistRegion + cap * 8);
   int *sbase = spfx + 32;
   int *stk = sbase + 32;
   const PT *__restrict__ pos = reinterpret_cast<const PT *>(a.pos);
@@ -165,13 +172,18 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       // adaptive shrink from the column histogram; compacts the list
       auto shrink = [&]() {
         unsigned c0 = 0, c1 = 0;
+        if constexpr (SPH_HIST_ROW) {
+          c0 = hist[lane];
+          c1 = lane + 32 < NB_HIST ? hist[lane + 32] : 0u;
+        } else {
 #pragma unroll 4
-        for (int c = 0; c < kHistStride - 1; ++c) {
-          const unsigned w0 = hist[lane * kHistStride + c];
-          c0 += (w0 & 0xffffu) + (w0 >> 16);
-          if (lane + 32 < NB_HIST) {
-            const unsigned w1 = hist[(lane + 32) * kHistStride + c];
-            c1 += (w1 & 0xffffu) + (w1 >> 16);
+          for (int c = 0; c < kHistStride - 1; ++c) {
+            const unsigned w0 = hist[lane * kHistStride + c];
+            c0 += (w0 & 0xffffu) + (w0 >> 16);
+            if (lane + 32 < NB_HIST) {
+              const unsigned w1 = hist[(lane + 32) * kHistStride + c];
+              c1 += (w1 & 0xffffu) + (w1 >> 16);
+            }
           }
         }
         // inclusive prefix over bins 0..31 then 32..NB_HIST-1
@@ -354,7 +366,10 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
                 in = ad <= (double)h_r2;
                 af = (float)ad;
               }
-              if (!COLLECT && in) atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
+              if (!COLLECT && in) {
+                if constexpr (SPH_HIST_ROW) atomicAdd(&hist[hist_bin(af * h_inv)], 1u);
+                else atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
+              }
             }
             bool lst = in;
             if constexpr (COLLECT) {
@@ -413,13 +428,18 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       // ---- bracket of the K-th from the histogram (bin sums per lane) ----
       {
         unsigned c0 = 0, c1 = 0;
+        if constexpr (SPH_HIST_ROW) {
+          c0 = hist[lane];
+          c1 = lane + 32 < NB_HIST ? hist[lane + 32] : 0u;
+        } else {
 #pragma unroll 4
-        for (int c = 0; c < kHistStride - 1; ++c) {
-          const unsigned w0 = hist[lane * kHistStride + c];
-          c0 += (w0 & 0xffffu) + (w0 >> 16);
-          if (lane + 32 < NB_HIST) {
-            const unsigned w1 = hist[(lane + 32) * kHistStride + c];
-            c1 += (w1 & 0xffffu) + (w1 >> 16);
+          for (int c = 0; c < kHistStride - 1; ++c) {
+            const unsigned w0 = hist[lane * kHistStride + c];
+            c0 += (w0 & 0xffffu) + (w0 >> 16);
+            if (lane + 32 < NB_HIST) {
+              const unsigned w1 = hist[(lane + 32) * kHistStride + c];
+              c1 += (w1 & 0xffffu) + (w1 >> 16);
+            }
           }
         }
         if (lane == 0) c0 -= 1u;  // self, bin 0
