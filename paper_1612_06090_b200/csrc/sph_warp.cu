@@ -234,20 +234,35 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       }
       bool grow = false, done_unreach = false;
       for (int pass = 0; pass < 1; ++pass) {
-      const int ns = a.periodic ? 3 : 1;
-      for (int ix = 0; ix < ns; ++ix) {
-      const int sx = ix == 0 ? 0 : (ix == 1 ? -1 : 1);
-      const float gxs = sx == 0 ? gsq[0][1] : (sx < 0 ? gsq[0][0] : gsq[0][2]);
-      if (gxs * (1.0f - 4.0f * kEps) > h_r2) continue;
-      for (int iy = 0; iy < ns; ++iy) {
-      const int sy = iy == 0 ? 0 : (iy == 1 ? -1 : 1);
-      const float gys = sy == 0 ? gsq[1][1] : (sy < 0 ? gsq[1][0] : gsq[1][2]);
-      if ((gxs + gys) * (1.0f - 4.0f * kEps) > h_r2) continue;
-      for (int iz = 0; iz < ns; ++iz) {
-        const int sz = iz == 0 ? 0 : (iz == 1 ? -1 : 1);
-        const float gzs = sz == 0 ? gsq[2][1] : (sz < 0 ? gsq[2][0] : gsq[2][2]);
-        if ((gxs + gys + gzs) * (1.0f - 4.0f * kEps) > h_r2) continue;
-        const int sidx = a.periodic ? (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1) : 0;
+      // unshifted image first; then the shifted images whose root-box gap (one
+      // shift per lane, tested once after the unshifted walk) is within the radius
+      unsigned rest = 0u;
+      for (int it = 0;; ++it) {
+        int sidx = center;
+        if (it > 0) {
+          if (it == 1) {
+            bool want = false;
+            if (a.periodic && lane < 27 && lane != 13) {
+              const int lx = lane / 9, ly = (lane / 3) % 3, lz = lane % 3;
+              const float gx = lx == 1 ? gsq[0][1] : (lx == 0 ? gsq[0][0] : gsq[0][2]);
+              const float gy = ly == 1 ? gsq[1][1] : (ly == 0 ? gsq[1][0] : gsq[1][2]);
+              const float gz = lz == 1 ? gsq[2][1] : (lz == 0 ? gsq[2][0] : gsq[2][2]);
+              want = (gx + gy + gz) * (1.0f - 4.0f * kEps) <= h_r2;
+            }
+            rest = __ballot_sync(FULL, want);
+          }
+          if (!rest) break;
+          sidx = __ffs(rest) - 1;
+          rest &= rest - 1u;
+        }
+        const int sx = a.periodic ? sidx / 9 - 1 : 0, sy = a.periodic ? (sidx / 3) % 3 - 1 : 0,
+                  sz = a.periodic ? sidx % 3 - 1 : 0;
+        if (it > 0) {  // re-check with the radius as it is now
+          const float gx = sx == 0 ? gsq[0][1] : (sx < 0 ? gsq[0][0] : gsq[0][2]);
+          const float gy = sy == 0 ? gsq[1][1] : (sy < 0 ? gsq[1][0] : gsq[1][2]);
+          const float gz = sz == 0 ? gsq[2][1] : (sz < 0 ? gsq[2][0] : gsq[2][2]);
+          if ((gx + gy + gz) * (1.0f - 4.0f * kEps) > h_r2) continue;
+        }
         const bool shifted = (sx | sy | sz) != 0;
         const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
         // the target in the tree frame of this shift (x_i - s*box), plus slack
@@ -398,10 +413,6 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           if (!COLLECT && seen > K + 1 && seen - seen_shrunk >= (K >> a.tshrink)) shrink();
         }
         if (stack_over) break;
-      }
-      if (stack_over) break;
-      }
-      if (stack_over) break;
       }
       __syncwarp();
       if (a.dbg && fallbacks && lane == 0) atomicAdd(fallbacks + 3, 1);  // walks (debug)
