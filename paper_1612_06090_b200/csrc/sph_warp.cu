@@ -132,24 +132,17 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
     float R = a.radius[p];
     if (!(R > 0.f)) R = 1e-30f;
     const float slack0 = F32 ? 0.f : fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))) * 1.2e-7f;
-    // squared per-axis gap from x_i - s*box (s = -1, 0, +1) to the root box
-    float gsq[3][3];
-    {
+    // squared gap from the image frame x_i - s*box to the root box (the
+    // shifted walks are tested with it, one shift per lane)
+    auto image_gap2 = [&](int sx, int sy, int sz) {
       const float4 l4 = nlo[0], h4 = nhi[0];
-      const double t3[3] = {tx, ty, tz};
-      const float lo3[3] = {l4.x, l4.y, l4.z}, hi3[3] = {h4.x, h4.y, h4.z};
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-#pragma unroll
-        for (int si = 0; si < 3; ++si) {
-          const int sv = si - 1;
-          const float q = (float)(t3[d] - sv * a.box);
-          const float sl = sv ? boxf * 4.8e-7f : slack0;
-          const float g = fmaxf(fmaxf(lo3[d] - q, q - hi3[d]) - sl, 0.f);
-          gsq[d][si] = (a.periodic || sv == 0) ? g * g : INFINITY;
-        }
-      }
-    }
+      const float qx = (float)(tx - sx * a.box), qy = (float)(ty - sy * a.box), qz = (float)(tz - sz * a.box);
+      const float sl = boxf * 4.8e-7f;
+      const float gx = fmaxf(fmaxf(l4.x - qx, qx - h4.x) - sl, 0.f);
+      const float gy = fmaxf(fmaxf(l4.y - qy, qy - h4.y) - sl, 0.f);
+      const float gz = fmaxf(fmaxf(l4.z - qz, qz - h4.z) - sl, 0.f);
+      return (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps);
+    };
 
     // collect instance: phase 0 lists the bracket (counting what lies below it),
     // phase 1 lists everything within the selected h for the density
@@ -242,13 +235,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         if (it > 0) {
           if (it == 1) {
             bool want = false;
-            if (a.periodic && lane < 27 && lane != 13) {
-              const int lx = lane / 9, ly = (lane / 3) % 3, lz = lane % 3;
-              const float gx = lx == 1 ? gsq[0][1] : (lx == 0 ? gsq[0][0] : gsq[0][2]);
-              const float gy = ly == 1 ? gsq[1][1] : (ly == 0 ? gsq[1][0] : gsq[1][2]);
-              const float gz = lz == 1 ? gsq[2][1] : (lz == 0 ? gsq[2][0] : gsq[2][2]);
-              want = (gx + gy + gz) * (1.0f - 4.0f * kEps) <= h_r2;
-            }
+            if (a.periodic && lane < 27 && lane != 13)
+              want = image_gap2(lane / 9 - 1, (lane / 3) % 3 - 1, lane % 3 - 1) <= h_r2;
             rest = __ballot_sync(FULL, want);
           }
           if (!rest) break;
@@ -257,12 +245,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         }
         const int sx = a.periodic ? sidx / 9 - 1 : 0, sy = a.periodic ? (sidx / 3) % 3 - 1 : 0,
                   sz = a.periodic ? sidx % 3 - 1 : 0;
-        if (it > 0) {  // re-check with the radius as it is now
-          const float gx = sx == 0 ? gsq[0][1] : (sx < 0 ? gsq[0][0] : gsq[0][2]);
-          const float gy = sy == 0 ? gsq[1][1] : (sy < 0 ? gsq[1][0] : gsq[1][2]);
-          const float gz = sz == 0 ? gsq[2][1] : (sz < 0 ? gsq[2][0] : gsq[2][2]);
-          if ((gx + gy + gz) * (1.0f - 4.0f * kEps) > h_r2) continue;
-        }
+        if (it > 0 && image_gap2(sx, sy, sz) > h_r2) continue;  // re-check with the radius as it is now
         const bool shifted = (sx | sy | sz) != 0;
         const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
         // the target in the tree frame of this shift (x_i - s*box), plus slack
