@@ -139,6 +139,7 @@ struct PassArgs {
   int lshrink;              // shrink after every candidate chunk (not only per flush)
   int lcompact;             // compact the list at a shrink once it holds more entries than this
   int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
+  int static_sched;         // per-target kernel: strided static assignment instead of the atomic counter
   uint32_t *fb_list;        // per-target kernel: targets left for the collect instance (+ counter)
   int *fb_count;
 };

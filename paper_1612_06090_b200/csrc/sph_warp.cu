@@ -100,13 +100,24 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   // work in chunks of CH targets per atomic (the collect instance scans sparse
   // targets: whole warps of them)
   const int CH = (COLLECT && !a.list) ? 32 : 1;  // a compacted list: one target per grab
+  // static_sched: warp w takes targets w, w + W, ... (no atomic; sorted
+  // neighbours, whose costs are alike, land on different warps)
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  const bool stat = !COLLECT && a.static_sched;
+  int snext = gwarp;
   unsigned pend = 0u;
   int cbase = 0;
   for (;;) {
     if (!pend) {
       int t0 = 0;
-      if (lane == 0) t0 = atomicAdd(a.work_counter, CH);
-      t0 = __shfl_sync(FULL, t0, 0);
+      if (stat) {
+        t0 = snext;
+        snext += nwarp;
+      } else {
+        if (lane == 0) t0 = atomicAdd(a.work_counter, CH);
+        t0 = __shfl_sync(FULL, t0, 0);
+      }
       if (t0 >= count) break;
       cbase = t0;
       const int q = t0 + lane;
