@@ -89,6 +89,10 @@ struct sph_ctx {
   int seed_stride = 4;   // SPH_SEED: per-target pass seeds (0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
+  int cell_lists = 192;  // SPH_CLIST: neighbour-cell list capacity (0 = off)
+  DevBuf<float4> clist;
+  DevBuf<int> clen, cellidx, cellnode;
+  DevBuf<float> crad2;
   int tshrink = 2;       // SPH_TSHRINK
   int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
@@ -645,6 +649,30 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
                                                       rmax, ctx->r0.p);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       launches += 3;
+      if (ctx->cell_lists > 0) {
+        // neighbour-cell lists for the radii the seeds imply
+        const int cap = ctx->cell_lists;
+        SPH_CK(ctx->cellidx.ensure(n_nodes));
+        SPH_CK(ctx->cellnode.ensure(n_nodes));
+        SPH_CK(cudaMemsetAsync(ctx->qints.p + 13, 0, sizeof(int), ctx->stream));
+        launch_cell_index(ctx->stream, ctx->nlo.p, n_nodes, ctx->cellidx.p, ctx->cellnode.p, ctx->qints.p + 13);
+        int ncell = 0;
+        SPH_CK(cudaMemcpyAsync(&ncell, ctx->qints.p + 13, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        SPH_CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->clist.ensure(2 * (size_t)ncell * cap) == cudaSuccess && ctx->clen.ensure(ncell) == cudaSuccess &&
+            ctx->crad2.ensure(ncell) == cudaSuccess) {
+          launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->qints.p + 13, cap, ctx->clist.p, ctx->clen.p,
+                            ctx->crad2.p, ctx->num_sms);
+          a.clist = ctx->clist.p;
+          a.clen = ctx->clen.p;
+          a.crad2 = ctx->crad2.p;
+          a.cellidx = ctx->cellidx.p;
+          a.clcap = cap;
+          launches += 2;
+        } else {
+          cudaGetLastError();
+        }
+      }
     }
     launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
     if (i < 64) {
@@ -1117,6 +1145,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
+  if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);
@@ -1139,7 +1168,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

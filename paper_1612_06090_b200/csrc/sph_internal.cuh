@@ -140,6 +140,11 @@ struct PassArgs {
   int lcompact;             // compact the list at a shrink once it holds more entries than this
   int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
   int static_sched;         // per-target kernel: strided static assignment instead of the atomic counter
+  const float4 *clist;      // per-target kernel: neighbour-cell lists (child records) per cell, clcap each
+  const int *clen;          // list length per cell (-1: none)
+  const float *crad2;       // squared radius a cell's list covers
+  const int *cellidx;       // cell index of each node (-1: internal)
+  int clcap;
   uint32_t *fb_list;        // per-target kernel: targets left for the collect instance (+ counter)
   int *fb_count;
 };
@@ -241,6 +246,9 @@ int lists_max_cap();
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,
                    bool collect = false);
+void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells);
+void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
+                       float4 *clist, int *clen, float *crad2, int num_sms);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof);
 // per-cell initial search radius from the node sizes and the parent chain

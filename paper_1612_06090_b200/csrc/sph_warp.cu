@@ -277,8 +277,21 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         // children of hit internal nodes (child lists), stream the hit cells ----
         // unshifted: start at the lowest ancestor of the target's cell whose box
         // holds the whole search sphere (no cell outside it can be within R)
+        // a neighbour-cell list of the target's own cell (built for the radius
+        // its seeds imply) replaces the unshifted traversal when it covers R
+        int lbase = -1, llen = 0;
+        if (!shifted && a.clist) {
+          const int ci = a.cellidx[a.tree.cellof[p]];
+          if (ci >= 0) {
+            const int len = a.clen[ci];
+            if (len >= 0 && h_r2 <= a.crad2[ci]) {
+              lbase = ci * a.clcap;
+              llen = len;
+            }
+          }
+        }
         int start = a.tree.root_start;
-        if (!shifted) {
+        if (!shifted && lbase < 0) {
           const int4 an = a.tree.anc4[a.tree.cellof[p]];
           const float rr = sqrtf(h_r2) * (1.0f + 8.0f * kEps) + pslack;
           const int my_anc = lane == 0 ? an.x : lane == 1 ? an.y : lane == 2 ? an.z : lane == 3 ? an.w : -1;
@@ -294,18 +307,24 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         // the stack holds hit internal nodes; a step expands up to 4 of them,
         // one child record per lane (8 slots each: box + node id or cell range)
         if (lane == 0) stk[0] = start;
-        int top = 1;
+        int top = lbase < 0 ? 1 : 0, li = 0;
         __syncwarp();
-        while (top > 0) {
-          const int np = min(top, 4);
-          top -= np;
-          const int pi = lane >> 3;
-          const int par = pi < np ? stk[top + pi] : -1;
-          __syncwarp();
+        while (lbase >= 0 ? li < llen : top > 0) {
+          const float4 *rec = nullptr;
+          if (lbase >= 0) {  // 32 listed cells per step
+            if (li + lane < llen) rec = a.clist + 2 * ((size_t)lbase + li + lane);
+            li += 32;
+          } else {
+            const int np = min(top, 4);
+            top -= np;
+            const int pi = lane >> 3;
+            const int par = pi < np ? stk[top + pi] : -1;
+            __syncwarp();
+            if (par >= 0) rec = a.tree.crec + 16 * (size_t)par + 2 * (lane & 7);
+          }
           bool hit = false, is_cell = false;
           int node = -1, my_start = 0, my_end = 0;
-          if (par >= 0) {
-            const float4 *rec = a.tree.crec + 16 * (size_t)par + 2 * (lane & 7);
+          if (rec) {
             const float4 l4 = rec[0], h4 = rec[1];
             const int code = __float_as_int(l4.w);
             is_cell = code < 0;
@@ -740,7 +759,108 @@ __global__ void k_r0(const float4 *__restrict__ nlo, const float4 *__restrict__ 
   for (int q = s0; q < e0; ++q) r0[q] = R;
 }
 
+// Neighbour-cell lists (per-target path, after the seeds): for every cell with
+// targets still to search, D = the largest initial radius of its targets and
+// the list of every cell whose box lies within D of its box (the child
+// records of those cells).  Any particle within D of a target of the cell is
+// in a listed cell.  len = -1: no list (no targets, or more than cap cells).
+__global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi,
+                                                    const float4 *__restrict__ crec, const int *__restrict__ cellnode,
+                                                    const int *__restrict__ ncells, const uint8_t *__restrict__ state,
+                                                    const float *__restrict__ r0, int n_nodes, int n, int root_start,
+                                                    int cap, float4 *__restrict__ clist, int *__restrict__ clen,
+                                                    float *__restrict__ crad2) {
+  __shared__ int s_stk[4][kStack];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int *stk = s_stk[wib];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int nc = *ncells;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int ci = gw; ci < nc; ci += nw) {
+    const int c = cellnode[ci];
+    const float4 cl = nlo[c], chh = nhi[c];
+    const int s0 = __float_as_int(chh.w);
+    const int e0 = c + 1 < n_nodes ? __float_as_int(nhi[c + 1].w) : n;
+    float D = 0.f;
+    for (int q = s0 + lane; q < e0; q += 32)
+      if (state[q] == ST_NEED_HIST) D = fmaxf(D, r0[q]);
+    for (int o = 16; o; o >>= 1) D = fmaxf(D, __shfl_xor_sync(FULL, D, o));
+    if (!(D > 0.f)) {
+      if (lane == 0) clen[ci] = -1;
+      continue;
+    }
+    const float D2 = D * D * (1.0f + 16.0f * kEps);
+    int len = 0;
+    if (lane == 0) stk[0] = root_start;
+    int top = 1;
+    bool over = false;
+    __syncwarp();
+    while (top > 0) {
+      const int np = min(top, 4);
+      top -= np;
+      const int pi = lane >> 3;
+      const int par = pi < np ? stk[top + pi] : -1;
+      __syncwarp();
+      bool hit = false, is_cell = false;
+      float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), h4 = l4;
+      if (par >= 0) {
+        const float4 *rec = crec + 16 * (size_t)par + 2 * (lane & 7);
+        l4 = rec[0];
+        h4 = rec[1];
+        is_cell = __float_as_int(l4.w) < 0;
+        const float gx = fmaxf(fmaxf(l4.x - chh.x, cl.x - h4.x), 0.f);
+        const float gy = fmaxf(fmaxf(l4.y - chh.y, cl.y - h4.y), 0.f);
+        const float gz = fmaxf(fmaxf(l4.z - chh.z, cl.z - h4.z), 0.f);
+        hit = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= D2;
+      }
+      const unsigned pm = __ballot_sync(FULL, hit && !is_cell);
+      if (top + __popc(pm) > kStack) { over = true; break; }
+      if (hit && !is_cell) stk[top + __popc(pm & lt)] = __float_as_int(l4.w);
+      top += __popc(pm);
+      const unsigned cm = __ballot_sync(FULL, hit && is_cell);
+      if (len + __popc(cm) > cap) { over = true; break; }
+      if (hit && is_cell) {
+        float4 *dst = clist + 2 * ((size_t)ci * cap + len + __popc(cm & lt));
+        dst[0] = l4;
+        dst[1] = h4;
+      }
+      len += __popc(cm);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      clen[ci] = over ? -1 : len;
+      crad2[ci] = D * D;
+    }
+  }
+}
+
+// cell index of every node (-1 for internal nodes) and the node of every cell
+__global__ void k_cell_index(const float4 *__restrict__ nlo, int n_nodes, int *__restrict__ cellidx,
+                             int *__restrict__ cellnode, int *__restrict__ ncells) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_nodes) return;
+  if (__float_as_int(nlo[k].w) == k + 1) {
+    const int ci = atomicAdd(ncells, 1);
+    cellidx[k] = ci;
+    cellnode[ci] = k;
+  } else {
+    cellidx[k] = -1;
+  }
+}
+
 }  // namespace
+
+void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells) {
+  k_cell_index<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, n_nodes, cellidx, cellnode, ncells);
+}
+
+void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
+                       float4 *clist, int *clen, float *crad2, int num_sms) {
+  k_cell_lists<<<num_sms * 8, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
+                                           a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen, crad2);
+}
 
 void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *nsize, const int *parent, int n_nodes,
                int n, int k, float r0_scale, float rmax, float root_side, float *r0) {
