@@ -86,7 +86,7 @@ struct sph_ctx {
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
-  int seed_stride = 4;   // SPH_SEED: per-target pass seeds (0/1 = off)
+  int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int cell_lists = 192;  // SPH_CLIST: neighbour-cell list capacity (0 = off)
