@@ -767,8 +767,9 @@ __global__ void k_r0(const float4 *__restrict__ nlo, const float4 *__restrict__ 
 __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ nlo, const float4 *__restrict__ nhi,
                                                     const float4 *__restrict__ crec, const int *__restrict__ cellnode,
                                                     const int *__restrict__ ncells, const uint8_t *__restrict__ state,
-                                                    const float *__restrict__ r0, int n_nodes, int n, int root_start,
-                                                    int cap, float4 *__restrict__ clist, int *__restrict__ clen,
+                                                    const float *__restrict__ r0, const int4 *__restrict__ anc4,
+                                                    int n_nodes, int n, int root_start, int cap,
+                                                    float4 *__restrict__ clist, int *__restrict__ clen,
                                                     float *__restrict__ crad2) {
   __shared__ int s_stk[4][kStack];
   const int lane = threadIdx.x & 31;
@@ -792,8 +793,24 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
       continue;
     }
     const float D2 = D * D * (1.0f + 16.0f * kEps);
+    // start at the lowest of the first four ancestors whose box holds the
+    // cell box grown by D (nothing outside it is within D)
+    int start = root_start;
+    {
+      const int4 an = anc4[c];
+      const float Dm = D * (1.0f + 8.0f * kEps);
+      const int my_anc = lane == 0 ? an.x : lane == 1 ? an.y : lane == 2 ? an.z : lane == 3 ? an.w : -1;
+      bool holds = false;
+      if (my_anc >= 0) {
+        const float4 l4 = nlo[my_anc], h4 = nhi[my_anc];
+        holds = l4.x <= cl.x - Dm && chh.x + Dm <= h4.x && l4.y <= cl.y - Dm && chh.y + Dm <= h4.y &&
+                l4.z <= cl.z - Dm && chh.z + Dm <= h4.z;
+      }
+      const unsigned hm = __ballot_sync(FULL, holds);
+      if (hm) start = __shfl_sync(FULL, my_anc, __ffs(hm) - 1);
+    }
     int len = 0;
-    if (lane == 0) stk[0] = root_start;
+    if (lane == 0) stk[0] = start;
     int top = 1;
     bool over = false;
     __syncwarp();
@@ -859,7 +876,8 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
                        float4 *clist, int *clen, float *crad2, int num_sms) {
   k_cell_lists<<<num_sms * 8, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
-                                           a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen, crad2);
+                                           a.tree.anc4, a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen,
+                                           crad2);
 }
 
 void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *nsize, const int *parent, int n_nodes,
