@@ -618,8 +618,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-  SPH_CK(ctx->qints.ensure(16));
-  SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 16 * sizeof(int), ctx->stream));
+  SPH_CK(ctx->qints.ensure(32));
+  SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 32 * sizeof(int), ctx->stream));
   PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
   rc = prepare_target_tree(ctx, n, n_nodes, a);
   if (rc) return rc;
@@ -708,10 +708,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     c.list = ctx->list.p;
     c.list_count = ctx->qints.p + 15;
     c.fb_list = nullptr;
-    launch_target(ctx->stream, compute_f32, c, 1024, ctx->qints.p + 10, ctx->num_sms, true);
+    launch_target(ctx->stream, compute_f32, c, 1024, ctx->qints.p + 16, ctx->num_sms, true);
     ++launches;
     int q2[5];
-    SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 10, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));
+    SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 16, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));
     SPH_CK(cudaStreamSynchronize(ctx->stream));
     coll_left = q2[0] + q2[1] + q2[4];
     if (ctx->debug)
@@ -749,7 +749,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     SPH_CK(ctx->owner.ensure(n));
     SPH_CK(ctx->v3scratch.ensure(v3_scratch_ints(ctx->num_sms)));
     if (ctx->lpool.ensure(std::min(list_cap, (size_t)INT32_MAX / 2)) != cudaSuccess) SPH_CK(ctx->lpool.ensure(1 << 22));
-    SPH_CK(ctx->qints.ensure(16));
+    SPH_CK(ctx->qints.ensure(32));
     cudaStream_t s = ctx->stream;
     k_init_state<<<nblk(n), kTB, 0, s>>>(n, n_targets, ctx->perm.p, ctx->state.p);
     k_iota<<<nblk(n), kTB, 0, s>>>(n, ctx->iota.p);
@@ -860,7 +860,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   {
     const int item_cap = 2 * n + 65536, pool_cap = 4 * n + 65536;
     if (ctx->items.ensure(item_cap) == cudaSuccess && ctx->pool.ensure(pool_cap) == cudaSuccess &&
-        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(16) == cudaSuccess) {
+        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(32) == cudaSuccess) {
       k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
       SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
       PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
@@ -905,7 +905,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (ctx->lists && ctx->list_mult > 0 && n <= (1 << 27)) {
     const size_t cap = std::min((size_t)ctx->list_mult * (size_t)k, (size_t)lists_max_cap());
     if (ctx->nlists.ensure(cap * (size_t)n) == cudaSuccess && ctx->ncount.ensure(n) == cudaSuccess &&
-        ctx->qints.ensure(16) == cudaSuccess) {
+        ctx->qints.ensure(32) == cudaSuccess) {
       a.nlists = ctx->nlists.p;
       a.ncount = ctx->ncount.p;
       a.ncap = (int)cap;
@@ -930,7 +930,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     t.list = ctx->list.p;
     t.ncount = a.ncount;
     SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-    SPH_CK(ctx->qints.ensure(16));
+    SPH_CK(ctx->qints.ensure(32));
     const int i = ctx->n_kev;
     if (i < 64) {
       ctx->kev_mode[i] = MODE_HIST;
