@@ -29,17 +29,17 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWarps = 4;
-constexpr int kHistOctaves = 12;
-constexpr int kHistBase = (127 - kHistOctaves) << 2;
-constexpr int NB_HIST = kHistOctaves * 4 + 2;
-#ifndef SPH_HIST_ROW
-#define SPH_HIST_ROW 1
+#ifndef SPH_HIST_BPO_LOG2
+#define SPH_HIST_BPO_LOG2 3
 #endif
-// SPH_HIST_ROW: one 32-bit counter per bin, updated with shared atomics (the
-// sums the shrink needs are then two loads per lane); else 16-bit per-lane
-// columns, two lanes per word, odd row stride (conflict-free column sums)
-constexpr int kHistStride = SPH_HIST_ROW ? 1 : 17;
-constexpr int kHistRegion = SPH_HIST_ROW ? 3328 : NB_HIST * 17 * 4;  // also holds the bracket doubles
+constexpr int kHistOctaves = 12;
+constexpr int kBinBits = SPH_HIST_BPO_LOG2;           // log2 bins per octave of d2 / R^2
+constexpr int kHistBase = (127 - kHistOctaves) << kBinBits;
+constexpr int NB_HIST = (kHistOctaves << kBinBits) + 2;  // <= 128: four bins per lane
+constexpr int kBinShift = 23 - kBinBits;
+// one 32-bit counter per bin, updated with shared atomics; the region also
+// holds the in-bracket doubles of the select
+constexpr int kHistRegion = 3328;
 constexpr int kInCapMain = 256;     // in-bracket entries (alias the histogram, 3.4 KB)
 constexpr int kInCapCollect = 416;  // the collect instance has no histogram to keep
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
@@ -62,7 +62,7 @@ __host__ __device__ constexpr int warp_smem_bytes(int cap) {
 
 
 __device__ __forceinline__ int hist_bin(float x) {  // x = d2 / R^2
-  return min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
+  return min(max((__float_as_int(x) >> kBinShift) - kHistBase + 1, 0), NB_HIST - 1);
 }
 
 // COLLECT: second instance for the targets whose list overflowed in the main
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       const float h_inv = 1.0f / hR2;
       float h_r2 = hR2;  // current acceptance radius^2 (shrinks)
       if (!COLLECT)
-        for (int bb = lane; bb < NB_HIST * kHistStride; bb += 32) hist[bb] = 0u;
+        for (int bb = lane; bb < NB_HIST; bb += 32) hist[bb] = 0u;
       int seen = 0, seen_shrunk = 0;  // warp-uniform: counted candidates (self included)
       int ne = 0;                     // warp-uniform: list entries
       bool over = false;              // list overflowed: no list-based select
@@ -174,34 +174,41 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       __syncwarp();
 
       // adaptive shrink from the column histogram; compacts the list
-      auto shrink = [&]() {
-        unsigned c0 = 0, c1 = 0;
-        if constexpr (SPH_HIST_ROW) {
-          c0 = hist[lane];
-          c1 = lane + 32 < NB_HIST ? hist[lane + 32] : 0u;
-        } else {
-#pragma unroll 4
-          for (int c = 0; c < kHistStride - 1; ++c) {
-            const unsigned w0 = hist[lane * kHistStride + c];
-            c0 += (w0 & 0xffffu) + (w0 >> 16);
-            if (lane + 32 < NB_HIST) {
-              const unsigned w1 = hist[(lane + 32) * kHistStride + c];
-              c1 += (w1 & 0xffffu) + (w1 >> 16);
-            }
+      // first bin whose cumulative count (bin 0 less `sub`) exceeds T; four
+      // consecutive bins per lane, one scan (NB_HIST when none)
+      auto first_bin_over = [&](int T, unsigned sub) -> int {
+        unsigned c[4], sum = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int b = 4 * lane + u;
+          c[u] = b < NB_HIST ? hist[b] : 0u;
+          if (b == 0) c[u] -= sub;
+          sum += c[u];
+        }
+        unsigned incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const unsigned excl = incl - sum;
+        const bool here = (int)incl > T && (int)excl <= T;
+        int bin = NB_HIST;
+        if (here) {
+          unsigned cum = excl;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cum += c[u];
+            if ((int)cum > T && bin == NB_HIST) bin = 4 * lane + u;
           }
         }
-        // inclusive prefix over bins 0..31 then 32..NB_HIST-1
-        unsigned s0 = c0, s1 = c1;
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned v0 = __shfl_up_sync(FULL, s0, o), v1 = __shfl_up_sync(FULL, s1, o);
-          if (lane >= o) { s0 += v0; s1 += v1; }
-        }
-        s1 += __shfl_sync(FULL, s0, 31);
-        const unsigned m0 = __ballot_sync(FULL, (int)s0 > K);
-        const unsigned m1 = __ballot_sync(FULL, (int)s1 > K && lane + 32 < NB_HIST);
-        const int bb = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : NB_HIST);
+        const unsigned hm = __ballot_sync(FULL, here);
+        return hm ? __shfl_sync(FULL, bin, __ffs(hm) - 1) : NB_HIST;
+      };
+      // adaptive shrink from the histogram (K others + self counted); compacts the list
+      auto shrink = [&]() {
+        const int bb = first_bin_over(K, 0u);
         if (bb < NB_HIST - 1) {
-          const float edge = __int_as_float((kHistBase + bb) << 21) * hR2 * (1.0f + 4.0f * kEps);
+          const float edge = __int_as_float((kHistBase + bb) << kBinShift) * hR2 * (1.0f + 4.0f * kEps);
           if (edge < h_r2) {
             h_r2 = edge;
             if (!over && ne > K) {
@@ -394,10 +401,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
                 in = ad <= (double)h_r2;
                 af = (float)ad;
               }
-              if (!COLLECT && in) {
-                if constexpr (SPH_HIST_ROW) atomicAdd(&hist[hist_bin(af * h_inv)], 1u);
-                else atomicAdd(&hist[hist_bin(af * h_inv) * kHistStride + (lane >> 1)], 1u << ((lane & 1) << 4));
-              }
+              if (!COLLECT && in) atomicAdd(&hist[hist_bin(af * h_inv)], 1u);
             }
             bool lst = in;
             if constexpr (COLLECT) {
@@ -449,43 +453,20 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         break;
       }
 
-      // ---- bracket of the K-th from the histogram (bin sums per lane) ----
+      // ---- bracket of the K-th from the histogram ----
       {
-        unsigned c0 = 0, c1 = 0;
-        if constexpr (SPH_HIST_ROW) {
-          c0 = hist[lane];
-          c1 = lane + 32 < NB_HIST ? hist[lane + 32] : 0u;
-        } else {
-#pragma unroll 4
-          for (int c = 0; c < kHistStride - 1; ++c) {
-            const unsigned w0 = hist[lane * kHistStride + c];
-            c0 += (w0 & 0xffffu) + (w0 >> 16);
-            if (lane + 32 < NB_HIST) {
-              const unsigned w1 = hist[(lane + 32) * kHistStride + c];
-              c1 += (w1 & 0xffffu) + (w1 >> 16);
-            }
-          }
-        }
-        if (lane == 0) c0 -= 1u;  // self, bin 0
-        unsigned s0 = c0, s1 = c1;
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned v0 = __shfl_up_sync(FULL, s0, o), v1 = __shfl_up_sync(FULL, s1, o);
-          if (lane >= o) { s0 += v0; s1 += v1; }
-        }
-        s1 += __shfl_sync(FULL, s0, 31);
-        const unsigned m0 = __ballot_sync(FULL, (int)s0 >= K);
-        const unsigned m1 = __ballot_sync(FULL, (int)s1 >= K && lane + 32 < NB_HIST);
-        const int bb = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : NB_HIST - 1);
+        const int bb0 = first_bin_over(K - 1, 1u);  // cumulative others >= K
+        const int bb = bb0 < NB_HIST ? bb0 : NB_HIST - 1;
         const double R2d = (double)hR2;
         if (bb == 0) {
           tl = 0.0;
-          th = (double)__int_as_float(kHistBase << 21) * R2d * (1.0 + 8.0 * kEpsD);
+          th = (double)__int_as_float(kHistBase << kBinShift) * R2d * (1.0 + 8.0 * kEpsD);
         } else if (bb >= NB_HIST - 1) {
           tl = R2d * (1.0 - 8.0 * kEpsD);
           th = R2d * (1.0 + 8.0 * kEpsD);
         } else {
-          tl = (double)__int_as_float((kHistBase + bb - 1) << 21) * R2d * (1.0 - 8.0 * kEpsD);
-          th = (double)__int_as_float((kHistBase + bb) << 21) * R2d * (1.0 + 8.0 * kEpsD);
+          tl = (double)__int_as_float((kHistBase + bb - 1) << kBinShift) * R2d * (1.0 - 8.0 * kEpsD);
+          th = (double)__int_as_float((kHistBase + bb) << kBinShift) * R2d * (1.0 + 8.0 * kEpsD);
         }
         // the list holds every candidate with d2 <= h_r2 (2^-20 guard)
         th = fmin(th, (double)h_r2 * (1.0 - 4.0 * kEpsD));
