@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   int snext = gwarp;
   unsigned pend = 0u;
   int cbase = 0;
+  // the next chunk's index is requested while the current one is processed
+  // (the atomic's latency hides behind a whole target)
+  int t_pref = 0;
+  if (!stat && lane == 0) t_pref = atomicAdd(a.work_counter, CH);
   for (;;) {
     if (!pend) {
       int t0 = 0;
@@ -115,8 +119,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         t0 = snext;
         snext += nwarp;
       } else {
-        if (lane == 0) t0 = atomicAdd(a.work_counter, CH);
-        t0 = __shfl_sync(FULL, t0, 0);
+        t0 = __shfl_sync(FULL, t_pref, 0);
+        if (lane == 0 && t0 < count) t_pref = atomicAdd(a.work_counter, CH);
       }
       if (t0 >= count) break;
       cbase = t0;
