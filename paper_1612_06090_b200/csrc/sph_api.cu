@@ -89,6 +89,7 @@ struct sph_ctx {
   int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
+  int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
   int cell_lists = 192;  // SPH_CLIST: neighbour-cell list capacity (0 = off)
   DevBuf<float4> clist;
   DevBuf<int> clen, cellidx, cellnode;
@@ -708,7 +709,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     c.list = ctx->list.p;
     c.list_count = ctx->qints.p + 15;
     c.fb_list = nullptr;
-    launch_target(ctx->stream, compute_f32, c, 1024, ctx->qints.p + 16, ctx->num_sms, true);
+    launch_target(ctx->stream, compute_f32, c, ctx->collect_cap, ctx->qints.p + 16, ctx->num_sms, true);
     ++launches;
     int q2[5];
     SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 16, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));
@@ -993,7 +994,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       use_target_tree(ctx, n_nodes, t);
       t.ncount = ctx->ncount.p;
       SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-      launch_target(ctx->stream, compute_f32, t, 1024, nullptr, ctx->num_sms, true);
+      launch_target(ctx->stream, compute_f32, t, ctx->collect_cap, nullptr, ctx->num_sms, true);
       ++launches;
     }
   }
@@ -1146,6 +1147,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
+  if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);

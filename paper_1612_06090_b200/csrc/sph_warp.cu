@@ -160,15 +160,20 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
     };
 
     // collect instance: phase 0 lists the bracket (counting what lies below it),
-    // phase 1 lists everything within the selected h for the density
-    int cphase = 0;
-    double d2k_c = 0.0;
+    // phase 1 lists everything within the selected h for the density; phase 2
+    // (a bracket too crowded to list) counts it in 32 sub-bins and narrows it
+    int cphase = 0, nrefine = 0;
+    double d2k_c = 0.0, ctl = 0.0, cth = 0.0;
+    if constexpr (COLLECT) {
+      ctl = a.t_lo[p];
+      cth = a.t_hi[p];
+    }
     for (;;) {  // grow loop
-      const float hR2 = COLLECT ? (float)(__double2float_ru((cphase ? d2k_c : a.t_hi[p]) * (1.0 + kEpsD)) + 1e-37f)
+      const float hR2 = COLLECT ? (float)(__double2float_ru((cphase == 1 ? d2k_c : cth) * (1.0 + kEpsD)) + 1e-37f)
                                 : R * R;
       const float h_inv = 1.0f / hR2;
       float h_r2 = hR2;  // current acceptance radius^2 (shrinks)
-      if (!COLLECT)
+      if (!COLLECT || cphase == 2)
         for (int bb = lane; bb < NB_HIST; bb += 32) hist[bb] = 0u;
       int seen = 0, seen_shrunk = 0;  // warp-uniform: counted candidates (self included)
       int ne = 0;                     // warp-uniform: list entries
@@ -242,10 +247,13 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
       double tl = 0.0, th = 0.0;
       float lo_c = -1.f;  // collect: candidates below the bracket are counted, not listed
       int cbelow = 0;
+      float rinv_c = 0.f;  // phase 2: sub-bins per unit fp32 d2
       if constexpr (COLLECT) {
-        tl = a.t_lo[p];
-        th = a.t_hi[p];
+        tl = ctl;
+        th = cth;
         lo_c = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
+        const float hi_c = __double2float_ru(th * (1.0 + kEpsD)) + 1e-37f;
+        rinv_c = 32.0f / fmaxf(hi_c - lo_c, 1e-37f);
       }
       bool grow = false, done_unreach = false;
       for (int pass = 0; pass < 1; ++pass) {
@@ -413,6 +421,13 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
                 ++cbelow;
                 lst = false;
               }
+              if (cphase == 2) {
+                if (in && !(j == p && sidx == center)) {
+                  if (af < lo_c) ++cbelow;
+                  else atomicAdd(&hist[min(max((int)((af - lo_c) * rinv_c), 0), 31)], 1u);
+                }
+                lst = false;
+              }
             }
             int nin = __popc(__ballot_sync(FULL, in));
             seen += nin;
@@ -493,6 +508,33 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           if (!COLLECT && a.fb_list) a.fb_list[atomicAdd(a.fb_count, 1)] = (uint32_t)p;
         }
       };
+      if constexpr (COLLECT) {
+        if (cphase == 2) {
+          // the sub-bin holding the K-th (fp32 d2; the exact select re-checks)
+          const int below_c = (int)__reduce_add_sync(FULL, (unsigned)cbelow);
+          const int rr = K - below_c;
+          const unsigned cnt = hist[lane];
+          unsigned incl = cnt;
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const unsigned hm = __ballot_sync(FULL, rr >= 1 && (int)incl >= rr);
+          if (!hm || nrefine >= 6) { ++fb_over; fallback(); break; }
+          const int sb = __ffs(hm) - 1;
+          const double w = 1.0 / (double)rinv_c;
+          ctl = fmax(ctl, ((double)lo_c + sb * w) * (1.0 - 4.0 * kEpsD));
+          cth = fmin(cth, ((double)lo_c + (sb + 1) * w) * (1.0 + 4.0 * kEpsD));
+          if (!(cth > ctl)) cth = ctl;
+          cphase = 0;
+          ++nrefine;
+          continue;
+        }
+        if (over && cphase == 0 && nrefine < 6) {  // too crowded to list: narrow it first
+          cphase = 2;
+          continue;
+        }
+      }
       if (over) { ++fb_over; fallback(); break; }
 
       double d2k;

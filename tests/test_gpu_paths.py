@@ -22,6 +22,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CONFIGS = {
     "per_target": {},
     "per_target_small_lists": {"SPH_TLISTCAP": "1"},
+    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
+    "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
     "hybrid_bundle_then_per_target": {"SPH_WARP": "0", "SPH_HYBRID": "1"},
     "hybrid_small_lists": {"SPH_WARP": "0", "SPH_HYBRID": "1", "SPH_LISTCAP": "1", "SPH_TLISTCAP": "1"},
     "bundle_rounds_with_lists": {"SPH_WARP": "0", "SPH_HYBRID": "0"},
