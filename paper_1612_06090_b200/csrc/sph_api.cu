@@ -90,6 +90,9 @@ struct sph_ctx {
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
+  cudaStream_t stream2 = nullptr;  // side stream for host-to-device copies the first kernels do not need
+  cudaEvent_t ev_side_start = nullptr, ev_mass = nullptr, ev_h = nullptr;
+  cudaEvent_t in_mass_ready = nullptr, in_h_ready = nullptr;  // set only during a host-API pass
   int cell_lists = 192;  // SPH_CLIST: neighbour-cell list capacity (0 = off)
   DevBuf<float4> clist;
   DevBuf<int> clen, cellidx, cellnode;
@@ -342,6 +345,7 @@ int stage_root(sph_ctx *ctx, int n, int precision, const void *x, const void *y,
 int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *x, const void *y, const void *z,
                const double *mass, int k, float rmax, int *n_nodes, int *launches, bool search_tree) {
   TreeBuffers tb = tree_buffers(ctx);
+  tb.mass_ready = ctx->in_mass_ready;
   // the per-target path derives R0 from the node sizes (k_r0) instead
   tb.emit_r0 = (ctx->warp && !ctx->fused && n <= (1 << 27)) ? 0 : 1;
   ctx->tb_emit_r0 = tb.emit_r0;
@@ -1012,6 +1016,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
   const unsigned long long bad_init = ~0ull;
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->in_h_ready) cudaStreamWaitEvent(ctx->stream, ctx->in_h_ready, 0);  // h0 copied on the side stream
   k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
       n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out, rounds_hist,
       ctx->stats.p + 2);
@@ -1128,6 +1133,10 @@ int sph_ctx_create(sph_ctx **out, int device) {
   sph_ctx *c = new sph_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_side_start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_mass, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_h, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return SPH_CUDA_ERROR;
@@ -1175,6 +1184,9 @@ void sph_ctx_destroy(sph_ctx *c) {
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
+  for (cudaEvent_t e : {c->ev_side_start, c->ev_mass, c->ev_h})
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -1296,11 +1308,23 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(h2d_strided(ctx->in_x.p, x, es, pos_stride, n, s));
   SPH_CK(h2d_strided(ctx->in_y.p, y, es, pos_stride, n, s));
   SPH_CK(h2d_strided(ctx->in_z.p, z, es, pos_stride, n, s));
-  SPH_CK(h2d_strided(ctx->in_m.p, mass, 8, mass_stride, n, s));
+  // masses and initial h on the side stream: they overlap the key / sort /
+  // tree kernels that only need positions (the pass waits on the events)
   const int64_t nt = prm->n_targets > 0 ? prm->n_targets : n;
-  SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, nt, s));
+  cudaStream_t s2 = ctx->stream2;
+  SPH_CK(cudaEventRecord(ctx->ev_side_start, s));
+  SPH_CK(cudaStreamWaitEvent(s2, ctx->ev_side_start, 0));  // reuse of the staging buffers is ordered
+  SPH_CK(h2d_strided(ctx->in_m.p, mass, 8, mass_stride, n, s2));
+  SPH_CK(cudaEventRecord(ctx->ev_mass, s2));
+  SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, nt, s2));
+  SPH_CK(cudaEventRecord(ctx->ev_h, s2));
+  ctx->in_mass_ready = ctx->ev_mass;
+  ctx->in_h_ready = ctx->ev_h;
   rc = density_pass_dev(ctx, prm, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, ctx->hfix.p, ctx->io_h.p,
                         ctx->out_rho.p, ctx->out_flags.p, st, tm);
+  ctx->in_mass_ready = nullptr;
+  ctx->in_h_ready = nullptr;
+  SPH_CK(cudaStreamWaitEvent(s, ctx->ev_h, 0));  // error paths: the side copies are done before returning
   if (rc == SPH_OK) {
     SPH_CK(d2h_strided(h, ctx->io_h.p, 8, h_stride, nt, s));
     SPH_CK(d2h_strided(rho, ctx->out_rho.p, 8, rho_stride, nt, s));

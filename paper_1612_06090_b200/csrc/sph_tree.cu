@@ -437,6 +437,7 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
                       const void *x, const void *y, const void *z, const double *mass, int k, float rmax,
                       int *launches) {
   const bool in32 = precision_in == 1;
+  if (tb.mass_ready) cudaStreamWaitEvent(s, tb.mass_ready, 0);  // masses copied on a side stream
   if (compute_f32) {
     if (in32)
       k_gather_f32<float><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const float *)x, (const float *)y,
