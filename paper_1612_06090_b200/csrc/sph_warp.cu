@@ -39,9 +39,12 @@ constexpr int NB_HIST = (kHistOctaves << kBinBits) + 2;  // <= 128: four bins pe
 constexpr int kBinShift = 23 - kBinBits;
 // one 32-bit counter per bin, updated with shared atomics; the region also
 // holds the in-bracket doubles of the select
-constexpr int kHistRegion = 3328;
-constexpr int kInCapMain = 256;     // in-bracket entries (alias the histogram, 3.4 KB)
-constexpr int kInCapCollect = 416;  // the collect instance has no histogram to keep
+#ifndef SPH_HIST_REGION
+#define SPH_HIST_REGION 1024
+#endif
+constexpr int kHistRegion = SPH_HIST_REGION;
+constexpr int kInCapMain = kHistRegion / 8 < 256 ? kHistRegion / 8 : 256;  // in-bracket entries (alias the histogram)
+constexpr int kInCapCollect = kHistRegion / 8;  // the collect instance has no histogram to keep
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_pass.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
 constexpr unsigned kNaNf = 0x7fc00000u;
@@ -54,7 +57,10 @@ template <> struct Pos<false> { using T = D4; };
 #ifndef SPH_TARGET_MINB
 #define SPH_TARGET_MINB 7
 #endif
-constexpr int kStack = 448;  // traversal stack (node ids) per warp
+#ifndef SPH_STACK
+#define SPH_STACK 256
+#endif
+constexpr int kStack = SPH_STACK;  // traversal stack (node ids) per warp
 
 __host__ __device__ constexpr int warp_smem_bytes(int cap) {
   return (32 + kHistRegion + cap * 8 + 2 * 32 * 4 + kStack * 4 + 15) & ~15;
@@ -584,6 +590,12 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           // R: search again with a slightly larger radius
           R = fminf(R * 1.26f, a.rmax);
           continue;
+        }
+        if constexpr (COLLECT) {
+          if (n_in > kInCap && nrefine < 6) {  // too many in the bracket to rank: narrow it
+            cphase = 2;
+            continue;
+          }
         }
         if (n_in > kInCap || r < 1 || r > n_in) {
           if (lane == 0 && a.dbg && fallbacks && atomicAdd(fallbacks + 2, 1) < 10)
