@@ -87,6 +87,8 @@ struct sph_ctx {
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
   int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
+  int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
+  DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
@@ -654,6 +656,26 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
                                                       rmax, ctx->r0.p);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       launches += 3;
+      if (ctx->bundle && compute_f32) {
+        // the bundle pass (sph_bundle.cu): 32 sorted targets per warp with the
+        // seeds' radii; what it leaves goes to the per-target kernel as a list
+        SPH_CK(ctx->left.ensure(n));
+        SPH_CK(cudaMemsetAsync(ctx->qints.p + 24, 0, 4 * sizeof(int), ctx->stream));
+        launch_bundle(ctx->stream, a, ctx->qints.p + 24, ctx->num_sms);
+        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+        launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->left.p, ctx->qints.p + 27,
+                      ctx->cub_temp.p, ctx->cub_bytes);
+        a.list = ctx->left.p;
+        a.list_count = ctx->qints.p + 27;
+        launches += 3;
+        if (ctx->debug) {
+          int bq[4];
+          cudaStreamSynchronize(ctx->stream);
+          cudaMemcpy(bq, ctx->qints.p + 24, sizeof(bq), cudaMemcpyDeviceToHost);
+          fprintf(stderr, "[sph bundle] %d bundles failed, %d lanes failed, %d targets done, %d left\n", bq[0], bq[1],
+                  bq[2], bq[3]);
+        }
+      }
       if (ctx->cell_lists > 0) {
         // neighbour-cell lists for the radii the seeds imply
         const int cap = ctx->cell_lists;
@@ -680,6 +702,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       }
     }
     launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+    a.list = nullptr;  // the bundle pass's leftover list is for this launch only
+    a.list_count = nullptr;
     if (i < 64) {
       cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
       ctx->n_kev = i + 1;
@@ -1155,6 +1179,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
+  if (const char *v = getenv("SPH_BUNDLE")) c->bundle = atoi(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
@@ -1179,7 +1204,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -247,6 +247,8 @@ int lists_max_cap();
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,
                    bool collect = false);
+// bundle pass: 32 consecutive sorted targets per warp (sph_bundle.cu)
+void launch_bundle(cudaStream_t s, const PassArgs &a, int *counters, int num_sms);
 void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells);
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
                        float4 *clist, int *clen, float *crad2, int num_sms);
