@@ -21,8 +21,12 @@ cpu_baseline: the CPU oracle (a C restatement of the reference pass, OpenMP
           on all host cores) on a bounded random target sample of the same
           workload, extrapolated: t = t_tree + t_sample * N / S.
 --impl reference times that CPU implementation alone (rank 0 only).
-Multi-GPU (torchrun, N > 1): independent replicas (one config-C box per
-rank, different seeds), no data-path collective: weak scaling.
+Multi-GPU (torchrun, N > 1): weak scaling over ONE global set of N x the
+1-GPU config (same generator, N x the halos and volume), each rank starting
+from an interleaved slice; a step is the whole decomposed pass (key-range
+ownership, NCCL all-to-all redistribution and ghost exchange, final per-rank
+pass; paper_1612_06090_b200/distributed.py), timed with CUDA events, max over
+ranks.
 """
 
 from __future__ import annotations
@@ -58,13 +62,14 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default="wendland_c6", choices=("wendland_c6", "m4"))
+    ap.add_argument("--decompose", action="store_true", help="run the decomposed multi-GPU path even at N=1")
     return ap.parse_args()
 
 
-def workload_config(cfg: int, seed: int | None):
+def workload_config(cfg: int, seed: int | None, n_ranks: int = 1):
     from paper_1612_06090_b200 import workload
     t0 = time.perf_counter()
-    w = workload.config(cfg, seed)
+    w = workload.config_weak(cfg, n_ranks, seed)
     w["gen_s"] = time.perf_counter() - t0
     return w
 
@@ -79,9 +84,14 @@ def config_json(w, cfg, n_gpus, kernel):
         5: "C5: 8,388,608 particles, fp32, single NFW halo c=20 r_vir=1 + 5% background, periodic box 4, K=128",
         6: "diagnostic: 1,048,576 uniform particles, fp32, periodic box 100, K=64 (not a BASELINE config)",
     }[cfg]
+    if n_gpus > 1:
+        desc = (f"{desc.split(':')[0]} weak-scaled x{n_gpus}: {int(w['pos'].shape[0]):,} particles "
+                f"({n_gpus} x the 1-GPU set: same generator, {n_gpus}x halos, box side {float(w['box']):.1f})")
     return {"workload": desc, "config_index": cfg, "n_particles": int(w["pos"].shape[0]), "k_neighbors": int(w["k"]),
             "box": float(w["box"]), "periodic": bool(w["periodic"]), "positions": "f32" if w["fp32"] else "f64",
-            "kernel": kernel, "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "1 GPU",
+            "kernel": kernel,
+            "parallelism": (f"{n_gpus} GPUs: key-range domain decomposition, NCCL all-to-all redistribution + "
+                            "ghost exchange" if n_gpus > 1 else "1 GPU"),
             "l2": "flushed before every step (256 MiB device write)",
             "h0": "reference initial_smoothing_length rule" if cfg != 1 else "2*N^(-1/3)"}
 
@@ -182,7 +192,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w = workload_config(args.config, args.seed)
+    w = workload_config(args.config, args.seed, max(1, args.gpus))
     n, k = w["pos"].shape[0], int(w["k"])
     vals = []
     base = None
@@ -215,7 +225,9 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = world > 1
+    if world > 1 or args.decompose:
+        return run_decomposed(args, world, rank, local)
+    dist = False
     if dist:
         import torch.distributed as tdist
         torch.cuda.set_device(local)
@@ -383,6 +395,123 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         tdist.destroy_process_group()
+
+
+def run_decomposed(args, world, rank, local):
+    """N > 1: one global weak-scaled set (N x the 1-GPU config), each rank
+    starting from an interleaved slice of it; a step is the whole decomposed
+    pass (bbox all-reduce, keys, splitters, NCCL all-to-all redistribution,
+    bounds, ghost exchange, the final per-rank pass)."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_1612_06090_b200 import distributed as D
+
+    torch.cuda.set_device(local)
+    if world == 1:  # --decompose outside torchrun
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    w = workload_config(args.config, args.seed, world)
+    n_glob, k = w["pos"].shape[0], int(w["k"])
+    sel = np.arange(rank, n_glob, world)
+    f32 = bool(w["fp32"])
+    pdt = torch.float32 if f32 else torch.float64
+    npdt = np.float32 if f32 else np.float64
+    hp = [np.ascontiguousarray(w["pos"][sel, i].astype(npdt)) for i in range(3)]
+    hm, hh0 = np.ascontiguousarray(w["mass"][sel]), np.ascontiguousarray(w["h0"][sel])
+    dx, dy, dz = (torch.from_numpy(a).to(device) for a in hp)
+    dm, dh0 = torch.from_numpy(hm).to(device), torch.from_numpy(hh0).to(device)
+    dgid = torch.from_numpy(sel.astype(np.int64)).to(device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    compute = D.LibCompute(device)
+    periodic, box = bool(w["periodic"]), float(w["box"])
+
+    def step(x, y, z, m, h0, gid):
+        return D.decomposed_pass(x, y, z, m, h0, gid, k, compute, periodic=periodic, box=box)
+
+    for i in range(args.warmup):
+        flush.fill_(i & 255)
+        r = step(dx, dy, dz, dm, dh0, dgid)
+    torch.cuda.synchronize(device)
+    tdist.barrier()
+    torch.cuda.synchronize(device)
+    clocks = ClockSampler(device)
+    clocks.start()
+    step_ms = []
+    for i in range(args.steps):
+        flush.fill_((i + 7) & 255)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        r = step(dx, dy, dz, dm, dh0, dgid)
+        ev1.record()
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize(device)
+    tdist.barrier()
+    clk = clocks.stop()
+    st = compute.last_stats or {}
+    t_local = torch.tensor([sum(step_ms) / len(step_ms)], dtype=torch.float64, device=device)
+    tdist.all_reduce(t_local, op=tdist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    info = torch.tensor([r.n_owned, r.n_ghosts, r.n_owned, r.n_owned], dtype=torch.float64, device=device)
+    isum = info.clone()
+    tdist.all_reduce(isum)
+    imax = info.clone()
+    tdist.all_reduce(imax, op=tdist.ReduceOp.MAX)
+    imin = info.clone()
+    tdist.all_reduce(imin, op=tdist.ReduceOp.MIN)
+    value = n_glob * k / (ms_max * 1e-3)
+
+    # end to end: pinned host slices in, owned (gid, h, rho) back to the host
+    e2e = None
+    if not args.no_e2e:
+        pin = [torch.from_numpy(a).pin_memory() for a in (*hp, hm, hh0, sel.astype(np.int64))]
+        e2e_ms = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize(device)
+            tdist.barrier()
+            t0 = time.perf_counter()
+            d = [t.to(device, non_blocking=True) for t in pin]
+            rr = step(*d)
+            out = (rr.gid.cpu(), rr.h.cpu(), rr.rho.cpu())
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_ms.append(dt * 1e3)
+        el = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=device)
+        tdist.all_reduce(el, op=tdist.ReduceOp.MAX)
+        es = 4 if f32 else 8
+        e2e = {"value": n_glob * k / (float(el.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(len(sel) * (3 * es + 8 + 8 + 8)),
+               "d2h_bytes_per_step": int(out[0].numel() * (8 + 8 + 8)), "ms_per_step": float(el.item()),
+               "api": "paper_1612_06090_b200.distributed.decomposed_pass (per-rank C ABI sph_density_pass_device), "
+                      "pinned host slices, max over ranks"}
+    if rank == 0:
+        tk = st.get("t_kernel_ms", {})
+        t_k = tk.get("search", 0.0) + tk.get("select", 0.0) + tk.get("density", 0.0)
+        peak = float(compute.L.sph_fp32_peak(compute.ctx)) / 1e12
+        ops = 6.0 * st.get("pair_tests", 0) + 10.0 * st.get("accepted_pairs", 0)
+        achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
+                "config": config_json(w, args.config, world, args.kernel),
+                "converged_particles_per_s": n_glob / (ms_max * 1e-3),
+                "gpu_launches": int(st.get("gpu_launches", 0)) + 1,
+                "clocks": clk,
+                "roofline": {"bound": "fp32", "kernel": "k_target (rank 0's final pass)", "achieved": achieved,
+                             "peak": peak, "unit": "Tops/s (fp32-pipe ops)", "frac": achieved / peak if peak else None,
+                             "traffic": None, "ops_model": "6 per pair test, +10 per accepted pair (density)"},
+                "decomposition": {"owned_min": int(imin[0].item()), "owned_max": int(imax[0].item()),
+                                  "ghosts_total": int(isum[1].item()), "ghosts_max": int(imax[1].item()),
+                                  "final_pass_ms_rank0": st.get("t_stage_ms", {}).get("total")},
+                "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
 
 
 def main():

@@ -120,6 +120,47 @@ int sph_density_pass_device(sph_ctx *ctx, const sph_params *params,
                             const double *d_mass, double *d_h, double *d_rho,
                             uint8_t *d_flags, sph_stats *stats);
 
+/* 63-bit x-major octant-path keys of device-resident positions from a given
+ * root cube (centre[3], half): the key the ordering sorts by (octree.py:93-104
+ * descent, 21 levels), here for the key-range domain decomposition
+ * (distributed ownership; no reference counterpart: the reference is one
+ * shared-memory process).  Enqueued on the context's stream (sph_ctx_stream). */
+int sph_morton_keys_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y,
+                           const void *d_z, const double *centre, double half, uint64_t *d_keys);
+
+/* Domain-decomposition helpers (device pointers, the context's stream):
+ *  pack_rows    : rows[i] = (x, y, z, m, h0, gid, key >> 32, key & 0xffffffff)
+ *                 of particle order[i], 8 doubles per record (the all-to-all payload)
+ *  gather_rows  : dst row i = src row idx[i], width doubles per row
+ *  row_keys     : keys of packed records (columns 6, 7) back to int64
+ *  level_bounds : per particle (key-sorted) an upper bound of its K-th
+ *                 neighbour distance: sqrt(3) * side of the deepest key cube
+ *                 holding it and >= K others (INFINITY when n <= K)
+ *  window_bounds: tightens bound[p] (in place, min) by the farthest of the K
+ *                 others in each of three windows of K+1 key-consecutive
+ *                 records around p (any K others bound the K-th distance)
+ *  ghost_mask   : mask[i] |= 1 << rank(f) for every particle i of my groups
+ *                 (descriptors gdesc, records rows) within foreign group f's
+ *                 margin of its box (min-image when periodic): the ghosts
+ *  group_boxes  : per group [start, start + count) of records: tight box of
+ *                 columns 0-2 and the largest bound -> 7 doubles */
+int sph_decomp_pack_rows_device(sph_ctx *ctx, int32_t precision, int64_t n, const int64_t *d_order,
+                                const void *d_x, const void *d_y, const void *d_z, const double *d_mass,
+                                const double *d_h0, const int64_t *d_gid, const int64_t *d_keys, double *d_rows);
+int sph_decomp_gather_rows_device(sph_ctx *ctx, int64_t n, int32_t width, const int64_t *d_idx,
+                                  const double *d_src, double *d_dst);
+int sph_decomp_row_keys_device(sph_ctx *ctx, int64_t n, const double *d_rows, int64_t *d_keys);
+int sph_decomp_level_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, const int64_t *d_keys_sorted, double half,
+                                   double *d_bound);
+int sph_decomp_window_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, int32_t width, const double *d_rows,
+                                    double *d_bound);
+int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d_gdesc, const int64_t *d_gstart,
+                                 const int64_t *d_gcount, int32_t width, const double *d_rows, int64_t n_foreign,
+                                 const double *d_fdesc, const int32_t *d_frank, int32_t periodic, double box,
+                                 uint32_t *d_mask);
+int sph_decomp_group_boxes_device(sph_ctx *ctx, int64_t n_groups, const int64_t *d_starts, const int64_t *d_counts,
+                                  int32_t width, const double *d_rows, const double *d_bound, double *d_out);
+
 /* Octree particle_perm (leaf capacity 8), bit-exact with the reference.
  * Host pointers; positions per precision (contiguous). */
 int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y,

@@ -101,6 +101,16 @@ def load():
         L.sph_fnv1a64.argtypes = [vp, ctypes.c_size_t]
         L.sph_fnv1a64.restype = ctypes.c_uint64
         L.sph_uniform_box_device.argtypes = [vp, i64, ctypes.c_uint64, ctypes.c_double, vp, vp, vp]
+        L.sph_morton_keys_device.argtypes = [vp, i32, i64, vp, vp, vp, ctypes.POINTER(ctypes.c_double),
+                                             ctypes.c_double, vp]
+        L.sph_decomp_pack_rows_device.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.sph_decomp_gather_rows_device.argtypes = [vp, i64, i32, vp, vp, vp]
+        L.sph_decomp_row_keys_device.argtypes = [vp, i64, vp, vp]
+        L.sph_decomp_level_bounds_device.argtypes = [vp, i64, i32, vp, ctypes.c_double, vp]
+        L.sph_decomp_window_bounds_device.argtypes = [vp, i64, i32, i32, vp, vp]
+        L.sph_decomp_ghost_mask_device.argtypes = [vp, i64, vp, vp, vp, i32, vp, i64, vp, vp, i32, ctypes.c_double,
+                                                   vp]
+        L.sph_decomp_group_boxes_device.argtypes = [vp, i64, vp, vp, i32, vp, vp, vp]
         _lib = L
         return L
 
@@ -130,6 +140,24 @@ def context(device: int = 0):
             c = h
             _ctx[device] = c
         return c
+
+
+def new_context(device: int = 0):
+    """A private context (its own stream and buffers), e.g. one per in-process
+    rank of an emulated decomposition; never destroyed before exit."""
+    L = load()
+    if L.sph_device_count() <= 0:
+        raise RuntimeError("no CUDA device visible: the B200 pass has no CPU fallback")
+    h = ctypes.c_void_p()
+    rc = L.sph_ctx_create(ctypes.byref(h), device)
+    if rc != SPH_OK:
+        raise RuntimeError(f"sph_ctx_create(device={device}) failed with status {rc}")
+    with _lock:
+        _private.append(h)
+    return h
+
+
+_private = []
 
 
 def stream_handle(ctx) -> int:

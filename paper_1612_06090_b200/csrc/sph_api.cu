@@ -1370,6 +1370,104 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   return rc;
 }
 
+int sph_morton_keys_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y,
+                           const void *d_z, const double *centre, double half, uint64_t *d_keys) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || n >= (1ll << 31)) return fail(ctx, SPH_INVALID, "n must be in [0, 2^31)");
+  if (precision != SPH_PRECISION_F32 && precision != SPH_PRECISION_F64)
+    return fail(ctx, SPH_INVALID, "precision must be f32 or f64");
+  if (!centre || !(half >= 0.0)) return fail(ctx, SPH_INVALID, "need a root centre and half-extent >= 0");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_keys_at(ctx->stream, (int)n, precision == SPH_PRECISION_F32 ? 1 : 0, d_x, d_y, d_z, centre, half,
+                 reinterpret_cast<unsigned long long *>(d_keys));
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_pack_rows_device(sph_ctx *ctx, int32_t precision, int64_t n, const int64_t *d_order,
+                                const void *d_x, const void *d_y, const void *d_z, const double *d_mass,
+                                const double *d_h0, const int64_t *d_gid, const int64_t *d_keys, double *d_rows) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0) return fail(ctx, SPH_INVALID, "n must be >= 0");
+  if (precision != SPH_PRECISION_F32 && precision != SPH_PRECISION_F64)
+    return fail(ctx, SPH_INVALID, "precision must be f32 or f64");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_pack_rows(ctx->stream, n, precision == SPH_PRECISION_F32 ? 1 : 0, d_order, d_x, d_y, d_z, d_mass, d_h0,
+                   d_gid, d_keys, d_rows);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_gather_rows_device(sph_ctx *ctx, int64_t n, int32_t width, const int64_t *d_idx,
+                                  const double *d_src, double *d_dst) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || width < 1) return fail(ctx, SPH_INVALID, "need n >= 0 and width >= 1");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_gather_rows(ctx->stream, n, width, d_idx, d_src, d_dst);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_row_keys_device(sph_ctx *ctx, int64_t n, const double *d_rows, int64_t *d_keys) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0) return fail(ctx, SPH_INVALID, "n must be >= 0");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_row_keys(ctx->stream, n, d_rows, d_keys);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_level_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, const int64_t *d_keys_sorted, double half,
+                                   double *d_bound) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || k < 1) return fail(ctx, SPH_INVALID, "need n >= 0 and k >= 1");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_level_bounds(ctx->stream, n, k, d_keys_sorted, 2.0 * half, d_bound);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_window_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, int32_t width, const double *d_rows,
+                                    double *d_bound) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || k < 1 || k > 2048 || width < 3) return fail(ctx, SPH_INVALID, "need n >= 0, 1 <= k <= 2048, width >= 3");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_window_bounds(ctx->stream, n, k, width, d_rows, d_bound);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d_gdesc, const int64_t *d_gstart,
+                                 const int64_t *d_gcount, int32_t width, const double *d_rows, int64_t n_foreign,
+                                 const double *d_fdesc, const int32_t *d_frank, int32_t periodic, double box,
+                                 uint32_t *d_mask) {
+  if (!ctx) return SPH_INVALID;
+  if (n_groups < 0 || n_foreign < 0 || width < 3) return fail(ctx, SPH_INVALID, "bad ghost-mask arguments");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_ghost_mask(ctx->stream, n_groups, d_gdesc, d_gstart, d_gcount, width, d_rows, n_foreign, d_fdesc, d_frank,
+                    periodic, box, d_mask);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_decomp_group_boxes_device(sph_ctx *ctx, int64_t n_groups, const int64_t *d_starts, const int64_t *d_counts,
+                                  int32_t width, const double *d_rows, const double *d_bound, double *d_out) {
+  if (!ctx) return SPH_INVALID;
+  if (n_groups < 0 || width < 3) return fail(ctx, SPH_INVALID, "need n_groups >= 0 and width >= 3");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  launch_group_boxes(ctx->stream, n_groups, d_starts, d_counts, width, d_rows, d_bound, d_out);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
 int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
                   int64_t *perm_out) {
   if (!ctx) return SPH_INVALID;

@@ -236,6 +236,22 @@ void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const v
                  const void *z, unsigned long long *ord, RootInfo *root, int *launches);
 
 size_t cub_temp_needed(int n);
+// domain decomposition helpers (sph_decomp.cu)
+void launch_pack_rows(cudaStream_t s, int64_t n, int precision_in, const int64_t *order, const void *x,
+                      const void *y, const void *z, const double *m, const double *h0, const int64_t *gid,
+                      const int64_t *keys, double *rows);
+void launch_gather_rows(cudaStream_t s, int64_t n, int width, const int64_t *idx, const double *src, double *dst);
+void launch_row_keys(cudaStream_t s, int64_t n, const double *rows, int64_t *keys);
+void launch_level_bounds(cudaStream_t s, int64_t n, int k, const int64_t *keys, double side0, double *bound);
+void launch_window_bounds(cudaStream_t s, int64_t n, int k, int width, const double *rows, double *bound);
+void launch_ghost_mask(cudaStream_t s, int64_t ng, const double *gdesc, const int64_t *gstart, const int64_t *gcount,
+                       int width, const double *rows, int64_t nf, const double *fdesc, const int32_t *frank,
+                       int periodic, double box, uint32_t *mask);
+void launch_group_boxes(cudaStream_t s, int64_t ng, const int64_t *starts, const int64_t *counts, int width,
+                        const double *rows, const double *bound, double *out);
+// 63-bit keys from a given root cube (domain decomposition)
+void launch_keys_at(cudaStream_t s, int n, int precision_in, const void *x, const void *y, const void *z,
+                    const double *centre, double half, unsigned long long *keys);
 
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };

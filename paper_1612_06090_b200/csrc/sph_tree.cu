@@ -380,6 +380,30 @@ __global__ void k_fill(int n, T *a, T v) {
 
 inline int nblk(long long n, int t = kTB) { return (int)((n + t - 1) / t); }
 
+// keys of the domain decomposition (distributed/decomp.py): the same 21-level
+// descent as k_keys, from a root cube given by value (the all-reduced one)
+template <typename PosT>
+__global__ void k_keys_at(int n, const PosT *__restrict__ x, const PosT *__restrict__ y,
+                          const PosT *__restrict__ z, double c0x, double c0y, double c0z, double half0,
+                          unsigned long long *__restrict__ keys) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double px = (double)x[i], py = (double)y[i], pz = (double)z[i];
+  double cx = c0x, cy = c0y, cz = c0z, half = half0;
+  unsigned long long key = 0;
+#pragma unroll
+  for (int l = 0; l < kMaxLevel; ++l) {
+    const int bx = px >= cx, by = py >= cy, bz = pz >= cz;
+    key = (key << 3) | (unsigned long long)((bx << 2) | (by << 1) | bz);
+    const double h2 = __dmul_rn(half, 0.5);
+    cx = bx ? __dadd_rn(cx, h2) : __dsub_rn(cx, h2);
+    cy = by ? __dadd_rn(cy, h2) : __dsub_rn(cy, h2);
+    cz = bz ? __dadd_rn(cz, h2) : __dsub_rn(cz, h2);
+    half = h2;
+  }
+  keys[i] = key;
+}
+
 }  // namespace
 
 size_t cub_temp_needed(int n) {
@@ -388,6 +412,17 @@ size_t cub_temp_needed(int n) {
                                   (uint32_t *)nullptr, (uint32_t *)nullptr, n, 0, 63);
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, n + 1);
   return a > b ? a : b;
+}
+
+void launch_keys_at(cudaStream_t s, int n, int precision_in, const void *x, const void *y, const void *z,
+                    const double *centre, double half, unsigned long long *keys) {
+  if (n <= 0) return;
+  if (precision_in == 1)
+    k_keys_at<float><<<(n + 255) / 256, 256, 0, s>>>(n, (const float *)x, (const float *)y, (const float *)z,
+                                                     centre[0], centre[1], centre[2], half, keys);
+  else
+    k_keys_at<double><<<(n + 255) / 256, 256, 0, s>>>(n, (const double *)x, (const double *)y, (const double *)z,
+                                                      centre[0], centre[1], centre[2], half, keys);
 }
 
 void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const void *y, const void *z,

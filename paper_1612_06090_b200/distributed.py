@@ -2,40 +2,47 @@
 
 The reference runs on one shared-memory node (threads, scheduler.py of the
 reference); it has no distributed mode.  Here each rank owns a contiguous
-range of the same 63-bit x-major Morton keys the ordering uses (the key of a
-particle is the reference octree path, octree.py:93-104), so a rank's
-particles form a compact piece of space.  The exchange steps:
+range of the same 63-bit x-major keys the ordering sorts by (the key of a
+particle is its reference octree path, octree.py:93-104), so a rank's
+particles form a compact piece of space, and the only data exchange of the
+path is the ghost layer.  Everything stays in device memory; the collectives
+are torch.distributed (NCCL over NVLink/NVSwitch on GPUs, gloo on CPU for the
+tests), the per-rank compute is pluggable (``LibCompute``: libsph_b200 on the
+rank's GPU; ``NumpyCompute``: any host pass, e.g. the CPU oracle in tests).
 
-  1. bbox all-reduce (MIN / MAX) -> the common root cube (octree.py:324-328)
-  2. key splitters from an all-gather of evenly spaced key samples
-     (count-balanced), then an all-to-all that moves every particle record
-     (x, y, z, m, h0, global id) to its owner
-  3. a local pass over owned particles only gives h_local >= h (a K-th
-     neighbour among a subset is never nearer): per rank, the ghost margin
-     m_r = max h_local is a guaranteed cover.  Ghosts = every particle
-     within m_r of rank r's box (min-image distance when periodic), sent
-     with a second all-to-all
-  4. the final pass over owned + ghosts with the owned particles as targets
-     (sph_params.n_targets) is exact: each target sees every particle within
-     its true h, so h is bit-identical to the single-GPU result and the todo
-     trace (a function of h0 and d2_K) is too.
+Steps of ``decomposed_pass`` (all ranks call it collectively):
 
-Collectives go through torch.distributed: NCCL (device tensors over
-NVLink/NVSwitch) on GPUs, gloo on CPU (tests).  ``local_pass`` is the
-per-rank compute; ``gpu_local_pass`` is the product one, the tests pass the
-CPU oracle instead to check the decomposition logic without GPUs.
+  1. bbox all-reduce -> the common root cube (octree.py:324-328 arithmetic)
+  2. keys from that cube (``sph_morton_keys_device``), count-balanced key
+     splitters from all-gathered samples, one all-to-all moving each record
+     (x, y, z, m, h0, global id, key) to its owner
+  3. a guaranteed per-particle bound on h without any search: a particle in a
+     level-l key cube that holds >= K+1 owned particles has K others within
+     the cube's diagonal, so h <= sqrt(3) * side(l) for the deepest such l
+     (a K-th neighbour among a subset is never nearer than among all)
+  4. descriptors: owned particles grouped by a coarse key prefix, per group
+     the tight box and the largest bound; all-gathered
+  5. ghosts: every owned particle within a peer group's bound of that group's
+     box (min-image when periodic) is sent to the peer (second all-to-all);
+     a target's true neighbours all lie within its bound of its own box
+  6. the final pass over owned + ghosts with the owned particles as targets
+     (``sph_params.n_targets``): h is bit-identical to one GPU and so is the
+     todo trace (a function of h0 and d2_K); densities agree to the fp32 sum
+     order (bit-identical on the fp64 paths).
 """
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
 
 KEY_LEVELS = 21
+_SQRT3 = math.sqrt(3.0)
 
 
-def root_cube(lo: np.ndarray, hi: np.ndarray):
+def root_cube(lo, hi):
     """Root centre and half-extent, fp64 op-for-op as octree.py:324-328."""
     lo = np.asarray(lo, dtype=np.float64)
     hi = np.asarray(hi, dtype=np.float64)
@@ -66,139 +73,17 @@ def box_distance2(pos: np.ndarray, lo: np.ndarray, hi: np.ndarray, periodic: boo
     when periodic)."""
     d = np.maximum(np.maximum(lo - pos, pos - hi), 0.0)
     if periodic:
-        # distance to the box images shifted by +-box along each axis
         dm = np.maximum(np.maximum((lo - box) - pos, pos - (hi - box)), 0.0)
         dp = np.maximum(np.maximum((lo + box) - pos, pos - (hi + box)), 0.0)
         d = np.minimum(d, np.minimum(dm, dp))
     return np.sum(d * d, axis=1)
 
 
-@dataclass
-class DistResult:
-    gid: np.ndarray       # global ids of the particles this rank owns
-    h: np.ndarray         # converged smoothing length
-    rho: np.ndarray       # density
-    todo_hist: np.ndarray  # reference rounds histogram contribution (PassStats.todo_sizes by sum)
-    n_ghosts: int
-    margin: float
-
-
-def _torch():
-    import torch
-    import torch.distributed as dist
-    return torch, dist
-
-
-def _all_to_all_rows(rows: np.ndarray, dest: np.ndarray, world: int, device) -> np.ndarray:
-    """Send row i to rank dest[i]; returns the rows received (float64)."""
-    torch, dist = _torch()
-    order = np.argsort(dest, kind="stable")
-    rows = np.ascontiguousarray(rows[order])
-    send_counts = np.bincount(dest, minlength=world).astype(np.int64)
-    sc = torch.from_numpy(send_counts).to(device)
-    rc = torch.empty_like(sc)
-    dist.all_to_all_single(rc, sc)
-    recv_counts = rc.cpu().numpy()
-    width = rows.shape[1] if rows.ndim == 2 else 1
-    send = torch.from_numpy(rows.reshape(-1)).to(device)
-    recv = torch.empty(int(recv_counts.sum()) * width, dtype=torch.float64, device=device)
-    dist.all_to_all_single(recv, send, output_split_sizes=(recv_counts * width).tolist(),
-                           input_split_sizes=(send_counts * width).tolist())
-    return recv.cpu().numpy().reshape(-1, width)
-
-
-def density_pass_distributed(x, y, z, mass, h0, gid, k: int, local_pass, *, periodic: bool = False,
-                             box: float = 0.0, samples: int = 1024, device="cpu",
-                             max_iterations: int = 100) -> DistResult:
-    """Collective call: every rank passes its local particles (any split).
-
-    ``local_pass(x, y, z, mass, h0_targets, k, n_targets, periodic, box,
-    max_iterations) -> (h, rho, todo_sizes)`` computes the targets
-    [0, n_targets) of the arrays it is given (the rest are ghosts);
-    ``todo_sizes`` is the reference todo trace over those targets.
-    """
-    torch, dist = _torch()
-    rank, world = dist.get_rank(), dist.get_world_size()
-    pos = np.column_stack([np.asarray(x, np.float64), np.asarray(y, np.float64), np.asarray(z, np.float64)])
-    n_local = pos.shape[0]
-
-    # 1. common root cube
-    big = np.finfo(np.float64).max
-    lo = torch.tensor(pos.min(axis=0) if n_local else np.full(3, big), dtype=torch.float64, device=device)
-    hi = torch.tensor(pos.max(axis=0) if n_local else np.full(3, -big), dtype=torch.float64, device=device)
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-    centre, half = root_cube(lo.cpu().numpy(), hi.cpu().numpy())
-
-    # 2. key-range ownership from sampled splitters
-    keys = morton_keys(pos, centre, half)
-    sk = np.sort(keys)
-    if n_local:
-        idx = np.linspace(0, n_local - 1, samples).astype(np.int64)
-        mine = sk[idx].astype(np.int64)  # keys < 2^63: exact in int64
-    else:
-        mine = np.full(samples, np.iinfo(np.int64).max, dtype=np.int64)
-    t = torch.from_numpy(mine).to(device)
-    gathered = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(gathered, t)
-    allk = np.sort(np.concatenate([g.cpu().numpy() for g in gathered]))
-    splitters = allk[(np.arange(1, world) * allk.size) // world].astype(np.uint64)
-    dest = np.searchsorted(splitters, keys, side="right").astype(np.int64)
-    rows = np.column_stack([pos, np.asarray(mass, np.float64), np.asarray(h0, np.float64),
-                            np.asarray(gid, np.float64)])
-    owned = _all_to_all_rows(rows, dest, world, device)
-    owned = owned[np.argsort(owned[:, 5], kind="stable")]  # deterministic order: by global id
-    n_own = owned.shape[0]
-
-    # 3. local pass on owned particles only -> guaranteed ghost margin
-    if n_own > k:
-        h_loc, _, _ = local_pass(owned[:, 0], owned[:, 1], owned[:, 2], owned[:, 3], owned[:, 4], k, n_own,
-                                 periodic, box, max_iterations)
-        margin = float(np.max(h_loc)) if n_own else 0.0
-    else:
-        margin = np.inf
-    if not np.isfinite(margin):
-        margin = float(box) if periodic else 2.0 * half * np.sqrt(3.0) + 1.0
-    olo = owned[:, :3].min(axis=0) if n_own else np.full(3, big)
-    ohi = owned[:, :3].max(axis=0) if n_own else np.full(3, -big)
-    info = torch.tensor(np.concatenate([olo, ohi, [margin]]), dtype=torch.float64, device=device)
-    infos = [torch.empty_like(info) for _ in range(world)]
-    dist.all_gather(infos, info)
-    infos = [i.cpu().numpy() for i in infos]
-
-    # ghosts: my owned particles within each peer's margin of the peer's box
-    send_rows, send_dest = [], []
-    for q in range(world):
-        if q == rank or n_own == 0:
-            continue
-        qlo, qhi, qm = infos[q][:3], infos[q][3:6], infos[q][6]
-        if not np.all(qlo <= qhi):
-            continue
-        sel = box_distance2(owned[:, :3], qlo, qhi, periodic, box) <= qm * qm * (1.0 + 1e-12)
-        if sel.any():
-            send_rows.append(owned[sel])
-            send_dest.append(np.full(int(sel.sum()), q, dtype=np.int64))
-    rows_g = np.concatenate(send_rows) if send_rows else np.zeros((0, 6))
-    dest_g = np.concatenate(send_dest) if send_dest else np.zeros(0, dtype=np.int64)
-    ghosts = _all_to_all_rows(rows_g, dest_g, world, device)
-
-    # 4. final pass: owned targets + ghosts
-    allp = np.concatenate([owned, ghosts]) if ghosts.size else owned
-    if n_own:
-        h, rho, todo = local_pass(allp[:, 0], allp[:, 1], allp[:, 2], allp[:, 3], owned[:, 4], k, n_own,
-                                  periodic, box, max_iterations)
-    else:
-        h = rho = np.zeros(0)
-        todo = np.zeros(0, dtype=np.int64)
-    hist = hist_from_todo_sizes(np.asarray(todo, dtype=np.int64), max_iterations)
-    return DistResult(gid=owned[:, 5].astype(np.int64), h=np.asarray(h), rho=np.asarray(rho), todo_hist=hist,
-                      n_ghosts=int(ghosts.shape[0]), margin=margin)
-
-
 def hist_from_todo_sizes(todo: np.ndarray, max_iterations: int) -> np.ndarray:
     """Rounds histogram (hist[r] = particles converging in round r) of a
     todo trace; traces of disjoint target sets add as histograms."""
     hist = np.zeros(max_iterations + 2, dtype=np.int64)
+    todo = np.asarray(todo, dtype=np.int64)
     nxt = np.append(todo[1:], 0)
     hist[1:len(todo) + 1] = todo - nxt
     return hist
@@ -211,13 +96,645 @@ def todo_sizes_from_hist(hist: np.ndarray) -> np.ndarray:
     return tail[1:last + 1].astype(np.int64)
 
 
+# ---------------------------------------------------------------------------
+# per-rank compute backends
+# ---------------------------------------------------------------------------
+class TorchOps:
+    """Record plumbing of the decomposition in plain torch ops (any device);
+    the host / test backend.  ``LibCompute`` replaces every op with the
+    library's kernels (csrc/sph_decomp.cu)."""
+
+    def pack_rows(self, order, x, y, z, m, h0, gid, keys):
+        import torch
+        k = keys[order]
+        return torch.stack([x[order].double(), y[order].double(), z[order].double(), m[order], h0[order],
+                            gid[order].double(), (k >> 32).double(), (k & 0xFFFFFFFF).double()], dim=1)
+
+    def gather_rows(self, rows, idx):
+        return rows[idx]
+
+    def row_keys(self, rows):
+        import torch
+        return (rows[:, 6].to(torch.int64) << 32) | rows[:, 7].to(torch.int64)
+
+    def level_bounds(self, keys_sorted, k, half):
+        return level_bounds(keys_sorted, k, half)
+
+    def window_bounds(self, rows, bound, k):
+        return window_bounds(rows, bound, k)
+
+    def ghost_mask(self, gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk=1 << 22):
+        return ghost_mask(gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk)
+
+    def group_boxes(self, rows, bound, starts, counts):
+        import torch
+        ng = starts.numel()
+        gid = torch.repeat_interleave(torch.arange(ng, device=rows.device), counts)
+        gidx = gid.view(-1, 1).expand(-1, 3)
+        big = float(np.finfo(np.float64).max)
+        pos = rows[:, :3]
+        lo = torch.full((ng, 3), big, dtype=torch.float64, device=rows.device).scatter_reduce(0, gidx, pos, "amin")
+        hi = torch.full((ng, 3), -big, dtype=torch.float64, device=rows.device).scatter_reduce(0, gidx, pos, "amax")
+        mb = torch.zeros(ng, dtype=torch.float64, device=rows.device).scatter_reduce(0, gid, bound, "amax")
+        return torch.cat([lo, hi, mb.view(-1, 1)], dim=1)
+
+
+class LibCompute(TorchOps):
+    """The product: libsph_b200 on this rank's GPU (device-resident arrays).
+    ``decomposed_pass`` runs on the library's stream, so torch ops, NCCL and
+    the library's kernels are ordered without extra synchronisation."""
+
+    def __init__(self, device: int = 0, private_context: bool = False):
+        import torch
+
+        from . import _lib
+        self.torch = torch
+        self.lib = _lib
+        self.L = _lib.load()
+        self.device = device
+        self.ctx = _lib.new_context(device) if private_context else _lib.context(device)
+        self.keep_inputs = False
+        self.last_inputs = None
+        self.stream = torch.cuda.ExternalStream(_lib.stream_handle(self.ctx), device=f"cuda:{device}")
+        self.last_stats = None
+
+    def _ck(self, rc, what):
+        if rc != self.lib.SPH_OK:
+            raise RuntimeError(f"{what} failed ({rc}): {self.lib.last_error(self.ctx)}")
+
+    @staticmethod
+    def _p(t):
+        import ctypes
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _sync_in(self, dev):
+        cur = self.torch.cuda.current_stream(dev)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
+        return cur
+
+    def _sync_out(self, cur):
+        if cur.cuda_stream != self.stream.cuda_stream:
+            cur.wait_stream(self.stream)
+
+    def keys(self, x, y, z, centre, half):
+        import ctypes
+        torch = self.torch
+        n = x.numel()
+        out = torch.empty(n, dtype=torch.int64, device=x.device)
+        if n == 0:
+            return out
+        prec = self.lib.PRECISION["f32" if x.dtype == torch.float32 else "f64"]
+        c3 = (ctypes.c_double * 3)(*[float(v) for v in centre])
+        cur = self._sync_in(x.device)
+        self._ck(self.L.sph_morton_keys_device(self.ctx, prec, n, self._p(x), self._p(y), self._p(z), c3,
+                                               float(half), self._p(out)), "sph_morton_keys_device")
+        self._sync_out(cur)
+        return out
+
+    def pack_rows(self, order, x, y, z, m, h0, gid, keys):
+        torch = self.torch
+        n = order.numel()
+        rows = torch.empty((n, 8), dtype=torch.float64, device=x.device)
+        if n == 0:
+            return rows
+        prec = self.lib.PRECISION["f32" if x.dtype == torch.float32 else "f64"]
+        cur = self._sync_in(x.device)
+        self._ck(self.L.sph_decomp_pack_rows_device(self.ctx, prec, n, self._p(order), self._p(x), self._p(y),
+                                                    self._p(z), self._p(m), self._p(h0), self._p(gid),
+                                                    self._p(keys), self._p(rows)), "sph_decomp_pack_rows_device")
+        self._sync_out(cur)
+        return rows
+
+    def gather_rows(self, rows, idx):
+        torch = self.torch
+        n = idx.numel()
+        out = torch.empty((n, rows.shape[1]), dtype=torch.float64, device=rows.device)
+        if n == 0:
+            return out
+        cur = self._sync_in(rows.device)
+        self._ck(self.L.sph_decomp_gather_rows_device(self.ctx, n, rows.shape[1], self._p(idx), self._p(rows),
+                                                      self._p(out)), "sph_decomp_gather_rows_device")
+        self._sync_out(cur)
+        return out
+
+    def row_keys(self, rows):
+        torch = self.torch
+        n = rows.shape[0]
+        out = torch.empty(n, dtype=torch.int64, device=rows.device)
+        if n == 0:
+            return out
+        cur = self._sync_in(rows.device)
+        self._ck(self.L.sph_decomp_row_keys_device(self.ctx, n, self._p(rows), self._p(out)),
+                 "sph_decomp_row_keys_device")
+        self._sync_out(cur)
+        return out
+
+    def level_bounds(self, keys_sorted, k, half):
+        torch = self.torch
+        n = keys_sorted.numel()
+        out = torch.empty(n, dtype=torch.float64, device=keys_sorted.device)
+        if n == 0:
+            return out
+        cur = self._sync_in(keys_sorted.device)
+        self._ck(self.L.sph_decomp_level_bounds_device(self.ctx, n, k, self._p(keys_sorted), float(half),
+                                                       self._p(out)), "sph_decomp_level_bounds_device")
+        self._sync_out(cur)
+        return out
+
+    def window_bounds(self, rows, bound, k):
+        n = rows.shape[0]
+        if n == 0:
+            return bound
+        cur = self._sync_in(rows.device)
+        self._ck(self.L.sph_decomp_window_bounds_device(self.ctx, n, k, rows.shape[1], self._p(rows), self._p(bound)),
+                 "sph_decomp_window_bounds_device")
+        self._sync_out(cur)
+        return bound
+
+    def ghost_mask(self, gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk=1 << 22):
+        torch = self.torch
+        mask = torch.zeros(rows.shape[0], dtype=torch.int32, device=rows.device)
+        if gdesc.shape[0] == 0 or fdesc.shape[0] == 0:
+            return mask
+        fr = frank.to(torch.int32).contiguous()
+        fd = fdesc.contiguous()
+        gd = gdesc.contiguous()
+        cur = self._sync_in(rows.device)
+        self._ck(self.L.sph_decomp_ghost_mask_device(self.ctx, gd.shape[0], self._p(gd), self._p(gstart),
+                                                     self._p(gcount), rows.shape[1], self._p(rows), fd.shape[0],
+                                                     self._p(fd), self._p(fr), 1 if periodic else 0, float(box),
+                                                     self._p(mask)), "sph_decomp_ghost_mask_device")
+        self._sync_out(cur)
+        return mask
+
+    def group_boxes(self, rows, bound, starts, counts):
+        torch = self.torch
+        ng = starts.numel()
+        out = torch.empty((ng, 7), dtype=torch.float64, device=rows.device)
+        if ng == 0:
+            return out
+        cur = self._sync_in(rows.device)
+        self._ck(self.L.sph_decomp_group_boxes_device(self.ctx, ng, self._p(starts), self._p(counts), rows.shape[1],
+                                                      self._p(rows), self._p(bound), self._p(out)),
+                 "sph_decomp_group_boxes_device")
+        self._sync_out(cur)
+        return out
+
+    def local_pass(self, x, y, z, m, h0_t, k, n_targets, periodic, box, max_iterations):
+        from .density import _raise_for
+        torch = self.torch
+        n = x.numel()
+        prec = "f32" if x.dtype == torch.float32 else "auto"
+        h = h0_t.to(torch.float64).clone()
+        rho = torch.empty(n_targets, dtype=torch.float64, device=x.device)
+        flags = torch.empty(n_targets, dtype=torch.uint8, device=x.device)
+        prm = self.lib.SphParams(n=n, k=k, max_iterations=max_iterations, precision=self.lib.PRECISION[prec],
+                                 periodic=1 if periodic else 0, box=float(box), kernel=0, reserved=0,
+                                 n_targets=0 if n_targets == n else n_targets)
+        if self.keep_inputs:
+            self.last_inputs = (x, y, z, m, h0_t.clone(), k, n_targets, periodic, box, max_iterations)
+        st = self.lib.SphStats()
+        cur = self._sync_in(x.device)
+        rc = self.L.sph_density_pass_device(self.ctx, prm, self._p(x), self._p(y), self._p(z), self._p(m),
+                                            self._p(h), self._p(rho), self._p(flags), st)
+        self._sync_out(cur)
+        _raise_for(rc, self.ctx)
+        self.last_stats = st.as_dict()
+        todo = np.array(self.last_stats["todo_sizes"], dtype=np.int64)
+        return h, rho, todo
+
+
+class NumpyCompute(TorchOps):
+    """A host pass (numpy arrays in and out) behind the same interface; the
+    CPU tests plug the oracle in here."""
+
+    stream = None
+
+    def __init__(self, local_pass):
+        self.fn = local_pass
+
+    def keys(self, x, y, z, centre, half):
+        import torch
+        pos = np.column_stack([x.double().cpu().numpy(), y.double().cpu().numpy(), z.double().cpu().numpy()])
+        return torch.from_numpy(morton_keys(pos, centre, half).astype(np.int64)).to(x.device)
+
+    def local_pass(self, x, y, z, m, h0_t, k, n_targets, periodic, box, max_iterations):
+        import torch
+        a = [t.double().cpu().numpy() for t in (x, y, z, m, h0_t)]
+        h, rho, todo = self.fn(*a, k, n_targets, periodic, box, max_iterations)
+        return (torch.from_numpy(np.asarray(h, np.float64)).to(x.device),
+                torch.from_numpy(np.asarray(rho, np.float64)).to(x.device), np.asarray(todo, np.int64))
+
+
+# ---------------------------------------------------------------------------
+# the decomposition
+# ---------------------------------------------------------------------------
+@dataclass
+class DecompResult:
+    gid: object           # global ids of the owned particles (tensor, int64)
+    h: object             # converged smoothing length (tensor, f64)
+    rho: object           # density (tensor, f64)
+    todo_hist: np.ndarray  # this rank's rounds histogram (add over ranks -> PassStats.todo_sizes)
+    n_owned: int
+    n_ghosts: int
+    max_bound: float
+
+
+def _comm_device(dist, t):
+    """gloo moves host tensors; NCCL (and in-process ranks) device tensors."""
+    return "cpu" if dist.get_backend() == "gloo" else t.device
+
+
+def _exchange(dist, rows, send_counts):
+    """All-to-all of row blocks: rows[sum(send_counts[:q]) : ...] go to rank q."""
+    import torch
+    cdev = _comm_device(dist, rows)
+    sc = send_counts.to(device=cdev, dtype=torch.int64)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc)
+    sl = sc.cpu().tolist()
+    rl = rc.cpu().tolist()
+    width = rows.shape[1]
+    recv = torch.empty(int(sum(rl)) * width, dtype=rows.dtype, device=cdev)
+    dist.all_to_all_single(recv, rows.reshape(-1).to(cdev), output_split_sizes=[c * width for c in rl],
+                           input_split_sizes=[c * width for c in sl])
+    return recv.to(rows.device).reshape(-1, width)
+
+
+def _all_gather_var(dist, t, world):
+    """all-gather of a 2-D tensor whose row count differs per rank."""
+    import torch
+    cdev = _comm_device(dist, t)
+    cnt = torch.tensor([t.shape[0]], dtype=torch.int64, device=cdev)
+    cnts = [torch.empty_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt)
+    cnts = [int(c.item()) for c in cnts]
+    mx = max(max(cnts), 1)
+    pad = torch.zeros((mx, t.shape[1]), dtype=t.dtype, device=cdev)
+    pad[:t.shape[0]] = t.to(cdev)
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad)
+    return [o[:c].to(t.device) for o, c in zip(outs, cnts)]
+
+
+def level_bounds(keys_sorted, k: int, half: float):
+    """Per particle (key order) a guaranteed upper bound of its K-th neighbour
+    distance among these particles: sqrt(3) x the side of the deepest key cube
+    holding it together with >= K others (inf when there are <= K particles).
+    torch restatement of k_level_bounds (csrc/sph_decomp.cu)."""
+    import torch
+    n = keys_sorted.numel()
+    dev = keys_sorted.device
+    w = k + 1
+    if n < w:
+        return torch.full((n,), float("inf"), dtype=torch.float64, device=dev)
+    a = keys_sorted[: n - w + 1]
+    b = keys_sorted[w - 1:]
+    # deepest common level of each window of K+1 consecutive keys
+    lvl = torch.zeros(n - w + 1, dtype=torch.int64, device=dev)
+    for level in range(1, KEY_LEVELS + 1):
+        sh = 63 - 3 * level
+        lvl += ((a >> sh) == (b >> sh)).to(torch.int64)
+    # a particle's level = the max over the windows containing it
+    padv = torch.full((w - 1,), -1, dtype=torch.int64, device=dev)
+    lv = torch.cat([padv, lvl, padv]).to(torch.float32).view(1, 1, -1)
+    lvp = torch.nn.functional.max_pool1d(lv, kernel_size=w, stride=1).view(-1).to(torch.int64)
+    side = (2.0 * half) * torch.pow(torch.tensor(0.5, dtype=torch.float64, device=dev), lvp.to(torch.float64))
+    return side * (_SQRT3 * (1.0 + 1e-9))
+
+
+def window_bounds(rows, bound, k: int, bins: int = 32):
+    """min(bound, an upper bound of the K-th neighbour distance from the 2W
+    key-consecutive records around p, W = 3K/2): the upper edge of the
+    linear d2/d2max bin holding their K-th smallest -- torch restatement of
+    k_window_bounds (csrc/sph_decomp.cu), bit for bit."""
+    import torch
+    n = rows.shape[0]
+    if n <= k:
+        return bound
+    w = (3 * k + 1) // 2
+    pos = rows[:, :3]
+    p = torch.arange(n, device=rows.device)
+    s0 = torch.clamp(torch.clamp(p - w, max=n - 1 - 2 * w), min=0)
+    e0 = torch.clamp(s0 + 2 * w, max=n - 1)
+    cols = []
+    for j in range(2 * w + 1):
+        q = s0 + j
+        valid = (q <= e0) & (q != p)
+        d = pos[torch.clamp(q, max=n - 1)] - pos
+        d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        cols.append(torch.where(valid, d2, torch.full_like(d2, -1.0)))
+    d2 = torch.stack(cols, dim=1)
+    d2max = d2.max(dim=1).values
+    ok = d2max > 0
+    safe = torch.where(ok, d2max, torch.ones_like(d2max))
+    bq = torch.clamp(((d2 / safe[:, None]) * float(bins)).to(torch.int64), max=bins - 1)
+    bq = torch.where(d2 >= 0, bq, torch.full_like(bq, bins))  # excluded slots
+    counts = torch.zeros((n, bins + 1), dtype=torch.int64, device=rows.device)
+    counts.scatter_add_(1, bq, torch.ones_like(bq))
+    cum = torch.cumsum(counts[:, :bins], dim=1)
+    enough = cum[:, -1] >= k
+    first = torch.argmax((cum >= k).to(torch.int64), dim=1)
+    e2 = ((first + 1).to(torch.float64) / float(bins)) * d2max
+    cand = torch.sqrt(e2) * (1.0 + 1e-9)
+    use = ok & enough
+    return torch.where(use, torch.minimum(bound, cand), bound)
+
+
+def ghost_mask(gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk=1 << 22):
+    """Bit q of mask[i]: particle i lies within a group of rank q's margin of
+    that group's box -- torch restatement of k_ghost_mask (csrc/sph_decomp.cu)."""
+    import torch
+    dev = rows.device
+    n = rows.shape[0]
+    mask = torch.zeros(n, dtype=torch.int64, device=dev)
+    ng, nf = gdesc.shape[0], fdesc.shape[0]
+    if ng == 0 or nf == 0:
+        return mask.to(torch.int32)
+    flo, fhi = fdesc[:, :3], fdesc[:, 3:6]
+    fm2 = (fdesc[:, 6] * (1.0 + 1e-9)) ** 2
+    mlo, mhi = gdesc[:, :3], gdesc[:, 3:6]
+    opos = rows[:, :3]
+    step = max(1, pair_chunk // nf)
+    for g0 in range(0, ng, step):
+        g1 = min(ng, g0 + step)
+        d2 = _gap2(mlo[g0:g1, None, :], mhi[g0:g1, None, :], flo[None], fhi[None], periodic, box)
+        gi, fi = torch.nonzero(d2 <= fm2[None], as_tuple=True)
+        if gi.numel() == 0:
+            continue
+        gi = gi + g0
+        cnt = gcount[gi]
+        pidx = torch.repeat_interleave(gstart[gi], cnt)
+        within = torch.arange(pidx.numel(), device=dev) - torch.repeat_interleave(torch.cumsum(cnt, 0) - cnt, cnt)
+        pidx = pidx + within
+        fi = torch.repeat_interleave(fi, cnt)
+        p = opos[pidx]
+        keep = _gap2(p, p, flo[fi], fhi[fi], periodic, box) <= fm2[fi]
+        for q in torch.unique(frank[fi][keep]).tolist():  # ranks < 32: one bit each
+            mask[pidx[keep & (frank[fi] == q)]] |= 1 << int(q)
+    return mask.to(torch.int32)
+
+
+def _gap2(alo, ahi, blo, bhi, periodic, box):
+    """Squared distance between boxes [alo, ahi] and [blo, bhi] (rows
+    broadcast), min-image per axis when periodic."""
+    import torch
+    d = torch.clamp(torch.maximum(blo - ahi, alo - bhi), min=0.0)
+    if periodic:
+        dm = torch.clamp(torch.maximum((blo - box) - ahi, alo - (bhi - box)), min=0.0)
+        dp = torch.clamp(torch.maximum((blo + box) - ahi, alo - (bhi + box)), min=0.0)
+        d = torch.minimum(d, torch.minimum(dm, dp))
+    return (d * d).sum(dim=-1)
+
+
+def decomposed_pass(x, y, z, mass, h0, gid, k: int, compute, *, periodic: bool = False, box: float = 0.0,
+                    samples: int = 1024, max_iterations: int = 100, group_particles: int = 256,
+                    pair_chunk: int = 1 << 22, comm=None) -> DecompResult:
+    """Collective call: every rank passes its local particles (any split) as
+    1-D tensors on its compute device (positions f32 or f64, mass/h0 f64,
+    gid int64).  Returns the owned particles' global ids, h and rho.
+    ``comm`` defaults to torch.distributed (``ThreadComm``: in-process ranks)."""
+    import contextlib
+
+    import torch
+    if comm is None:
+        import torch.distributed as comm
+    stream = getattr(compute, "stream", None)
+    ctxm = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctxm:
+        return _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_iterations,
+                           group_particles, pair_chunk, comm)
+
+
+class ThreadComm:
+    """The collectives of ``decomposed_pass`` between ranks that are threads
+    of one process (one shared ``ThreadWorld``): checks the decomposition at
+    world sizes beyond the GPUs at hand.  Host-side barriers only; no kernel
+    waits on another rank."""
+
+    def __init__(self, world_state, rank: int):
+        import torch.distributed as tdist
+        self.W = world_state
+        self.rank = rank
+        self.ReduceOp = tdist.ReduceOp
+
+    def get_rank(self):
+        return self.rank
+
+    def get_world_size(self):
+        return self.W.world
+
+    def get_backend(self):
+        return "thread"
+
+    def _swap(self, obj):
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+        self.W.slots[self.rank] = obj
+        self.W.barrier.wait()
+        vals = list(self.W.slots)
+        self.W.barrier.wait()
+        return vals
+
+    def all_reduce(self, t, op=None):
+        import torch
+        vals = self._swap(t.clone())
+        st = torch.stack([v.to(t.device) for v in vals])
+        if op is None or op == self.ReduceOp.SUM:
+            r = st.sum(0)
+        elif op == self.ReduceOp.MAX:
+            r = st.max(0).values
+        else:
+            r = st.min(0).values
+        t.copy_(r)
+
+    def all_gather(self, outs, t):
+        vals = self._swap(t.clone())
+        for o, v in zip(outs, vals):
+            o.copy_(v.to(o.device))
+
+    def all_to_all_single(self, out, inp, output_split_sizes=None, input_split_sizes=None):
+        import torch
+        w = self.W.world
+        if input_split_sizes is None:
+            input_split_sizes = [inp.numel() // w] * w
+        chunks = [c.clone() for c in torch.split(inp, input_split_sizes)]
+        vals = self._swap(chunks)
+        got = [vals[q][self.rank].to(out.device) for q in range(w)]
+        out.copy_(torch.cat(got) if got else out)
+
+
+class ThreadWorld:
+    def __init__(self, world: int):
+        import threading
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+
+
+def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_iterations, group_particles,
+                pair_chunk, dist):
+    import os
+    import time
+
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = x.device
+    pdt = x.dtype
+    f64 = torch.float64
+    n_local = x.numel()
+    cdev = _comm_device(dist, x)
+    _tm = [] if os.environ.get("SPH_DECOMP_TIMING") else None
+
+    def mark(name):
+        if _tm is not None:
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            _tm.append((name, time.perf_counter()))
+    mark("start")
+
+    # 1. common root cube; global particle count
+    big = float(np.finfo(np.float64).max)
+    if n_local:
+        mx = [torch.aminmax(t) for t in (x, y, z)]
+        lo = torch.stack([v.min for v in mx]).to(f64)
+        hi = torch.stack([v.max for v in mx]).to(f64)
+    else:
+        lo = torch.full((3,), big, dtype=f64, device=dev)
+        hi = torch.full((3,), -big, dtype=f64, device=dev)
+    mm = torch.cat([-lo, hi, torch.tensor([float(n_local)], dtype=f64, device=dev)]).to(cdev)
+    nl = mm[6:].clone()
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+    dist.all_reduce(nl)
+    mm = mm.cpu().numpy()
+    n_total = int(nl.item())
+    centre, half = root_cube(-mm[:3], mm[3:6])
+    mark("bbox")
+
+    # 2. keys, splitters, key-sorted records, redistribution
+    keys = compute.keys(x, y, z, centre, half)
+    sk, order = torch.sort(keys)
+    if n_local:
+        idx = torch.linspace(0, n_local - 1, samples, device=dev).round().to(torch.int64)
+        mine = sk[idx]
+    else:
+        mine = torch.full((samples,), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
+    gathered = [torch.empty(samples, dtype=torch.int64, device=cdev) for _ in range(world)]
+    dist.all_gather(gathered, mine.to(cdev))
+    allk = torch.sort(torch.cat(gathered)).values.to(dev)
+    splitters = allk[(torch.arange(1, world, device=dev) * allk.numel()) // world]
+    cuts = torch.searchsorted(sk, splitters)  # rank q owns keys in [splitter[q-1], splitter[q])
+    edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts,
+                       torch.full((1,), n_local, dtype=torch.int64, device=dev)])
+    rows = compute.pack_rows(order, x, y, z, mass.to(f64), h0.to(f64), gid.to(torch.int64), keys)
+    mark("keys+pack")
+    recv = _exchange(dist, rows, edges[1:] - edges[:-1])
+    mark("redistribute")
+    okeys, o2 = torch.sort(compute.row_keys(recv), stable=True)
+    owned = compute.gather_rows(recv, o2)
+    n_own = owned.shape[0]
+    mark("sort owned")
+
+    # 3. bounds, 4. descriptors (groups of a coarse key prefix)
+    bound = compute.window_bounds(owned, compute.level_bounds(okeys, k, half), k)
+    gl = int(min(KEY_LEVELS, max(1, round(math.log(max(n_total / group_particles, 1.0), 8)))))
+    if n_own:
+        # a descriptor = <= group_particles consecutive records of one key cube
+        pref = okeys >> (63 - 3 * gl)
+        newg = torch.ones(n_own, dtype=torch.bool, device=dev)
+        newg[1:] = pref[1:] != pref[:-1]
+        cstart = torch.nonzero(newg).view(-1)
+        ccnt = torch.diff(torch.cat([cstart, torch.full((1,), n_own, dtype=torch.int64, device=dev)]))
+        nch = (ccnt + group_particles - 1) // group_particles
+        first = torch.cumsum(nch, 0) - nch
+        j = torch.arange(int(nch.sum().item()), device=dev) - torch.repeat_interleave(first, nch)
+        gstart = torch.repeat_interleave(cstart, nch) + j * group_particles
+        gcnt = torch.diff(torch.cat([gstart, torch.full((1,), n_own, dtype=torch.int64, device=dev)]))
+        desc = compute.group_boxes(owned, bound, gstart, gcnt)
+    else:
+        desc = torch.zeros((0, 7), dtype=f64, device=dev)
+        gcnt = torch.zeros(0, dtype=torch.int64, device=dev)
+        gstart = gcnt
+    descs = _all_gather_var(dist, desc, world)
+    mark("bounds+descriptors")
+
+    # 5. ghosts: my particles within a peer group's bound of that group's box
+    if world > 32:
+        raise ValueError("the ghost masks hold up to 32 ranks")
+    fr = [d for q, d in enumerate(descs) if q != rank]
+    if fr and n_own:
+        fdesc = torch.cat(fr)
+        frank = torch.cat([torch.full((d.shape[0],), q, dtype=torch.int32, device=dev)
+                           for q, d in enumerate(descs) if q != rank])
+        mask = compute.ghost_mask(desc, gstart, gcnt, owned, fdesc, frank, periodic, box)
+        sel = [torch.nonzero((mask >> q) & 1).view(-1) for q in range(world)]
+        gp = torch.cat(sel)
+        gcounts = torch.tensor([t.numel() for t in sel], dtype=torch.int64, device=dev)
+    else:
+        gp = torch.zeros(0, dtype=torch.int64, device=dev)
+        gcounts = torch.zeros(world, dtype=torch.int64, device=dev)
+    mark("ghost select")
+    ghosts = _exchange(dist, compute.gather_rows(owned, gp), gcounts)
+    mark("ghost exchange")
+
+    # 6. final pass: owned targets first, then ghosts
+    allp = torch.cat([owned, ghosts]) if ghosts.shape[0] else owned
+    if n_own:
+        ax, ay, az = (allp[:, i].to(pdt).contiguous() for i in range(3))
+        h, rho, todo = compute.local_pass(ax, ay, az, allp[:, 3].contiguous(), owned[:, 4].contiguous(), k,
+                                          n_own, periodic, box, max_iterations)
+    else:
+        h = rho = torch.zeros(0, dtype=f64, device=dev)
+        todo = np.zeros(0, dtype=np.int64)
+    mark("final pass")
+    if _tm is not None and rank == 0:
+        print("[decomp] " + " ".join(f"{_tm[i][0]} {1e3 * (_tm[i][1] - _tm[i - 1][1]):.2f}"
+                                     for i in range(1, len(_tm))), flush=True)
+    hist = hist_from_todo_sizes(np.asarray(todo, dtype=np.int64), max_iterations)
+    mb = float(bound.max().item()) if n_own else 0.0
+    return DecompResult(gid=owned[:, 5].to(torch.int64), h=h, rho=rho, todo_hist=hist, n_owned=n_own,
+                        n_ghosts=int(ghosts.shape[0]), max_bound=mb)
+
+
+# ---------------------------------------------------------------------------
+# numpy front end (host arrays in and out)
+# ---------------------------------------------------------------------------
+@dataclass
+class DistResult:
+    gid: np.ndarray
+    h: np.ndarray
+    rho: np.ndarray
+    todo_hist: np.ndarray
+    n_ghosts: int
+    margin: float
+
+
+def density_pass_distributed(x, y, z, mass, h0, gid, k: int, local_pass, *, periodic: bool = False,
+                             box: float = 0.0, samples: int = 1024, device="cpu",
+                             max_iterations: int = 100) -> DistResult:
+    """``decomposed_pass`` on host arrays.  ``local_pass`` is either a host
+    function ``(x, y, z, mass, h0_targets, k, n_targets, periodic, box,
+    max_iterations) -> (h, rho, todo_sizes)`` (numpy) or a compute backend
+    (``LibCompute``)."""
+    import torch
+    compute = local_pass if hasattr(local_pass, "local_pass") else NumpyCompute(local_pass)
+    if isinstance(compute, LibCompute):
+        device = f"cuda:{compute.device}"
+    xa = np.asarray(x)
+    pdt = torch.float32 if xa.dtype == np.float32 else torch.float64
+
+    def t(a, dt):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+
+    r = decomposed_pass(t(x, pdt), t(y, pdt), t(z, pdt), t(mass, torch.float64), t(h0, torch.float64),
+                        t(gid, torch.int64), k, compute, periodic=periodic, box=box, samples=samples,
+                        max_iterations=max_iterations)
+    return DistResult(gid=r.gid.cpu().numpy(), h=r.h.cpu().numpy(), rho=r.rho.cpu().numpy(),
+                      todo_hist=r.todo_hist, n_ghosts=r.n_ghosts, margin=r.max_bound)
+
+
 def gpu_local_pass(device: int = 0):
     """The product per-rank compute: libsph_b200 on this rank's GPU."""
-    from .density import density_pass_soa
-
-    def run(x, y, z, m, h0_t, k, n_targets, periodic, box, max_iterations):
-        h, rho, _, st = density_pass_soa(x, y, z, m, h0_t, k, max_iterations, precision="auto",
-                                         periodic=periodic, box=box, device=device, n_targets=n_targets)
-        return h, rho, st.todo_sizes
-
-    return run
+    return LibCompute(device)

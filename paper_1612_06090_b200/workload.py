@@ -196,6 +196,27 @@ def config(number: int, seed: int | None = None):
     raise ValueError(f"unknown config {number}")
 
 
+def config_weak(number: int, n_ranks: int, seed: int | None = None):
+    """Weak-scaled form of config ``number`` for ``n_ranks`` GPUs: n_ranks
+    times the particles, halos and volume (box side x n_ranks^(1/3)) of the
+    one-GPU config, the same generator; n_ranks = 1 is ``config(number)``."""
+    if n_ranks == 1 or number not in (2, 3, 6):
+        return config(number, seed)
+    seed = number if seed is None else seed
+    g = n_ranks ** (1.0 / 3.0)
+    if number in (2, 3):
+        n1, box1, halos1 = {2: (1 << 20, 100.0, 200), 3: (1 << 24, 100.0 * 16 ** (1.0 / 3.0), 20000)}[number]
+        n, box = n1 * n_ranks, box1 * g
+        pos, vel, _ = nfw_halos(n, box, halos1 * n_ranks, seed)
+    else:
+        n, box = (1 << 20) * n_ranks, 100.0 * g
+        pos = (np.random.default_rng(seed).random((n, 3)) * box).astype(np.float32).astype(np.float64)
+        pos[pos >= box] = np.float64(np.nextafter(np.float32(box), np.float32(0.0)))
+        vel = np.zeros((n, 3), np.float32)
+    return dict(pos=pos, vel=vel, mass=np.full(n, 1.0 / n), h0=np.full(n, _initial_h(box, n, 64)), k=64, box=box,
+                periodic=True, fp32=True, name=f"C{number} weak x{n_ranks}: {n} fp32")
+
+
 def _initial_h(box: float, n: int, k: int) -> float:
     # density.py:136-140
     return box * (3.0 * k / (4.0 * math.pi * n)) ** (1.0 / 3.0)

@@ -115,3 +115,83 @@ def test_todo_hist_roundtrip():
     hist = D.hist_from_todo_sizes(todo, 10)
     assert hist.sum() == 100
     assert np.array_equal(D.todo_sizes_from_hist(hist), todo)
+
+
+def test_level_bounds_cover_true_kth_distance():
+    # the search-free bound of the ghost margin is never below the true K-th
+    # neighbour distance (brute force), clustered and uniform points
+    import torch
+    rng = np.random.default_rng(5)
+    pos = np.concatenate([rng.normal(2.0, 0.05, (600, 3)), rng.random((900, 3)) * 4.0])
+    k = 16
+    lo, hi = pos.min(0), pos.max(0)
+    c, half = D.root_cube(lo, hi)
+    keys = D.morton_keys(pos, c, half).astype(np.int64)
+    order = np.argsort(keys, kind="stable")
+    b = D.level_bounds(torch.from_numpy(keys[order]), k, half).numpy()
+    d2 = ((pos[:, None, :] - pos[None, :, :]) ** 2).sum(-1)
+    np.fill_diagonal(d2, np.inf)
+    kth = np.sqrt(np.sort(d2, axis=1)[:, k - 1])
+    assert np.all(b >= kth[order])
+    # and it is not vacuous: within a small factor of h for most particles
+    assert np.median(b / kth[order]) < 8.0
+    # the window bound (K key-consecutive others) is tighter and still covers
+    rows = torch.from_numpy(pos[order])
+    wb = D.window_bounds(rows, torch.from_numpy(b.copy()), k).numpy()
+    assert np.all(wb >= kth[order]) and np.all(wb <= b)
+    assert np.median(wb / kth[order]) < np.median(b / kth[order])
+    # fewer than K+1 particles: no bound
+    assert np.isinf(D.level_bounds(torch.from_numpy(keys[order][:k]), k, half).numpy()).all()
+
+
+def test_key_halves_roundtrip():
+    import torch
+    keys = torch.tensor([0, 1, (1 << 63) - 1, 0x7FF0000000000001, 123456789012345], dtype=torch.int64)
+    hi = (keys >> 32).to(torch.float64)
+    lo = (keys & 0xFFFFFFFF).to(torch.float64)
+    back = (hi.to(torch.int64) << 32) | lo.to(torch.int64)
+    assert torch.equal(back, keys)
+
+
+@pytest.mark.parametrize("world,periodic", [(4, True), (5, False)])
+def test_thread_ranks_match_single_process(world, periodic):
+    # in-process ranks (ThreadComm) over the oracle: the same decomposition at
+    # world sizes beyond what process spawning makes cheap
+    import threading
+
+    import torch
+    n, k, seed = 2400, 16, 13
+    pos, mass, h0, box = _dataset(n, periodic, seed)
+    W = D.ThreadWorld(world)
+    out = [None] * world
+    errs = []
+
+    def run(r):
+        try:
+            sel = np.arange(r, n, world)
+            t = [torch.from_numpy(np.ascontiguousarray(pos[sel, i])) for i in range(3)]
+            res = D.decomposed_pass(*t, torch.from_numpy(mass[sel]), torch.from_numpy(h0[sel]),
+                                    torch.from_numpy(sel.astype(np.int64)), k, D.NumpyCompute(oracle_local_pass),
+                                    periodic=periodic, box=box, samples=64, comm=D.ThreadComm(W, r))
+            out[r] = res
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            W.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not errs, errs
+    gid = np.concatenate([o.gid.numpy() for o in out])
+    assert np.array_equal(np.sort(gid), np.arange(n))
+    h = np.empty(n)
+    rho = np.empty(n)
+    h[gid] = np.concatenate([o.h.numpy() for o in out])
+    rho[gid] = np.concatenate([o.rho.numpy() for o in out])
+    if periodic:
+        want = oracle.density_pass_periodic(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, box, threads=1)
+    else:
+        want = oracle.density_pass(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, threads=1)
+    assert np.array_equal(h, want.h)
+    assert np.array_equal(rho, want.rho)
+    assert np.array_equal(D.todo_sizes_from_hist(sum(o.todo_hist for o in out)), want.todo_sizes)

@@ -58,3 +58,71 @@ def test_two_ranks_match_single_gpu(tmp_path):
     assert np.array_equal(h, want_h)
     assert float(np.max(np.abs(rho - want_rho) / want_rho)) <= 1e-4
     assert np.array_equal(D.todo_sizes_from_hist(sum(p["hist"] for p in parts)), st.todo_sizes)
+
+
+def test_device_keys_match_host_keys():
+    # sph_morton_keys_device (the decomposition's keys) == the numpy restatement
+    import torch
+    from paper_1612_06090_b200 import distributed as D
+    pos, _, _ = _data(20000, 4)
+    lo, hi = pos.min(0).astype(np.float64), pos.max(0).astype(np.float64)
+    c, half = D.root_cube(lo, hi)
+    comp = D.LibCompute(0)
+    for dt in (torch.float32, torch.float64):
+        t = [torch.from_numpy(np.ascontiguousarray(pos[:, i])).to("cuda:0", dtype=dt) for i in range(3)]
+        got = comp.keys(*t, c, half).cpu().numpy()
+        want = D.morton_keys(pos.astype(np.float64), c, half).astype(np.int64)
+        assert np.array_equal(got, want)
+
+
+def test_decomposed_bench_path_single_rank(tmp_path):
+    # the NCCL plumbing of bench.py's multi-GPU path, world size 1 (--decompose)
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT=str(_port()))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "6", "--steps", "2", "--warmup",
+                        "1", "--decompose", "--no-e2e"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["decomposition"]["owned_min"] == 1 << 20
+
+
+def test_library_decomposition_ops_match_torch_ops():
+    # pack / gather / row keys / level bounds / group boxes: kernels == torch restatement
+    import torch
+    from paper_1612_06090_b200 import distributed as D
+    pos, mass, h0 = _data(50000, 6)
+    lib, ref = D.LibCompute(0), D.TorchOps()
+    dev = "cuda:0"
+    x, y, z = (torch.from_numpy(np.ascontiguousarray(pos[:, i])).to(dev) for i in range(3))
+    m = torch.from_numpy(mass).to(dev)
+    hh = torch.from_numpy(h0).to(dev)
+    gid = torch.arange(len(mass), device=dev) * 7 + 3
+    c, half = D.root_cube(pos.min(0).astype(np.float64), pos.max(0).astype(np.float64))
+    keys = lib.keys(x, y, z, c, half)
+    sk, order = torch.sort(keys)
+    rows = lib.pack_rows(order, x, y, z, m, hh, gid, keys)
+    assert torch.equal(rows, ref.pack_rows(order, x, y, z, m, hh, gid, keys))
+    assert torch.equal(lib.row_keys(rows), sk)
+    idx = torch.randperm(len(mass), device=dev)[:1000]
+    assert torch.equal(lib.gather_rows(rows, idx), rows[idx])
+    for k in (16, 64):
+        assert torch.allclose(lib.level_bounds(sk, k, half), ref.level_bounds(sk, k, half), rtol=1e-14, atol=0)
+    b = lib.level_bounds(sk, 64, half)
+    wb = lib.window_bounds(rows, b.clone(), 64)
+    assert torch.allclose(wb, ref.window_bounds(rows, b.clone(), 64), rtol=1e-12, atol=0)
+    assert bool((wb <= b).all())
+    starts = torch.arange(0, len(mass), 300, device=dev)
+    counts = torch.diff(torch.cat([starts, torch.tensor([len(mass)], device=dev)]))
+    gd = lib.group_boxes(rows, b, starts, counts)
+    assert torch.equal(gd, ref.group_boxes(rows, b, starts, counts))
+    # ghost masks against shifted copies of the groups as "foreign" descriptors
+    fd = gd.clone()
+    fd[:, :6] += 0.7
+    fr = (torch.arange(fd.shape[0], device=dev) % 5).to(torch.int32)
+    for periodic in (False, True):
+        got = lib.ghost_mask(gd, starts, counts, rows, fd, fr, periodic, 20.0)
+        want = ref.ghost_mask(gd, starts, counts, rows, fd, fr, periodic, 20.0)
+        assert torch.equal(got, want) and int((got != 0).sum()) > 0

@@ -24,6 +24,7 @@ CONFIGS = {
     "per_target_small_lists": {"SPH_TLISTCAP": "1"},
     "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
     "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
+    "bundle_after_seeds": {"SPH_BUNDLE": "1"},
     "hybrid_bundle_then_per_target": {"SPH_WARP": "0", "SPH_HYBRID": "1"},
     "hybrid_small_lists": {"SPH_WARP": "0", "SPH_HYBRID": "1", "SPH_LISTCAP": "1", "SPH_TLISTCAP": "1"},
     "bundle_rounds_with_lists": {"SPH_WARP": "0", "SPH_HYBRID": "0"},
