@@ -27,6 +27,9 @@ EXPORTED_SYMBOLS = (
     "sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_device_count",
     "sph_density_pass", "sph_density_pass_device", "sph_sort_perm",
     "sph_neighbor_counts", "sph_fnv1a64", "sph_ctx_stream", "sph_fp32_peak", "sph_uniform_box_device",
+    "sph_morton_keys_device", "sph_decomp_pack_rows_device", "sph_decomp_gather_rows_device",
+    "sph_decomp_row_keys_device", "sph_decomp_level_bounds_device", "sph_decomp_window_bounds_device",
+    "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device",
 )
 
 
