@@ -153,7 +153,11 @@ int sph_decomp_row_keys_device(sph_ctx *ctx, int64_t n, const double *d_rows, in
 int sph_decomp_level_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, const int64_t *d_keys_sorted, double half,
                                    double *d_bound);
 int sph_decomp_window_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, int32_t width, const double *d_rows,
-                                    double *d_bound);
+                                    double max_abs_coord, double *d_bound);
+/* per-axis min / max of device-resident positions -> d_out[0..2] = lo,
+ * d_out[3..5] = hi (fp64, device pointer), on the context's stream */
+int sph_bbox_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y, const void *d_z,
+                    double *d_out);
 int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d_gdesc, const int64_t *d_gstart,
                                  const int64_t *d_gcount, int32_t width, const double *d_rows, int64_t n_foreign,
                                  const double *d_fdesc, const int32_t *d_frank, int32_t periodic, double box,

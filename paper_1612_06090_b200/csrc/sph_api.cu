@@ -89,6 +89,7 @@ struct sph_ctx {
   int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
   int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
   DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
+  DevBuf<double> dscratch;  // decomposition helpers: super boxes of the ghost marking
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
@@ -1204,7 +1205,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->dscratch.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
@@ -1433,12 +1434,14 @@ int sph_decomp_level_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, const int
 }
 
 int sph_decomp_window_bounds_device(sph_ctx *ctx, int64_t n, int32_t k, int32_t width, const double *d_rows,
-                                    double *d_bound) {
+                                    double max_abs_coord, double *d_bound) {
   if (!ctx) return SPH_INVALID;
-  if (n < 0 || k < 1 || k > 2048 || width < 3) return fail(ctx, SPH_INVALID, "need n >= 0, 1 <= k <= 2048, width >= 3");
+  if (n < 0 || k < 1 || k > 1024 || width < 3) return fail(ctx, SPH_INVALID, "need n >= 0, 1 <= k <= 1024, width >= 3");
+  if (!(max_abs_coord >= 0.0)) return fail(ctx, SPH_INVALID, "max_abs_coord must be >= 0");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
-  launch_window_bounds(ctx->stream, n, k, width, d_rows, d_bound);
+  // fp32 coordinates are within 2^-24 |x| of the records: 4 such errors per difference, with room
+  launch_window_bounds(ctx->stream, n, k, width, d_rows, max_abs_coord * 1e-6 + 1e-30, d_bound);
   SPH_CK(cudaGetLastError());
   return SPH_OK;
 }
@@ -1451,8 +1454,9 @@ int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d
   if (n_groups < 0 || n_foreign < 0 || width < 3) return fail(ctx, SPH_INVALID, "bad ghost-mask arguments");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
+  SPH_CK(ctx->dscratch.ensure(7 * ((n_foreign + 31) / 32) + 7));
   launch_ghost_mask(ctx->stream, n_groups, d_gdesc, d_gstart, d_gcount, width, d_rows, n_foreign, d_fdesc, d_frank,
-                    periodic, box, d_mask);
+                    periodic, box, d_mask, ctx->dscratch.p);
   SPH_CK(cudaGetLastError());
   return SPH_OK;
 }
@@ -1464,6 +1468,25 @@ int sph_decomp_group_boxes_device(sph_ctx *ctx, int64_t n_groups, const int64_t 
   cudaSetDevice(ctx->device);
   ctx->err.clear();
   launch_group_boxes(ctx->stream, n_groups, d_starts, d_counts, width, d_rows, d_bound, d_out);
+  SPH_CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+int sph_bbox_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y, const void *d_z,
+                    double *d_out) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 1 || n >= (1ll << 31)) return fail(ctx, SPH_INVALID, "n must be in [1, 2^31)");
+  if (precision != SPH_PRECISION_F32 && precision != SPH_PRECISION_F64)
+    return fail(ctx, SPH_INVALID, "precision must be f32 or f64");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = ensure_common(ctx, n, 1);
+  if (rc) return rc;
+  int launches = 0;
+  launch_bbox(ctx->stream, (int)n, precision == SPH_PRECISION_F32 ? 1 : 0, d_x, d_y, d_z, ctx->bbox_ord.p,
+              ctx->root.p, &launches);
+  SPH_CK(cudaMemcpyAsync(d_out, ctx->root.p->lo, 3 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  SPH_CK(cudaMemcpyAsync(d_out + 3, ctx->root.p->hi, 3 * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   SPH_CK(cudaGetLastError());
   return SPH_OK;
 }

@@ -69,27 +69,23 @@ __global__ void k_level_bounds(int64_t n, int k, const int64_t *__restrict__ key
 // to ANY set of others bounds the K-th neighbour distance from above, so take
 // the 2W key-consecutive records around p (W = 3K/2) and bin their squared
 // distances (32 linear bins of d2 / d2max per thread): the upper edge of the
-// bin holding the K-th is an upper bound.  Unfused fp64 (same as the torch
-// restatement, bit for bit)
+// bin holding the K-th is an upper bound.  fp32 arithmetic, made safe by a
+// relative 1e-5 and an absolute slack (fp32 rounding of the coordinates)
 constexpr int kWinTile = 128;
 constexpr int kWinBins = 32;
 __global__ void __launch_bounds__(kWinTile) k_window_bounds(int64_t n, int k, int w, int width,
-                                                            const double *__restrict__ rows,
+                                                            const double *__restrict__ rows, float abs_slack,
                                                             double *__restrict__ bound) {
-  extern __shared__ double sp[];  // (kWinTile + 2w) x 3 positions, then the bins
+  extern __shared__ float4 sp4[];  // kWinTile + 4w positions, then the bins [bin][thread]
   const int64_t b0 = (int64_t)blockIdx.x * kWinTile;
-  const int64_t lo = b0 - w > 0 ? b0 - w : 0;
   const int span = kWinTile + 4 * w;
+  const int64_t base = b0 - 2 * w;
   for (int t = threadIdx.x; t < span; t += blockDim.x) {
-    const int64_t j = b0 - 2 * w + t;
-    if (j >= 0 && j < n) {
-      sp[3 * t] = rows[j * width];
-      sp[3 * t + 1] = rows[j * width + 1];
-      sp[3 * t + 2] = rows[j * width + 2];
-    }
+    const int64_t j = base + t;
+    if (j >= 0 && j < n) sp4[t] = make_float4((float)rows[j * width], (float)rows[j * width + 1],
+                                              (float)rows[j * width + 2], 0.f);
   }
-  (void)lo;
-  unsigned short *bins = reinterpret_cast<unsigned short *>(sp + 3 * span) + threadIdx.x * kWinBins;
+  unsigned short *bins = reinterpret_cast<unsigned short *>(sp4 + span) + threadIdx.x;
   __syncthreads();
   const int64_t p = b0 + threadIdx.x;
   if (p >= n) return;
@@ -97,37 +93,38 @@ __global__ void __launch_bounds__(kWinTile) k_window_bounds(int64_t n, int k, in
     bound[p] = INFINITY;
     return;
   }
-  const int64_t base = b0 - 2 * w;
   int64_t s = p - w;
   if (s > n - 1 - 2 * w) s = n - 1 - 2 * w;
   if (s < 0) s = 0;
   int64_t e = s + 2 * w;
   if (e > n - 1) e = n - 1;
-  const int lp = (int)(p - base);
-  const double px = sp[3 * lp], py = sp[3 * lp + 1], pz = sp[3 * lp + 2];
-  auto d2of = [&](int64_t j) {
-    const int lj = (int)(j - base);
-    const double dx = __dsub_rn(sp[3 * lj], px), dy = __dsub_rn(sp[3 * lj + 1], py), dz = __dsub_rn(sp[3 * lj + 2], pz);
-    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  };
-  double d2max = 0.0;
-  for (int64_t j = s; j <= e; ++j)
-    if (j != p) d2max = fmax(d2max, d2of(j));
-  if (!(d2max > 0.0)) return;  // coincident window: keep the cube bound
-  for (int q = 0; q < kWinBins; ++q) bins[q] = 0;
-  for (int64_t j = s; j <= e; ++j) {
-    if (j == p) continue;
-    const int bq = min((int)__dmul_rn(__ddiv_rn(d2of(j), d2max), (double)kWinBins), kWinBins - 1);
-    ++bins[bq];
+  const int ls = (int)(s - base), le = (int)(e - base), lp = (int)(p - base);
+  const float4 q = sp4[lp];
+  float d2max = 0.f;
+  for (int j = ls; j <= le; ++j) {
+    const float4 c = sp4[j];
+    const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (j != lp) d2max = fmaxf(d2max, d2);
+  }
+  if (!(d2max > 0.f)) return;  // coincident window: keep the cube bound
+  for (int b = 0; b < kWinBins; ++b) bins[b * kWinTile] = 0;
+  const float scale = (float)kWinBins / d2max;
+  for (int j = ls; j <= le; ++j) {
+    const float4 c = sp4[j];
+    const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (j != lp) ++bins[min((int)(d2 * scale), kWinBins - 1) * kWinTile];
   }
   int cum = 0, bq = kWinBins - 1;
-  for (int q = 0; q < kWinBins; ++q) {
-    cum += bins[q];
-    if (cum >= k) { bq = q; break; }
+  for (int b = 0; b < kWinBins; ++b) {
+    cum += bins[b * kWinTile];
+    if (cum >= k) { bq = b; break; }
   }
   if (cum < k) return;  // fewer than K others in the window
-  const double e2 = __dmul_rn((double)(bq + 1) / (double)kWinBins, d2max);
-  bound[p] = fmin(bound[p], sqrt(e2) * (1.0 + 1e-9));
+  // upper edge of the bin (a bin index may be one too low from rounding: +1 bin)
+  const double e2 = (double)min(bq + 2, kWinBins) / (double)kWinBins * (double)d2max;
+  bound[p] = fmin(bound[p], sqrt(e2) * (1.0 + 1e-5) + (double)abs_slack);
 }
 
 // per group of consecutive records: tight box of the positions and the
@@ -185,12 +182,22 @@ __device__ __forceinline__ double box_gap2(const double *a, const double *b, int
 // ghost marking: a particle of my group g is sent to rank q when it lies
 // within the margin of some group f of q (margin = the largest bound on h of
 // f's particles, so every neighbour of f's targets is covered).  One warp per
-// my group: the lanes scan the foreign groups (box vs box), and for each hit
-// the warp tests the group's particles (point vs box) and ORs rank bits.
+// my group: the lanes scan super boxes of 32 consecutive foreign groups (box
+// vs box), then the members of the hit ones, and for each hit member the warp
+// tests the group's particles (point vs box) and ORs the rank bit.
+__device__ __forceinline__ bool desc_hit(const double *gb, const double *__restrict__ d, int periodic, double box) {
+  double fb[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) fb[i] = d[i];
+  const double m = d[6] * (1.0 + 1e-9);
+  return box_gap2(gb, fb, periodic, box) <= m * m;
+}
+
 __global__ void k_ghost_mask(int64_t ng, const double *__restrict__ gdesc, const int64_t *__restrict__ gstart,
                              const int64_t *__restrict__ gcount, int width, const double *__restrict__ rows,
                              int64_t nf, const double *__restrict__ fdesc, const int32_t *__restrict__ frank,
-                             int periodic, double box, uint32_t *__restrict__ mask) {
+                             int64_t nsup, const double *__restrict__ sdesc, int periodic, double box,
+                             uint32_t *__restrict__ mask) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= ng) return;
@@ -198,29 +205,27 @@ __global__ void k_ghost_mask(int64_t ng, const double *__restrict__ gdesc, const
 #pragma unroll
   for (int i = 0; i < 6; ++i) gb[i] = gdesc[7 * g + i];
   const int64_t s = gstart[g], c = gcount[g];
-  for (int64_t f0 = 0; f0 < nf; f0 += 32) {
-    const int64_t f = f0 + lane;
-    bool hit = false;
-    double fb[7];
-    if (f < nf) {
+  for (int64_t s0 = 0; s0 < nsup; s0 += 32) {
+    const int64_t sv = s0 + lane;
+    unsigned sh = __ballot_sync(0xffffffffu, sv < nsup && desc_hit(gb, sdesc + 7 * sv, periodic, box));
+    while (sh) {
+      const int64_t S = s0 + __ffs(sh) - 1;
+      sh &= sh - 1u;
+      const int64_t f = S * 32 + lane;
+      unsigned fm = __ballot_sync(0xffffffffu, f < nf && desc_hit(gb, fdesc + 7 * f, periodic, box));
+      while (fm) {
+        const int64_t fh = S * 32 + __ffs(fm) - 1;
+        fm &= fm - 1u;
+        double hb[6];
 #pragma unroll
-      for (int i = 0; i < 7; ++i) fb[i] = fdesc[7 * f + i];
-      const double m = fb[6] * (1.0 + 1e-9);
-      hit = box_gap2(gb, fb, periodic, box) <= m * m;
-    }
-    unsigned hm = __ballot_sync(0xffffffffu, hit);
-    while (hm) {
-      const int src = __ffs(hm) - 1;
-      hm &= hm - 1u;
-      double hb[7];
-#pragma unroll
-      for (int i = 0; i < 7; ++i) hb[i] = __shfl_sync(0xffffffffu, fb[i], src);
-      const uint32_t bit = 1u << __shfl_sync(0xffffffffu, f < nf ? frank[f] : 0, src);
-      const double m = hb[6] * (1.0 + 1e-9);
-      for (int64_t i = lane; i < c; i += 32) {
-        const double *r = rows + (s + i) * width;
-        const double pb[6] = {r[0], r[1], r[2], r[0], r[1], r[2]};
-        if (box_gap2(pb, hb, periodic, box) <= m * m) atomicOr(mask + s + i, bit);
+        for (int i = 0; i < 6; ++i) hb[i] = fdesc[7 * fh + i];
+        const double m = fdesc[7 * fh + 6] * (1.0 + 1e-9);
+        const uint32_t bit = 1u << frank[fh];
+        for (int64_t i = lane; i < c; i += 32) {
+          const double *r = rows + (s + i) * width;
+          const double pb[6] = {r[0], r[1], r[2], r[0], r[1], r[2]};
+          if (box_gap2(pb, hb, periodic, box) <= m * m) atomicOr(mask + s + i, bit);
+        }
       }
     }
   }
@@ -254,20 +259,41 @@ void launch_level_bounds(cudaStream_t s, int64_t n, int k, const int64_t *keys, 
   if (n > 0) k_level_bounds<<<nb(n), kDT, 0, s>>>(n, k, keys, side0, bound);
 }
 
-void launch_window_bounds(cudaStream_t s, int64_t n, int k, int width, const double *rows, double *bound) {
+void launch_window_bounds(cudaStream_t s, int64_t n, int k, int width, const double *rows, double abs_slack,
+                          double *bound) {
   if (n <= 0) return;
   const int w = (3 * k + 1) / 2;
-  const size_t smem = (size_t)(kWinTile + 4 * w) * 3 * sizeof(double) + kWinTile * kWinBins * sizeof(unsigned short);
+  const size_t smem = (size_t)(kWinTile + 4 * w) * sizeof(float4) + kWinTile * kWinBins * sizeof(unsigned short);
   cudaFuncSetAttribute(k_window_bounds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_window_bounds<<<(unsigned)((n + kWinTile - 1) / kWinTile), kWinTile, smem, s>>>(n, k, w, width, rows, bound);
+  k_window_bounds<<<(unsigned)((n + kWinTile - 1) / kWinTile), kWinTile, smem, s>>>(n, k, w, width, rows,
+                                                                                    (float)abs_slack, bound);
+}
+
+// super boxes of 32 consecutive descriptors (box union, largest margin)
+__global__ void k_super_desc(int64_t nf, const double *__restrict__ fdesc, int64_t nsup, double *__restrict__ sdesc) {
+  const int64_t S = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (S >= nsup) return;
+  double o[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
+  for (int64_t f = S * 32; f < nf && f < S * 32 + 32; ++f) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      o[i] = fmin(o[i], fdesc[7 * f + i]);
+      o[3 + i] = fmax(o[3 + i], fdesc[7 * f + 3 + i]);
+    }
+    o[6] = fmax(o[6], fdesc[7 * f + 6]);
+  }
+#pragma unroll
+  for (int i = 0; i < 7; ++i) sdesc[7 * S + i] = o[i];
 }
 
 void launch_ghost_mask(cudaStream_t s, int64_t ng, const double *gdesc, const int64_t *gstart, const int64_t *gcount,
                        int width, const double *rows, int64_t nf, const double *fdesc, const int32_t *frank,
-                       int periodic, double box, uint32_t *mask) {
-  if (ng > 0 && nf > 0)
-    k_ghost_mask<<<nb(ng * 32), kDT, 0, s>>>(ng, gdesc, gstart, gcount, width, rows, nf, fdesc, frank, periodic, box,
-                                             mask);
+                       int periodic, double box, uint32_t *mask, double *scratch) {
+  if (ng <= 0 || nf <= 0) return;
+  const int64_t nsup = (nf + 31) / 32;
+  k_super_desc<<<nb(nsup), kDT, 0, s>>>(nf, fdesc, nsup, scratch);
+  k_ghost_mask<<<nb(ng * 32), kDT, 0, s>>>(ng, gdesc, gstart, gcount, width, rows, nf, fdesc, frank, nsup, scratch,
+                                           periodic, box, mask);
 }
 
 void launch_group_boxes(cudaStream_t s, int64_t ng, const int64_t *starts, const int64_t *counts, int width,

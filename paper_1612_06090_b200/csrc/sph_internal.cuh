@@ -243,10 +243,11 @@ void launch_pack_rows(cudaStream_t s, int64_t n, int precision_in, const int64_t
 void launch_gather_rows(cudaStream_t s, int64_t n, int width, const int64_t *idx, const double *src, double *dst);
 void launch_row_keys(cudaStream_t s, int64_t n, const double *rows, int64_t *keys);
 void launch_level_bounds(cudaStream_t s, int64_t n, int k, const int64_t *keys, double side0, double *bound);
-void launch_window_bounds(cudaStream_t s, int64_t n, int k, int width, const double *rows, double *bound);
+void launch_window_bounds(cudaStream_t s, int64_t n, int k, int width, const double *rows, double abs_slack,
+                          double *bound);
 void launch_ghost_mask(cudaStream_t s, int64_t ng, const double *gdesc, const int64_t *gstart, const int64_t *gcount,
                        int width, const double *rows, int64_t nf, const double *fdesc, const int32_t *frank,
-                       int periodic, double box, uint32_t *mask);
+                       int periodic, double box, uint32_t *mask, double *scratch);
 void launch_group_boxes(cudaStream_t s, int64_t ng, const int64_t *starts, const int64_t *counts, int width,
                         const double *rows, const double *bound, double *out);
 // 63-bit keys from a given root cube (domain decomposition)

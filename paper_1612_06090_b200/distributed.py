@@ -120,8 +120,13 @@ class TorchOps:
     def level_bounds(self, keys_sorted, k, half):
         return level_bounds(keys_sorted, k, half)
 
-    def window_bounds(self, rows, bound, k):
+    def window_bounds(self, rows, bound, k, max_abs=0.0):
         return window_bounds(rows, bound, k)
+
+    def bbox(self, x, y, z):
+        import torch
+        mx = [torch.aminmax(t) for t in (x, y, z)]
+        return torch.stack([v.min for v in mx] + [v.max for v in mx]).to(torch.float64)
 
     def ghost_mask(self, gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk=1 << 22):
         return ghost_mask(gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk)
@@ -242,15 +247,25 @@ class LibCompute(TorchOps):
         self._sync_out(cur)
         return out
 
-    def window_bounds(self, rows, bound, k):
+    def window_bounds(self, rows, bound, k, max_abs=0.0):
         n = rows.shape[0]
         if n == 0:
             return bound
         cur = self._sync_in(rows.device)
-        self._ck(self.L.sph_decomp_window_bounds_device(self.ctx, n, k, rows.shape[1], self._p(rows), self._p(bound)),
-                 "sph_decomp_window_bounds_device")
+        self._ck(self.L.sph_decomp_window_bounds_device(self.ctx, n, k, rows.shape[1], self._p(rows), float(max_abs),
+                                                        self._p(bound)), "sph_decomp_window_bounds_device")
         self._sync_out(cur)
         return bound
+
+    def bbox(self, x, y, z):
+        torch = self.torch
+        out = torch.empty(6, dtype=torch.float64, device=x.device)
+        prec = self.lib.PRECISION["f32" if x.dtype == torch.float32 else "f64"]
+        cur = self._sync_in(x.device)
+        self._ck(self.L.sph_bbox_device(self.ctx, prec, x.numel(), self._p(x), self._p(y), self._p(z), self._p(out)),
+                 "sph_bbox_device")
+        self._sync_out(cur)
+        return out
 
     def ghost_mask(self, gdesc, gstart, gcount, rows, fdesc, frank, periodic, box, pair_chunk=1 << 22):
         torch = self.torch
@@ -260,6 +275,8 @@ class LibCompute(TorchOps):
         fr = frank.to(torch.int32).contiguous()
         fd = fdesc.contiguous()
         gd = gdesc.contiguous()
+        if self.keep_inputs:
+            self.last_ghost_inputs = (gd, gstart, gcount, rows, fd, fr, periodic, box)
         cur = self._sync_in(rows.device)
         self._ck(self.L.sph_decomp_ghost_mask_device(self.ctx, gd.shape[0], self._p(gd), self._p(gstart),
                                                      self._p(gcount), rows.shape[1], self._p(rows), fd.shape[0],
@@ -598,9 +615,8 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     # 1. common root cube; global particle count
     big = float(np.finfo(np.float64).max)
     if n_local:
-        mx = [torch.aminmax(t) for t in (x, y, z)]
-        lo = torch.stack([v.min for v in mx]).to(f64)
-        hi = torch.stack([v.max for v in mx]).to(f64)
+        bb = compute.bbox(x, y, z)
+        lo, hi = bb[:3], bb[3:]
     else:
         lo = torch.full((3,), big, dtype=f64, device=dev)
         hi = torch.full((3,), -big, dtype=f64, device=dev)
@@ -638,19 +654,16 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     mark("sort owned")
 
     # 3. bounds, 4. descriptors (groups of a coarse key prefix)
-    bound = compute.window_bounds(owned, compute.level_bounds(okeys, k, half), k)
+    max_abs = float(np.max(np.abs(centre)) + half)
+    bound = compute.window_bounds(owned, compute.level_bounds(okeys, k, half), k, max_abs)
     gl = int(min(KEY_LEVELS, max(1, round(math.log(max(n_total / group_particles, 1.0), 8)))))
     if n_own:
         # a descriptor = <= group_particles consecutive records of one key cube
         pref = okeys >> (63 - 3 * gl)
         newg = torch.ones(n_own, dtype=torch.bool, device=dev)
         newg[1:] = pref[1:] != pref[:-1]
-        cstart = torch.nonzero(newg).view(-1)
-        ccnt = torch.diff(torch.cat([cstart, torch.full((1,), n_own, dtype=torch.int64, device=dev)]))
-        nch = (ccnt + group_particles - 1) // group_particles
-        first = torch.cumsum(nch, 0) - nch
-        j = torch.arange(int(nch.sum().item()), device=dev) - torch.repeat_interleave(first, nch)
-        gstart = torch.repeat_interleave(cstart, nch) + j * group_particles
+        newg[::group_particles] = True  # and at most group_particles records each
+        gstart = torch.nonzero(newg).view(-1)
         gcnt = torch.diff(torch.cat([gstart, torch.full((1,), n_own, dtype=torch.int64, device=dev)]))
         desc = compute.group_boxes(owned, bound, gstart, gcnt)
     else:

@@ -95,7 +95,20 @@ def main():
             ms.append(s.elapsed_time(e))
         per_rank.append({"owned": out[r].n_owned, "ghosts": out[r].n_ghosts, "max_bound": out[r].max_bound,
                          "final_pass_ms": min(ms)})
-    res = {"config": args.config, "world": world, "n": n, "h_mismatches": h_mis, "rho_max_rel": rho_rel,
+    # rank 0's ghost marking alone
+    c = comps[0]
+    gm = []
+    for rep in range(3):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(c.stream):
+            s.record()
+            c.ghost_mask(*c.last_ghost_inputs)
+            e.record()
+        e.synchronize()
+        gm.append(s.elapsed_time(e))
+    res = {"config": args.config, "ghost_mask_ms_rank0": min(gm),
+           "n_groups_rank0": int(c.last_ghost_inputs[0].shape[0]), "n_foreign_rank0": int(c.last_ghost_inputs[4].shape[0]), "world": world, "n": n, "h_mismatches": h_mis, "rho_max_rel": rho_rel,
            "single_gpu_pass_ms": t_single, "per_rank": per_rank,
            "final_pass_ms_max": max(p["final_pass_ms"] for p in per_rank),
            "ghost_fraction": sum(p["ghosts"] for p in per_rank) / n}
