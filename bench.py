@@ -407,14 +407,30 @@ def run_decomposed(args, world, rank, local):
 
     from paper_1612_06090_b200 import distributed as D
 
+    # test hooks: SPH_BENCH_DEVICE pins every rank to one GPU and
+    # SPH_BENCH_BACKEND=gloo replaces NCCL, so the torchrun path can be run
+    # with several ranks on a one-GPU box (tests/test_gpu_distributed.py)
+    if os.environ.get("SPH_BENCH_DEVICE") is not None:
+        local = int(os.environ["SPH_BENCH_DEVICE"])
+    backend = os.environ.get("SPH_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world == 1:  # --decompose outside torchrun
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-    tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        tdist.init_process_group(backend)
     device = local
+
+    def red(t, op=None):  # all-reduce in place (host staging for gloo)
+        h = t.cpu() if backend == "gloo" else t
+        tdist.all_reduce(h, op=op if op is not None else tdist.ReduceOp.SUM)
+        if h is not t:
+            t.copy_(h)
+
     w = workload_config(args.config, args.seed, world)
     n_glob, k = w["pos"].shape[0], int(w["k"])
     sel = np.arange(rank, n_glob, world)
@@ -456,15 +472,15 @@ def run_decomposed(args, world, rank, local):
     clk = clocks.stop()
     st = compute.last_stats or {}
     t_local = torch.tensor([sum(step_ms) / len(step_ms)], dtype=torch.float64, device=device)
-    tdist.all_reduce(t_local, op=tdist.ReduceOp.MAX)
+    red(t_local, tdist.ReduceOp.MAX)
     ms_max = float(t_local.item())
     info = torch.tensor([r.n_owned, r.n_ghosts, r.n_owned, r.n_owned], dtype=torch.float64, device=device)
     isum = info.clone()
-    tdist.all_reduce(isum)
+    red(isum)
     imax = info.clone()
-    tdist.all_reduce(imax, op=tdist.ReduceOp.MAX)
+    red(imax, tdist.ReduceOp.MAX)
     imin = info.clone()
-    tdist.all_reduce(imin, op=tdist.ReduceOp.MIN)
+    red(imin, tdist.ReduceOp.MIN)
     value = n_glob * k / (ms_max * 1e-3)
 
     # end to end: pinned host slices in, owned (gid, h, rho) back to the host
@@ -483,7 +499,7 @@ def run_decomposed(args, world, rank, local):
             if i >= args.warmup:
                 e2e_ms.append(dt * 1e3)
         el = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=device)
-        tdist.all_reduce(el, op=tdist.ReduceOp.MAX)
+        red(el, tdist.ReduceOp.MAX)
         es = 4 if f32 else 8
         e2e = {"value": n_glob * k / (float(el.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(len(sel) * (3 * es + 8 + 8 + 8)),

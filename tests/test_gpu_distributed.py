@@ -133,3 +133,25 @@ def test_library_decomposition_ops_match_torch_ops():
         got = lib.ghost_mask(gd, starts, counts, rows, fd, fr, periodic, 20.0)
         want = ref.ghost_mask(gd, starts, counts, rows, fd, fr, periodic, 20.0)
         assert torch.equal(got, want) and int((got != 0).sum()) > 0
+
+
+def test_bench_torchrun_two_ranks_one_gpu():
+    # bench.py's multi-GPU path under torchrun with 2 ranks pinned to the one
+    # GPU (gloo instead of NCCL, which refuses two ranks per device)
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SPH_BENCH_DEVICE="0", SPH_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                        os.path.join(root, "bench.py"), "--gpus", "2", "--config", "6", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 prints the one line
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["n_particles"] == 2 << 20 and line["value"] > 0
+    d = line["decomposition"]
+    assert d["owned_min"] + d["owned_max"] <= 2 << 20 and d["ghosts_total"] > 0
+    assert line["e2e"]["value"] > 0
