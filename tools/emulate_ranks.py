@@ -30,6 +30,7 @@ def main():
     ap.add_argument("config", type=int)
     ap.add_argument("world", type=int)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--group", type=int, default=256)
     args = ap.parse_args()
     world = args.world
     t0 = time.time()
@@ -55,7 +56,7 @@ def main():
             t = [torch.from_numpy(np.ascontiguousarray(pos32[sel, i])).cuda() for i in range(3)]
             res = D.decomposed_pass(*t, torch.from_numpy(w["mass"][sel]).cuda(), torch.from_numpy(w["h0"][sel]).cuda(),
                                     torch.from_numpy(sel.astype(np.int64)).cuda(), k, c, periodic=True, box=box,
-                                    comm=D.ThreadComm(W, r))
+                                    comm=D.ThreadComm(W, r), group_particles=args.group)
             torch.cuda.synchronize()
             out[r] = res
         except Exception as e:
