@@ -87,6 +87,7 @@ struct sph_ctx {
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
   int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
+  int seed_outer = 0;    // SPH_SEED2: a sparser seed level at seed_stride x seed_outer first (0/1 = off; measured slower on C2: launch tails)
   int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
   DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
   DevBuf<double> dscratch;  // decomposition helpers: super boxes of the ghost marking
@@ -180,10 +181,11 @@ __global__ void k_seed_list(int ns, int stride, uint32_t *seeds, int *count) {
 
 // initial radius of the non-seed targets: margin x the larger converged h of
 // the two seeds around them (their own estimate when neither seed converged)
-__global__ void k_seed_radius(int n, int stride, const uint8_t *__restrict__ state, const double *__restrict__ d2k,
-                              float margin, float rmax, float *__restrict__ r0) {
+// (only positions that are multiples of `only`: the next seed level)
+__global__ void k_seed_radius(int n, int stride, int only, const uint8_t *__restrict__ state,
+                              const double *__restrict__ d2k, float margin, float rmax, float *__restrict__ r0) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n || p % stride == 0 || state[p] != ST_NEED_HIST) return;
+  if (p >= n || p % stride == 0 || p % only != 0 || state[p] != ST_NEED_HIST) return;
   const int s0 = p - p % stride, s1 = s0 + stride;
   double h = 0.0;
   if (state[s0] == ST_FINAL) h = d2k[s0];
@@ -648,13 +650,26 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       // neighbours are spatial neighbours): fewer regrows, tighter radii
       const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
       SPH_CK(ctx->seeds.ensure(ns));
-      k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
       PassArgs sa = a;
       sa.list = ctx->seeds.p;
       sa.list_count = ctx->qints.p + 14;
+      const int outer = ctx->seed_stride * ctx->seed_outer;
+      if (ctx->seed_outer > 1 && n >= 64 * outer) {
+        // a sparser seed level first: every outer-th position from the tree's
+        // estimate, then the seeds from those seeds' h (the next launch skips
+        // the outer seeds already settled)
+        const int no = (n + outer - 1) / outer;
+        k_seed_list<<<nblk(no), kTB, 0, ctx->stream>>>(no, outer, ctx->seeds.p, ctx->qints.p + 14);
+        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+        k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, outer, ctx->seed_stride, ctx->state.p, ctx->d2k.p,
+                                                        ctx->seed_margin, rmax, ctx->r0.p);
+        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+        launches += 3;
+      }
+      k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
       launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-      k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, ctx->state.p, ctx->d2k.p, ctx->seed_margin,
-                                                      rmax, ctx->r0.p);
+      k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, 1, ctx->state.p, ctx->d2k.p,
+                                                      ctx->seed_margin, rmax, ctx->r0.p);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       launches += 3;
       if (ctx->bundle && compute_f32) {
@@ -1180,6 +1195,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
   if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
+  if (const char *v = getenv("SPH_SEED2")) c->seed_outer = atoi(v);
   if (const char *v = getenv("SPH_BUNDLE")) c->bundle = atoi(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
