@@ -356,6 +356,7 @@ class DecompResult:
     n_owned: int
     n_ghosts: int
     max_bound: float
+    bound: object = None   # the per-owned-particle bound on h (diagnostics)
 
 
 def _comm_device(dist, t):
@@ -708,7 +709,7 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     hist = hist_from_todo_sizes(np.asarray(todo, dtype=np.int64), max_iterations)
     mb = float(bound.max().item()) if n_own else 0.0
     return DecompResult(gid=owned[:, 5].to(torch.int64), h=h, rho=rho, todo_hist=hist, n_owned=n_own,
-                        n_ghosts=int(ghosts.shape[0]), max_bound=mb)
+                        n_ghosts=int(ghosts.shape[0]), max_bound=mb, bound=bound)
 
 
 # ---------------------------------------------------------------------------
