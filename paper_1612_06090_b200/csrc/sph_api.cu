@@ -91,6 +91,8 @@ struct sph_ctx {
   int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
   DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
   DevBuf<double> dscratch;  // decomposition helpers: super boxes of the ghost marking
+  DevBuf<int> ncell_dev;    // cells of the search tree (counted with the tree, read with n_nodes)
+  int last_ncell = -1;
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
@@ -357,11 +359,25 @@ int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *
   const int in32 = precision == SPH_PRECISION_F32 ? 1 : 0;
   tree_build(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, launches);
   if (search_tree) tree_build_search(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, rmax, launches);
-  int host[2] = {0, 0};
+  int host[3] = {0, 0, -1};
+  const bool index_cells = search_tree && ctx->warp && ctx->cell_lists > 0;
+  if (index_cells) {
+    // cell index of every node, counted before the one sync of this stage
+    // (the node count is still on the device: a grid over its upper bound)
+    SPH_CK(ctx->cellidx.ensure(2 * (size_t)n + 64));
+    SPH_CK(ctx->cellnode.ensure(2 * (size_t)n + 64));
+    SPH_CK(ctx->ncell_dev.ensure(1));
+    SPH_CK(cudaMemsetAsync(ctx->ncell_dev.p, 0, sizeof(int), ctx->stream));
+    launch_cell_index_dev(ctx->stream, ctx->nlo.p, ctx->noff.p + n, 2 * n + 64, ctx->cellidx.p, ctx->cellnode.p,
+                          ctx->ncell_dev.p);
+    SPH_CK(cudaMemcpyAsync(&host[2], ctx->ncell_dev.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ++*launches;
+  }
   SPH_CK(cudaMemcpyAsync(&host[0], ctx->ints.p + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   if (search_tree)
     SPH_CK(cudaMemcpyAsync(&host[1], ctx->noff.p + n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   SPH_CK(cudaStreamSynchronize(ctx->stream));
+  ctx->last_ncell = host[2];
   SPH_CK(cudaGetLastError());
   if (host[0])
     return fail(ctx, SPH_UNSUPPORTED,
@@ -586,6 +602,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   if (rc) return rc;
   tm.mark(2);
   int hist_rounds = 0, band_rounds = 0;
+  bool warp_deferred = false;  // per-target path: fallback counters checked with the results
+  PassArgs warp_args{};
   if (ctx->fused) {
   // ---- search + select + density: one fused persistent kernel over tasks ----
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
@@ -695,23 +713,17 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       if (ctx->cell_lists > 0) {
         // neighbour-cell lists for the radii the seeds imply
         const int cap = ctx->cell_lists;
-        SPH_CK(ctx->cellidx.ensure(n_nodes));
-        SPH_CK(ctx->cellnode.ensure(n_nodes));
-        SPH_CK(cudaMemsetAsync(ctx->qints.p + 13, 0, sizeof(int), ctx->stream));
-        launch_cell_index(ctx->stream, ctx->nlo.p, n_nodes, ctx->cellidx.p, ctx->cellnode.p, ctx->qints.p + 13);
-        int ncell = 0;
-        SPH_CK(cudaMemcpyAsync(&ncell, ctx->qints.p + 13, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        SPH_CK(cudaStreamSynchronize(ctx->stream));
-        if (ctx->clist.ensure(2 * (size_t)ncell * cap) == cudaSuccess && ctx->clen.ensure(ncell) == cudaSuccess &&
-            ctx->crad2.ensure(ncell) == cudaSuccess) {
-          launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->qints.p + 13, cap, ctx->clist.p, ctx->clen.p,
+        const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
+        if (ncell >= 0 && ctx->clist.ensure(2 * (size_t)ncell * cap) == cudaSuccess &&
+            ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess) {
+          launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
                             ctx->crad2.p, ctx->num_sms);
           a.clist = ctx->clist.p;
           a.clen = ctx->clen.p;
           a.crad2 = ctx->crad2.p;
           a.cellidx = ctx->cellidx.p;
           a.clcap = cap;
-          launches += 2;
+          launches += 1;  // (the cell index is counted by stage_tree)
         } else {
           cudaGetLastError();
         }
@@ -740,14 +752,14 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     for (int i = 0; i < 16; ++i) if (cnt[i]) fprintf(stderr, " %d:%d", i, cnt[i]);
     fprintf(stderr, "\n");
   }
-  // fallback counters of the main kernel: [5] overflowed lists [6] bracket
-  // misses [9] stack overflows (one small read; the empty fallback launches are skipped)
-  int q[16];
-  SPH_CK(cudaMemcpyAsync(q, ctx->qints.p, sizeof(q), cudaMemcpyDeviceToHost, ctx->stream));
-  SPH_CK(cudaStreamSynchronize(ctx->stream));
-  int coll_left = 0;
-  if (q[5] + q[6] > 0) {
-    // overflowed lists: the collect instance (bracket list, then the density list)
+  // the collect instance for overflowed lists is enqueued unconditionally: it
+  // reads its target count on the device ([15], appended by the main kernel)
+  // and exits at once when there is none, so no host round trip is needed
+  // here.  The main kernel's other fallback counters ([6] bracket misses, [9]
+  // stack overflows) and the collect instance's ([16..20]) are read with the
+  // results; the walking passes for what is left then run before a second
+  // finalize (never seen in the bench configs).
+  {
     SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
     PassArgs c = a;
     c.list = ctx->list.p;
@@ -755,34 +767,13 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     c.fb_list = nullptr;
     launch_target(ctx->stream, compute_f32, c, ctx->collect_cap, ctx->qints.p + 16, ctx->num_sms, true);
     ++launches;
-    int q2[5];
-    SPH_CK(cudaMemcpyAsync(q2, ctx->qints.p + 16, sizeof(q2), cudaMemcpyDeviceToHost, ctx->stream));
-    SPH_CK(cudaStreamSynchronize(ctx->stream));
-    coll_left = q2[0] + q2[1] + q2[4];
-    if (ctx->debug)
-      fprintf(stderr, "[sph collect] %d targets; still to the walking select: %d overflowed, %d bracket misses, %d stack\n",
-              q[5] + q[6], q2[0], q2[1], q2[4]);
   }
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);
-  if (q[9] > 0) {
-    // targets the stack could not serve: the bundle search passes
-    int hr = 0;
-    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hr);
-    if (rc) return rc;
-    hist_rounds += hr;
-  }
-  if (q[9] > 0 || coll_left > 0) {
-    // targets no list could serve: walking select + density
-    rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
-    if (rc) return rc;
-    tm.mark(4);
-    timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
-    ++launches;
-  } else {
-    tm.mark(4);
-  }
+  warp_deferred = true;
+  warp_args = a;
+  tm.mark(4);
   tm.mark(5);
   } else if (ctx->v3) {
   // ---- "walk once, sweep narrow": k_form groups, one recorded walk per group ----
@@ -1053,21 +1044,46 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   // ---- finalize ----
   int *rounds_hist = ctx->ints.p + kIntsFixed;
-  SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
-  const unsigned long long bad_init = ~0ull;
-  SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->in_h_ready) cudaStreamWaitEvent(ctx->stream, ctx->in_h_ready, 0);  // h0 copied on the side stream
-  k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
-      n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out, rounds_hist,
-      ctx->stats.p + 2);
-  ++launches;
-  tm.mark(6);
   std::vector<int> hist(max_it + 2);
   unsigned long long stat_all[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
-  SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
-  SPH_CK(cudaStreamSynchronize(ctx->stream));
-  SPH_CK(cudaGetLastError());
+  for (int attempt = 0;; ++attempt) {
+    SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
+    const unsigned long long bad_init = ~0ull;
+    SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->in_h_ready) cudaStreamWaitEvent(ctx->stream, ctx->in_h_ready, 0);  // h0 copied on the side stream
+    k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
+        n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out,
+        rounds_hist, ctx->stats.p + 2);
+    ++launches;
+    tm.mark(6);
+    int qd[32];
+    SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
+    SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
+    if (warp_deferred) SPH_CK(cudaMemcpyAsync(qd, ctx->qints.p, sizeof(qd), cudaMemcpyDeviceToHost, ctx->stream));
+    SPH_CK(cudaStreamSynchronize(ctx->stream));
+    SPH_CK(cudaGetLastError());
+    if (!warp_deferred || attempt > 0) break;
+    // fallbacks of the per-target path: [9] stack overflows, [16] + [17] + [20]
+    // what even the collect instance could not serve
+    const int coll_left = qd[16] + qd[17] + qd[20];
+    if (ctx->debug)
+      fprintf(stderr, "[sph collect] %d targets; still to the walking select: %d overflowed, %d bracket misses, %d stack\n",
+              qd[5] + qd[6], qd[16], qd[17], qd[20]);
+    if (qd[9] == 0 && coll_left == 0) break;
+    PassArgs wa = warp_args;
+    if (qd[9] > 0) {
+      // targets the stack could not serve: the bundle search passes
+      int hr = 0;
+      rc = run_rounds(ctx, MODE_HIST, compute_f32, wa, ST_NEED_HIST, 64, &launches, &hr);
+      if (rc) return rc;
+      hist_rounds += hr;
+    }
+    // targets no list could serve: walking select + density
+    rc = run_rounds(ctx, MODE_BAND, compute_f32, wa, ST_NEED_BAND, 64, &launches, &band_rounds);
+    if (rc) return rc;
+    timed_pass(ctx, MODE_DENS, compute_f32, wa, n, ST_DONE);
+    ++launches;
+  }
   collect_kernel_times(ctx, st);
   if (st && ctx->fused) {
     // split the fused kernel's device time over its phases by their warp cycles
@@ -1221,7 +1237,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->dscratch.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->dscratch.release(); c->ncell_dev.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -267,6 +267,8 @@ void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fal
 // bundle pass: 32 consecutive sorted targets per warp (sph_bundle.cu)
 void launch_bundle(cudaStream_t s, const PassArgs &a, int *counters, int num_sms);
 void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells);
+void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes_dev, int max_nodes, int *cellidx,
+                           int *cellnode, int *ncells);
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
                        float4 *clist, int *clen, float *crad2, int num_sms);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,

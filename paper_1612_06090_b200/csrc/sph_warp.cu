@@ -906,7 +906,26 @@ __global__ void k_cell_index(const float4 *__restrict__ nlo, int n_nodes, int *_
   }
 }
 
+// the same with the node count on the device (grid over an upper bound)
+__global__ void k_cell_index_dev(const float4 *__restrict__ nlo, const int *__restrict__ n_nodes_dev,
+                                 int *__restrict__ cellidx, int *__restrict__ cellnode, int *__restrict__ ncells) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= *n_nodes_dev) return;
+  if (__float_as_int(nlo[k].w) == k + 1) {
+    const int ci = atomicAdd(ncells, 1);
+    cellidx[k] = ci;
+    cellnode[ci] = k;
+  } else {
+    cellidx[k] = -1;
+  }
+}
+
 }  // namespace
+
+void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes_dev, int max_nodes, int *cellidx,
+                           int *cellnode, int *ncells) {
+  k_cell_index_dev<<<(max_nodes + 255) / 256, 256, 0, s>>>(nlo, n_nodes_dev, cellidx, cellnode, ncells);
+}
 
 void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells) {
   k_cell_index<<<(n_nodes + 255) / 256, 256, 0, s>>>(nlo, n_nodes, cellidx, cellnode, ncells);
