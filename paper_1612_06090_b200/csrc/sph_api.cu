@@ -69,6 +69,7 @@ struct sph_ctx {
   DevBuf<uint32_t> members;
   DevBuf<int> cells;
   DevBuf<int> noff;
+  DevBuf<int> node_p;
   DevBuf<float4> nlo, nhi;
   DevBuf<int> nsize;
   DevBuf<float> r0;
@@ -292,6 +293,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->ints.ensure(kIntsFixed + (size_t)max_it + 2));
   SPH_CK(ctx->noff.ensure(n + 1));
   SPH_CK(ctx->nlo.ensure(2 * n + 64));
+  SPH_CK(ctx->node_p.ensure(2 * n + 64));
   SPH_CK(ctx->nhi.ensure(2 * n + 64));
   SPH_CK(ctx->nsize.ensure(2 * n + 64));
   SPH_CK(ctx->r0.ensure(n));
@@ -333,6 +335,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.r0_scale = ctx->r0_scale;
   tb.c0_scale = ctx->c0_scale;
   tb.emit_r0 = 1;
+  tb.node_p = ctx->node_p.p;
   return tb;
 }
 
@@ -1237,7 +1240,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->dscratch.release(); c->ncell_dev.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

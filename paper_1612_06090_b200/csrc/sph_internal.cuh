@@ -222,6 +222,7 @@ struct TreeBuffers {
   float r0_scale;                       // initial radius = r0_scale * density estimate
   float c0_scale;                       // ... capped by c0_scale * the cell's own tight-box estimate
   int emit_r0;                          // 0: R0 comes from k_r0 (per-target path) instead of k_node_emit
+  int *node_p;                          // per node: its first sorted position (per-node emission, emit_r0 == 0)
   cudaEvent_t mass_ready;               // optional: wait for it before the masses are read
 };
 

@@ -49,14 +49,38 @@ __global__ void k_bbox(int n, const PosT *__restrict__ x, const PosT *__restrict
   }
   bad = __any_sync(0xffffffffu, bad);
   notf = __any_sync(0xffffffffu, notf);
+  // block reduction first: one set of global atomics per block, not per warp
+  __shared__ double s_mn[3][32], s_mx[3][32];
+  __shared__ int s_bad, s_notf;
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) s_bad = s_notf = 0;
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      atomicMin(&ord[a], dbl_to_ord(mn[a]));
-      atomicMax(&ord[3 + a], dbl_to_ord(mx[a]));
+      s_mn[a][w] = mn[a];
+      s_mx[a][w] = mx[a];
     }
-    if (bad) atomicOr(&root->nonfinite, 1);
-    if (notf) atomicOr(&root->not_f32, 1);
+    if (bad) atomicOr(&s_bad, 1);
+    if (notf) atomicOr(&s_notf, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double v = l < nw ? s_mn[a][l] : INFINITY, u = l < nw ? s_mx[a][l] : -INFINITY;
+      for (int o = 16; o; o >>= 1) {
+        v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+        u = fmax(u, __shfl_xor_sync(0xffffffffu, u, o));
+      }
+      if (l == 0) {
+        atomicMin(&ord[a], dbl_to_ord(v));
+        atomicMax(&ord[3 + a], dbl_to_ord(u));
+      }
+    }
+    if (l == 0 && s_bad) atomicOr(&root->nonfinite, 1);
+    if (l == 0 && s_notf) atomicOr(&root->not_f32, 1);
   }
 }
 
@@ -372,6 +396,66 @@ __global__ void k_node_emit(int n, const unsigned long long *__restrict__ keys, 
   }
 }
 
+// per-node form of k_node_emit for the per-target path (no R0 here: k_r0):
+// k_node_owner records the first position p of every node, then one thread
+// per node descends to its level and finds its end, so the long chains of
+// the top nodes' binary searches run side by side instead of in one thread.
+__global__ void k_node_owner(int n, const int *__restrict__ noff, int *__restrict__ node_p) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  for (int i = noff[p]; i < noff[p + 1]; ++i) node_p[i] = p;
+}
+
+template <bool F32>
+__global__ void k_node_emit_nodes(int n, const unsigned long long *__restrict__ keys, const int *__restrict__ noff,
+                                  const uint8_t *__restrict__ lvl32, const int *__restrict__ node_p,
+                                  const RootInfo *__restrict__ root, const void *__restrict__ pos_sorted,
+                                  float4 *__restrict__ nlo, float4 *__restrict__ nhi, int *__restrict__ nsize) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= noff[n]) return;
+  const int p = node_p[node];
+  const int L = first_level(keys, p) + (node - noff[p]);
+  const int Lc = lvl32[p];
+  const unsigned long long kp = keys[p];
+  const double pad2 = 2.0 * root->pad;
+  double c[3] = {root->c[0], root->c[1], root->c[2]};
+  double half = root->half;
+  for (int l = 1; l <= L; ++l) {  // the reference centre arithmetic down to L
+    const int o = (int)((kp >> (63 - 3 * l)) & 7ull);
+    const double h2 = __dmul_rn(half, 0.5);
+    c[0] = (o & 4) ? __dadd_rn(c[0], h2) : __dsub_rn(c[0], h2);
+    c[1] = (o & 2) ? __dadd_rn(c[1], h2) : __dsub_rn(c[1], h2);
+    c[2] = (o & 1) ? __dadd_rn(c[2], h2) : __dsub_rn(c[2], h2);
+    half = h2;
+  }
+  const int end = (L == 0) ? n : upper_bound_key(keys, p + 1, n, kp | low_mask(L));
+  const int skip = noff[end];
+  float4 lo, hi;
+  if (L < Lc) {
+    const double e = half + pad2;
+    lo = make_float4(f_rd(c[0] - e), f_rd(c[1] - e), f_rd(c[2] - e), __int_as_float(skip));
+    hi = make_float4(f_ru(c[0] + e), f_ru(c[1] + e), f_ru(c[2] + e), __int_as_float(p));
+  } else {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = p; q < end; ++q) {
+      if (F32) {
+        const float4 v = reinterpret_cast<const float4 *>(pos_sorted)[q];
+        mn[0] = fminf(mn[0], v.x); mn[1] = fminf(mn[1], v.y); mn[2] = fminf(mn[2], v.z);
+        mx[0] = fmaxf(mx[0], v.x); mx[1] = fmaxf(mx[1], v.y); mx[2] = fmaxf(mx[2], v.z);
+      } else {
+        const D4 v = reinterpret_cast<const D4 *>(pos_sorted)[q];
+        mn[0] = fminf(mn[0], f_rd(v.x)); mn[1] = fminf(mn[1], f_rd(v.y)); mn[2] = fminf(mn[2], f_rd(v.z));
+        mx[0] = fmaxf(mx[0], f_ru(v.x)); mx[1] = fmaxf(mx[1], f_ru(v.y)); mx[2] = fmaxf(mx[2], f_ru(v.z));
+      }
+    }
+    lo = make_float4(mn[0], mn[1], mn[2], __int_as_float(skip));
+    hi = make_float4(mx[0], mx[1], mx[2], __int_as_float(p));
+  }
+  nlo[node] = lo;
+  nhi[node] = hi;
+  nsize[node] = end - p;
+}
+
 template <typename T>
 __global__ void k_fill(int n, T *a, T v) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -491,6 +575,18 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   k_node_count<<<nblk(n + 1), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff);
   size_t tbytes = tb.cub_temp_bytes;
   cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
+  if (!tb.emit_r0 && tb.node_p) {
+    k_node_owner<<<nblk(n), kTB, 0, s>>>(n, tb.noff, tb.node_p);
+    const int max_nodes = 2 * n + 64;
+    if (compute_f32)
+      k_node_emit_nodes<true><<<nblk(max_nodes), kTB, 0, s>>>(n, tb.keys, tb.noff, tb.lvl32, tb.node_p, tb.root,
+                                                              tb.pos_sorted, tb.nlo, tb.nhi, tb.nsize);
+    else
+      k_node_emit_nodes<false><<<nblk(max_nodes), kTB, 0, s>>>(n, tb.keys, tb.noff, tb.lvl32, tb.node_p, tb.root,
+                                                               tb.pos_sorted, tb.nlo, tb.nhi, tb.nsize);
+    *launches += 4;
+    return 0;
+  }
   if (compute_f32)
     k_node_emit<true><<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff, tb.root, tb.pos_sorted, k, rmax, tb.r0_scale, tb.c0_scale, tb.emit_r0,
                                               tb.nlo, tb.nhi, tb.nsize, tb.r0);
