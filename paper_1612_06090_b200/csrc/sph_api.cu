@@ -93,6 +93,7 @@ struct sph_ctx {
   DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
   DevBuf<double> dscratch;  // decomposition helpers: super boxes of the ghost marking
   DevBuf<int> ncell_dev;    // cells of the search tree (counted with the tree, read with n_nodes)
+  DevBuf<uint32_t> tlist;   // compacted target positions (ghost-aware seeding)
   int last_ncell = -1;
   float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
@@ -193,6 +194,33 @@ __global__ void k_seed_radius(int n, int stride, int only, const uint8_t *__rest
   double h = 0.0;
   if (state[s0] == ST_FINAL) h = d2k[s0];
   if (s1 < n && state[s1] == ST_FINAL) h = fmax(h, d2k[s1]);
+  if (h > 0.0) r0[p] = fminf((float)sqrt(h) * margin, rmax);
+}
+
+// ghost-aware seeding (n_targets < n): seeds and radii along the compacted
+// target order, so targets next to ghosts in sorted order still get seeds
+__global__ void k_seed_list_from(int ns, int stride, const uint32_t *__restrict__ tlist, uint32_t *seeds,
+                                 int *count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *count = ns;
+  if (i < ns) seeds[i] = tlist[(size_t)i * stride];
+}
+
+__global__ void k_seed_radius_from(int nt, int stride, const uint32_t *__restrict__ tlist,
+                                   const uint8_t *__restrict__ state, const double *__restrict__ d2k, float margin,
+                                   float rmax, float *__restrict__ r0) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nt || j % stride == 0) return;
+  const int p = (int)tlist[j];
+  if (state[p] != ST_NEED_HIST) return;
+  const int j0 = j - j % stride, j1 = j0 + stride;
+  const int s0 = (int)tlist[j0];
+  double h = 0.0;
+  if (state[s0] == ST_FINAL) h = d2k[s0];
+  if (j1 < nt) {
+    const int s1 = (int)tlist[j1];
+    if (state[s1] == ST_FINAL) h = fmax(h, d2k[s1]);
+  }
   if (h > 0.0) r0[p] = fminf((float)sqrt(h) * margin, rmax);
 }
 
@@ -687,10 +715,25 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
         launches += 3;
       }
-      k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
-      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-      k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, 1, ctx->state.p, ctx->d2k.p,
-                                                      ctx->seed_margin, rmax, ctx->r0.p);
+      if (n_targets < n) {
+        // ghosts in the set: seed along the target order (compacted targets)
+        SPH_CK(ctx->tlist.ensure(n));
+        launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->tlist.p, ctx->qints.p + 28,
+                      ctx->cub_temp.p, ctx->cub_bytes);
+        const int nst = (n_targets + ctx->seed_stride - 1) / ctx->seed_stride;
+        k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
+                                                             ctx->qints.p + 14);
+        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+        k_seed_radius_from<<<nblk(n_targets), kTB, 0, ctx->stream>>>(n_targets, ctx->seed_stride, ctx->tlist.p,
+                                                                     ctx->state.p, ctx->d2k.p, ctx->seed_margin,
+                                                                     rmax, ctx->r0.p);
+        launches += 2;
+      } else {
+        k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
+        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+        k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, 1, ctx->state.p, ctx->d2k.p,
+                                                        ctx->seed_margin, rmax, ctx->r0.p);
+      }
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       launches += 3;
       if (ctx->bundle && compute_f32) {
@@ -1240,7 +1283,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
