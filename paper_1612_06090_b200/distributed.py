@@ -371,8 +371,7 @@ def _exchange(dist, rows, send_counts):
     sc = send_counts.to(device=cdev, dtype=torch.int64)
     rc = torch.empty_like(sc)
     dist.all_to_all_single(rc, sc)
-    sl = sc.cpu().tolist()
-    rl = rc.cpu().tolist()
+    sl, rl = torch.stack([sc, rc]).cpu().tolist()  # one host round trip
     width = rows.shape[1]
     recv = torch.empty(int(sum(rl)) * width, dtype=rows.dtype, device=cdev)
     dist.all_to_all_single(recv, rows.reshape(-1).to(cdev), output_split_sizes=[c * width for c in rl],
@@ -387,7 +386,7 @@ def _all_gather_var(dist, t, world):
     cnt = torch.tensor([t.shape[0]], dtype=torch.int64, device=cdev)
     cnts = [torch.empty_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt)
-    cnts = [int(c.item()) for c in cnts]
+    cnts = torch.cat(cnts).cpu().tolist()  # one host round trip
     mx = max(max(cnts), 1)
     pad = torch.zeros((mx, t.shape[1]), dtype=t.dtype, device=cdev)
     pad[:t.shape[0]] = t.to(cdev)
@@ -625,8 +624,8 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     nl = mm[6:].clone()
     dist.all_reduce(mm, op=dist.ReduceOp.MAX)
     dist.all_reduce(nl)
-    mm = mm.cpu().numpy()
-    n_total = int(nl.item())
+    mm = torch.cat([mm[:6], nl]).cpu().numpy()  # one host round trip
+    n_total = int(mm[6])
     centre, half = root_cube(-mm[:3], mm[3:6])
     mark("bbox")
 
@@ -683,9 +682,11 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
         frank = torch.cat([torch.full((d.shape[0],), q, dtype=torch.int32, device=dev)
                            for q, d in enumerate(descs) if q != rank])
         mask = compute.ghost_mask(desc, gstart, gcnt, owned, fdesc, frank, periodic, box)
-        sel = [torch.nonzero((mask >> q) & 1).view(-1) for q in range(world)]
-        gp = torch.cat(sel)
-        gcounts = torch.tensor([t.numel() for t in sel], dtype=torch.int64, device=dev)
+        # (rank, particle) pairs grouped by rank: one nonzero over the rank bits
+        bits = (mask.view(1, -1) >> torch.arange(world, device=dev, dtype=mask.dtype).view(-1, 1)) & 1
+        nz = torch.nonzero(bits)
+        gp = nz[:, 1]
+        gcounts = torch.bincount(nz[:, 0], minlength=world)
     else:
         gp = torch.zeros(0, dtype=torch.int64, device=dev)
         gcounts = torch.zeros(world, dtype=torch.int64, device=dev)
