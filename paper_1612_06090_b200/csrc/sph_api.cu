@@ -107,6 +107,7 @@ struct sph_ctx {
   DevBuf<float> crad2;
   int tshrink = 2;       // SPH_TSHRINK
   int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
+  int tchunk = 1;        // SPH_TCHUNK: consecutive targets per work grab of the per-target kernel (2-16 measured slower on C2)
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
   DevBuf<uint2> nlists;
@@ -462,6 +463,7 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.shortcut = ctx->shortcut;
   a.tshrink = ctx->tshrink;
   a.static_sched = ctx->static_sched;
+  a.tchunk = ctx->tchunk;
   if (ctx->debug && ctx->dbg.ensure(8 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
   return a;
 }
@@ -1264,6 +1266,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);
+  if (const char *v = getenv("SPH_TCHUNK")) c->tchunk = atoi(v);
   if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);

@@ -140,6 +140,7 @@ struct PassArgs {
   int lcompact;             // compact the list at a shrink once it holds more entries than this
   int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
   int static_sched;         // per-target kernel: strided static assignment instead of the atomic counter
+  int tchunk;               // per-target kernel: consecutive targets per work grab (identity target order)
   const float4 *clist;      // per-target kernel: neighbour-cell lists (child records) per cell, clcap each
   const int *clen;          // list length per cell (-1: none)
   const float *crad2;       // squared radius a cell's list covers

@@ -28,7 +28,10 @@ namespace sph {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kWarps = 4;
+#ifndef SPH_TARGET_WARPS
+#define SPH_TARGET_WARPS 4
+#endif
+constexpr int kWarps = SPH_TARGET_WARPS;
 #ifndef SPH_HIST_BPO_LOG2
 #define SPH_HIST_BPO_LOG2 3
 #endif
@@ -105,7 +108,10 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   const int count = a.list ? *a.list_count : a.static_count;
   // work in chunks of CH targets per atomic (the collect instance scans sparse
   // targets: whole warps of them)
-  const int CH = (COLLECT && !a.list) ? 32 : 1;  // a compacted list: one target per grab
+  // a compacted list: one target per grab; the identity order: a.tchunk
+  // consecutive targets (neighbours in space: their cell lists and candidates
+  // stay in this SM's L1)
+  const int CH = COLLECT ? (a.list ? 1 : 32) : max(1, min(a.tchunk, 32));
   // static_sched: warp w takes targets w, w + W, ... (no atomic; sorted
   // neighbours, whose costs are alike, land on different warps)
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
