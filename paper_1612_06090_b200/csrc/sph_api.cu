@@ -105,6 +105,9 @@ struct sph_ctx {
   DevBuf<float4> clist;
   DevBuf<int> clen, cellidx, cellnode;
   DevBuf<float> crad2;
+  DevBuf<int> cnear;
+  float near_frac = 0.5f;   // SPH_NEARF: cell-list records beyond near_frac * D go to the list's back
+  float d_pct = 1.0f;       // SPH_DPCT: cell-list radius D = this quantile of the cell's target radii
   int tshrink = 2;       // SPH_TSHRINK
   int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
   int tchunk = 1;        // SPH_TCHUNK: consecutive targets per work grab of the per-target kernel (2-16 measured slower on C2)
@@ -763,9 +766,12 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         const int cap = ctx->cell_lists;
         const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
         if (ncell >= 0 && ctx->clist.ensure(2 * (size_t)ncell * cap) == cudaSuccess &&
-            ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess) {
+            ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
+            ctx->cnear.ensure(ncell) == cudaSuccess) {
           launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
-                            ctx->crad2.p, ctx->num_sms);
+                            ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms);
+          a.cnear = ctx->cnear.p;
+          a.near_frac2 = ctx->near_frac * ctx->near_frac;
           a.clist = ctx->clist.p;
           a.clen = ctx->clen.p;
           a.crad2 = ctx->crad2.p;
@@ -1267,6 +1273,8 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);
   if (const char *v = getenv("SPH_TCHUNK")) c->tchunk = atoi(v);
+  if (const char *v = getenv("SPH_NEARF")) c->near_frac = (float)atof(v);
+  if (const char *v = getenv("SPH_DPCT")) c->d_pct = (float)atof(v);
   if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
   if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
@@ -1286,7 +1294,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -145,6 +145,8 @@ struct PassArgs {
   const int *clen;          // list length per cell (-1: none)
   const float *crad2;       // squared radius a cell's list covers
   const int *cellidx;       // cell index of each node (-1: internal)
+  const int *cnear;         // records of each list within near_frac * D of the cell box (the rest at its back)
+  float near_frac2;         // near_frac^2
   int clcap;
   uint32_t *fb_list;        // per-target kernel: targets left for the collect instance (+ counter)
   int *fb_count;
@@ -272,7 +274,8 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes_dev, int max_nodes, int *cellidx,
                            int *cellnode, int *ncells);
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
-                       float4 *clist, int *clen, float *crad2, int num_sms);
+                       float4 *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
+                       int num_sms);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof);
 // per-cell initial search radius from the node sizes and the parent chain

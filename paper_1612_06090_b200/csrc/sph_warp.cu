@@ -310,14 +310,20 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         // holds the whole search sphere (no cell outside it can be within R)
         // a neighbour-cell list of the target's own cell (built for the radius
         // its seeds imply) replaces the unshifted traversal when it covers R
-        int lbase = -1, llen = 0;
+        int lbase = -1, llen = 0, lnear = 0, lfar_off = 0;
         if (!shifted && a.clist) {
           const int ci = a.cellidx[a.tree.cellof[p]];
           if (ci >= 0) {
             const int len = a.clen[ci];
-            if (len >= 0 && h_r2 <= a.crad2[ci]) {
+            const float cr2 = a.crad2[ci];
+            if (len >= 0 && h_r2 <= cr2) {
               lbase = ci * a.clcap;
               llen = len;
+              lnear = a.cnear[ci];
+              lfar_off = a.clcap - len;  // far records sit at the back of the list
+              // far records lie beyond near_frac * D of the cell box: skipped
+              // when the radius is below that
+              if (h_r2 <= a.near_frac2 * cr2 * (1.0f - 16.0f * kEps)) llen = lnear;
             }
           }
         }
@@ -343,7 +349,10 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         while (lbase >= 0 ? li < llen : top > 0) {
           const float4 *rec = nullptr;
           if (lbase >= 0) {  // 32 listed cells per step
-            if (li + lane < llen) rec = a.clist + 2 * ((size_t)lbase + li + lane);
+            if (li + lane < llen) {
+              const int e = li + lane;
+              rec = a.clist + 2 * ((size_t)lbase + (e < lnear ? e : e + lfar_off));
+            }
             li += 32;
           } else {
             const int np = min(top, 4);
@@ -815,7 +824,8 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
                                                     const float *__restrict__ r0, const int4 *__restrict__ anc4,
                                                     int n_nodes, int n, int root_start, int cap,
                                                     float4 *__restrict__ clist, int *__restrict__ clen,
-                                                    float *__restrict__ crad2) {
+                                                    float *__restrict__ crad2, int *__restrict__ cnear,
+                                                    float near_frac, float d_pct) {
   __shared__ int s_stk[4][kStack];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -829,10 +839,29 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
     const float4 cl = nlo[c], chh = nhi[c];
     const int s0 = __float_as_int(chh.w);
     const int e0 = c + 1 < n_nodes ? __float_as_int(nhi[c + 1].w) : n;
+    // D = the d_pct quantile of the cell's target radii (cells hold <= 32
+    // particles: one per lane); targets above it walk the tree instead
     float D = 0.f;
-    for (int q = s0 + lane; q < e0; q += 32)
-      if (state[q] == ST_NEED_HIST) D = fmaxf(D, r0[q]);
-    for (int o = 16; o; o >>= 1) D = fmaxf(D, __shfl_xor_sync(FULL, D, o));
+    {
+      const int q = s0 + lane;
+      const float Rq = (q < e0 && lane < 32 && state[q] == ST_NEED_HIST) ? r0[q] : 0.f;
+      const unsigned tm = __ballot_sync(FULL, Rq > 0.f);
+      const int cnt = __popc(tm);
+      float mx = Rq;
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+      D = mx;
+      if (cnt > 0 && d_pct < 1.0f && e0 - s0 <= 32) {
+        // rank of each lane's radius among the targets (ties by lane)
+        int rank = 0;
+        for (int l = 0; l < 32; ++l) {
+          const float v = __shfl_sync(FULL, Rq, l);
+          rank += (v > 0.f) && (v < Rq || (v == Rq && l < lane));
+        }
+        const int want = min(cnt - 1, (int)ceilf(d_pct * (float)(cnt - 1)));
+        const unsigned pm = __ballot_sync(FULL, Rq > 0.f && rank == want);
+        if (pm) D = __shfl_sync(FULL, Rq, __ffs(pm) - 1);
+      }
+    }
     if (!(D > 0.f)) {
       if (lane == 0) clen[ci] = -1;
       continue;
@@ -854,7 +883,10 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
       const unsigned hm = __ballot_sync(FULL, holds);
       if (hm) start = __shfl_sync(FULL, my_anc, __ffs(hm) - 1);
     }
-    int len = 0;
+    // records whose gap to the cell box exceeds near_frac * D go to the back
+    // of the list: targets whose radius is below that skip them entirely
+    const float N2 = near_frac * near_frac * D * D;
+    int len = 0, nnear = 0, nfar = 0;
     if (lane == 0) stk[0] = start;
     int top = 1;
     bool over = false;
@@ -866,6 +898,7 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
       const int par = pi < np ? stk[top + pi] : -1;
       __syncwarp();
       bool hit = false, is_cell = false;
+      float g2 = 0.f;
       float4 l4 = make_float4(0.f, 0.f, 0.f, 0.f), h4 = l4;
       if (par >= 0) {
         const float4 *rec = crec + 16 * (size_t)par + 2 * (lane & 7);
@@ -875,24 +908,31 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
         const float gx = fmaxf(fmaxf(l4.x - chh.x, cl.x - h4.x), 0.f);
         const float gy = fmaxf(fmaxf(l4.y - chh.y, cl.y - h4.y), 0.f);
         const float gz = fmaxf(fmaxf(l4.z - chh.z, cl.z - h4.z), 0.f);
-        hit = (gx * gx + gy * gy + gz * gz) * (1.0f - 4.0f * kEps) <= D2;
+        g2 = gx * gx + gy * gy + gz * gz;
+        hit = g2 * (1.0f - 4.0f * kEps) <= D2;
       }
       const unsigned pm = __ballot_sync(FULL, hit && !is_cell);
       if (top + __popc(pm) > kStack) { over = true; break; }
       if (hit && !is_cell) stk[top + __popc(pm & lt)] = __float_as_int(l4.w);
       top += __popc(pm);
-      const unsigned cm = __ballot_sync(FULL, hit && is_cell);
-      if (len + __popc(cm) > cap) { over = true; break; }
+      const bool far = g2 * (1.0f - 4.0f * kEps) > N2;
+      const unsigned cm = __ballot_sync(FULL, hit && is_cell && !far);
+      const unsigned fm = __ballot_sync(FULL, hit && is_cell && far);
+      if (len + __popc(cm) + __popc(fm) > cap) { over = true; break; }
       if (hit && is_cell) {
-        float4 *dst = clist + 2 * ((size_t)ci * cap + len + __popc(cm & lt));
+        const int slot = far ? cap - 1 - (nfar + __popc(fm & lt)) : nnear + __popc(cm & lt);
+        float4 *dst = clist + 2 * ((size_t)ci * cap + slot);
         dst[0] = l4;
         dst[1] = h4;
       }
-      len += __popc(cm);
+      nnear += __popc(cm);
+      nfar += __popc(fm);
+      len = nnear + nfar;
       __syncwarp();
     }
     if (lane == 0) {
       clen[ci] = over ? -1 : len;
+      cnear[ci] = nnear;
       crad2[ci] = D * D;
     }
   }
@@ -938,10 +978,11 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 }
 
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
-                       float4 *clist, int *clen, float *crad2, int num_sms) {
+                       float4 *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
+                       int num_sms) {
   k_cell_lists<<<num_sms * 8, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
                                            a.tree.anc4, a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen,
-                                           crad2);
+                                           crad2, cnear, near_frac, d_pct);
 }
 
 void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *nsize, const int *parent, int n_nodes,
