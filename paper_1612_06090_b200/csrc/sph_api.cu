@@ -80,8 +80,6 @@ struct sph_ctx {
   DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
   bool debug = false;
-  bool fused = false;  // SPH_FUSED=1: single fused search/select/density kernel (experimental)
-  bool v3 = false;     // SPH_V3=1: walk-once / sweep-narrow kernels (sph_knn.cu, experimental)
   bool warp = true;    // SPH_WARP=0: bundle histogram pass first (SPH_HYBRID) or bundle rounds
   bool hybrid = true;  // SPH_HYBRID=0: bundle histogram rounds until settled
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
@@ -120,14 +118,10 @@ struct sph_ctx {
   bool crec_ready = false;
   int tb_emit_r0 = 1;    // did the last tree build compute R0 (k_node_emit)?
   DevBuf<int> ncount;
-  bool v3band = false; // SPH_V3BAND=1: select from the recorded lists (else k_pass BAND tasks)
   int last_legacy = 0;
   DevBuf<uint32_t> mpool;
   DevBuf<int4> sgs;
-  DevBuf<int> owner, v3scratch, lpool;
-  bool mega = false;   // SPH_MEGA=1: work-queue megakernel instead of round-by-round kernels
-  int mega_fallbacks = 0;
-  double last_mega_ms = 0.0;
+  DevBuf<int> owner, lpool;
   DevBuf<int4> items;
   DevBuf<uint32_t> pool;
   DevBuf<uint8_t> band_rounds;
@@ -389,7 +383,7 @@ int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *
   TreeBuffers tb = tree_buffers(ctx);
   tb.mass_ready = ctx->in_mass_ready;
   // the per-target path derives R0 from the node sizes (k_r0) instead
-  tb.emit_r0 = (ctx->warp && !ctx->fused && n <= (1 << 27)) ? 0 : 1;
+  tb.emit_r0 = (ctx->warp && n <= (1 << 27)) ? 0 : 1;
   ctx->tb_emit_r0 = tb.emit_r0;
   const int in32 = precision == SPH_PRECISION_F32 ? 1 : 0;
   tree_build(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, launches);
@@ -633,51 +627,13 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const int compute_f32 = prm->precision == SPH_PRECISION_F32 || (prm->precision == 2 && !root.not_f32);
   const float rmax = compute_rmax(root, prm->periodic, prm->box);
   int n_nodes = 0;
-  ctx->last_mega_ms = 0.0;
   rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
   if (rc) return rc;
   tm.mark(2);
   int hist_rounds = 0, band_rounds = 0;
   bool warp_deferred = false;  // per-target path: fallback counters checked with the results
   PassArgs warp_args{};
-  if (ctx->fused) {
-  // ---- search + select + density: one fused persistent kernel over tasks ----
-  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
-  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  launch_form_only(ctx->stream, compute_f32, a, n, ST_NEED_HIST, ctx->num_sms);
-  SPH_CK(ctx->cells.ensure(fused_cell_list_ints(compute_f32, ctx->num_sms)));
-  FusedArgs fa{};
-  fa.n = n;
-  fa.k = k;
-  fa.kernel_kind = prm->kernel;
-  fa.dens64 = a.dens64;
-  fa.periodic = prm->periodic;
-  fa.box = prm->box;
-  fa.rmax = rmax;
-  fa.nlo = ctx->nlo.p;
-  fa.nhi = ctx->nhi.p;
-  fa.n_nodes = n_nodes;
-  fa.pos = ctx->pos_sorted.p;
-  fa.mass64 = ctx->mass_s.p;
-  fa.r0 = ctx->r0.p;
-  fa.tasks = ctx->tasks.p;
-  fa.members = ctx->members.p;
-  fa.task_count = a.task_count;
-  fa.work_counter = a.work_counter;
-  fa.d2k = ctx->d2k.p;
-  fa.rho = ctx->rho_s.p;
-  fa.state = ctx->state.p;
-  fa.cell_lists = ctx->cells.p;
-  fa.stats = ctx->stats.p;
-  fa.dbg = a.dbg;
-  tm.mark(3);
-  launch_fused(ctx->stream, compute_f32, fa, ctx->num_sms);
-  launches += 2;
-  tm.mark(4);
-  debug_report(ctx, 9, n);
-  tm.mark(5);
-  } else if (ctx->warp && n <= (1 << 27)) {
+  if (ctx->warp && n <= (1 << 27)) {
   // ---- one warp per target: search, exact select and density in one kernel ----
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
@@ -829,160 +785,6 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   warp_args = a;
   tm.mark(4);
   tm.mark(5);
-  } else if (ctx->v3) {
-  // ---- "walk once, sweep narrow": k_form groups, one recorded walk per group ----
-  int rc3 = 0;
-  {
-    const size_t member_cap = 3 * (size_t)n + 1024, list_cap = 160 * (size_t)n + (1u << 20);
-    SPH_CK(ctx->mpool.ensure(member_cap));
-    SPH_CK(ctx->sgs.ensure(3 * (size_t)n + 1024));
-    SPH_CK(ctx->owner.ensure(n));
-    SPH_CK(ctx->v3scratch.ensure(v3_scratch_ints(ctx->num_sms)));
-    if (ctx->lpool.ensure(std::min(list_cap, (size_t)INT32_MAX / 2)) != cudaSuccess) SPH_CK(ctx->lpool.ensure(1 << 22));
-    SPH_CK(ctx->qints.ensure(32));
-    cudaStream_t s = ctx->stream;
-    k_init_state<<<nblk(n), kTB, 0, s>>>(n, n_targets, ctx->perm.p, ctx->state.p);
-    k_iota<<<nblk(n), kTB, 0, s>>>(n, ctx->iota.p);
-    SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), s));
-    SPH_CK(cudaMemsetAsync(ctx->owner.p, 0xff, sizeof(int) * n, s));
-    SPH_CK(cudaMemsetAsync(ctx->qints.p, 0, 8 * sizeof(int), s));  // [0] member cursor [1] list cursor [2] legacy [3] sg total
-    PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-    V3Args v{};
-    v.a = a;
-    v.f32 = compute_f32;
-    v.sgs = ctx->sgs.p;
-    v.members = ctx->mpool.p;
-    v.owner = ctx->owner.p;
-    v.scratch = ctx->v3scratch.p;
-    v.list_pool = ctx->lpool.p;
-    v.list_cursor = ctx->qints.p + 1;
-    v.list_cap = (int)std::min(ctx->lpool.cap, (size_t)INT32_MAX / 2);
-    v.legacy_count = ctx->qints.p + 2;
-    int sg_total = 0, remaining = n_targets;
-    const uint32_t *list = nullptr;
-    if (ctx->debug) fprintf(stderr, "[sph v3] start n=%d nodes=%d\n", n, n_nodes);
-    for (int round = 0; remaining > 0 && round < 24; ++round) {
-      // group this round's targets into the member pool
-      PassArgs f = a;
-      f.list = list;
-      f.members = ctx->mpool.p;
-      f.member_cursor = ctx->qints.p + 0;
-      SPH_CK(cudaMemsetAsync(f.task_count, 0, sizeof(int), s));
-      launch_form_only_keep(s, compute_f32, f, list ? remaining : n, ST_NEED_HIST, ctx->num_sms);
-      k_append_sgs<<<nblk(list ? remaining : n), kTB, 0, s>>>(ctx->tasks.p, f.task_count, ctx->sgs.p, sg_total);
-      v.sg_begin = sg_total;
-      v.sg_count = f.task_count;
-      launch_v3(s, MODE_HIST, v, ctx->num_sms);
-      launches += 3;
-      ++hist_rounds;
-      int tc = 0;
-      SPH_CK(cudaMemcpyAsync(&tc, f.task_count, sizeof(int), cudaMemcpyDeviceToHost, s));
-      launch_select(s, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
-                    ctx->cub_bytes);
-      int mc = 0;
-      SPH_CK(cudaMemcpyAsync(&remaining, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
-      SPH_CK(cudaMemcpyAsync(&mc, ctx->qints.p + 0, sizeof(int), cudaMemcpyDeviceToHost, s));
-      SPH_CK(cudaStreamSynchronize(s));
-      SPH_CK(cudaGetLastError());
-      sg_total += tc;
-      list = ctx->list.p;
-      if (ctx->debug) fprintf(stderr, "[sph v3] hist round %d: %d groups, %d still searching, members %d\n", round, tc, remaining, mc);
-      if ((size_t)mc + (size_t)remaining > member_cap || (size_t)sg_total + (size_t)remaining > ctx->sgs.cap) {
-        k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_NEED_HIST, ST_LEGACY);
-        break;
-      }
-    }
-    if (remaining > 0) k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_NEED_HIST, ST_LEGACY);
-    tm.mark(3);
-    SPH_CK(cudaMemcpyAsync(ctx->qints.p + 3, &sg_total, sizeof(int), cudaMemcpyHostToDevice, s));
-    SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-    // select: every group, lanes whose bracket it found
-    v.sg_begin = 0;
-    v.sg_count = ctx->qints.p + 3;
-    int band_left = ctx->v3band ? 1 : 0;
-    if (!ctx->v3band) {
-      PassArgs b = base_args(ctx, n, k, n_nodes, prm, rmax);
-      rc3 = run_rounds(ctx, MODE_BAND, compute_f32, b, ST_NEED_BAND, 64, &launches, &band_rounds);
-      if (rc3) return rc3;
-    }
-    for (int round = 0; band_left > 0 && round < 40; ++round) {
-      launch_v3(s, MODE_BAND, v, ctx->num_sms);
-      ++launches;
-      ++band_rounds;
-      launch_select(s, ctx->iota.p, n, ctx->state.p, ST_NEED_BAND, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
-                    ctx->cub_bytes);
-      SPH_CK(cudaMemcpyAsync(&band_left, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
-      SPH_CK(cudaStreamSynchronize(s));
-      SPH_CK(cudaGetLastError());
-      if (ctx->debug) fprintf(stderr, "[sph v3] band round %d: %d left\n", round, band_left);
-    }
-    if (band_left > 0) rc3 = fail(ctx, SPH_CUDA_ERROR, "exact K-th neighbour selection did not settle");
-    tm.mark(4);
-    launch_v3(s, MODE_DENS, v, ctx->num_sms);
-    ++launches;
-    // targets the recorded lists could not serve: round-by-round kernels
-    int legacy = 0;
-    SPH_CK(cudaMemcpyAsync(&legacy, ctx->qints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
-    launch_select(s, ctx->iota.p, n, ctx->state.p, ST_LEGACY, ctx->list.p, ctx->ints.p + 2, ctx->cub_temp.p,
-                  ctx->cub_bytes);
-    int nleg = 0;
-    SPH_CK(cudaMemcpyAsync(&nleg, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SPH_CK(cudaStreamSynchronize(s));
-    SPH_CK(cudaGetLastError());
-    ctx->last_legacy = nleg;
-    if (nleg > 0 && rc3 == 0) {
-      k_state_map<<<nblk(n), kTB, 0, s>>>(n, ctx->state.p, ST_LEGACY, ST_NEED_HIST);
-      PassArgs b = base_args(ctx, n, k, n_nodes, prm, rmax);
-      int hr = 0, br = 0;
-      rc = run_rounds(ctx, MODE_HIST, compute_f32, b, ST_NEED_HIST, 64, &launches, &hr);
-      if (rc) return rc;
-      rc = run_rounds(ctx, MODE_BAND, compute_f32, b, ST_NEED_BAND, 64, &launches, &br);
-      if (rc) return rc;
-      timed_pass(ctx, MODE_DENS, compute_f32, b, n, ST_DONE);
-      ++launches;
-    }
-    tm.mark(5);
-  }
-  if (rc3) return rc3;
-  } else if (ctx->mega) {
-  // ---- search + select + density: one persistent kernel over a device work queue ----
-  bool done_mega = false;
-  {
-    const int item_cap = 2 * n + 65536, pool_cap = 4 * n + 65536;
-    if (ctx->items.ensure(item_cap) == cudaSuccess && ctx->pool.ensure(pool_cap) == cudaSuccess &&
-        ctx->band_rounds.ensure(n) == cudaSuccess && ctx->qints.ensure(32) == cudaSuccess) {
-      k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
-      SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-      PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-      tm.mark(3);
-      launch_mega(ctx->stream, compute_f32, a, n, n_targets, ctx->items.p, item_cap, ctx->pool.p, pool_cap,
-                  ctx->qints.p, ctx->band_rounds.p, ctx->num_sms);
-      launches += 3;
-      int ovf = 0;
-      SPH_CK(cudaMemcpyAsync(&ovf, ctx->qints.p + 4, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      SPH_CK(cudaStreamSynchronize(ctx->stream));
-      SPH_CK(cudaGetLastError());
-      tm.mark(4);
-      tm.mark(5);
-      done_mega = ovf == 0;
-      ctx->last_mega_ms = done_mega ? tm.ms(3, 4) : 0.0;
-    }
-  }
-  if (!done_mega) {  // queue storage exhausted: the round-by-round path below
-    ctx->mega_fallbacks++;
-  }
-  if (!done_mega) {
-  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
-  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-  k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
-  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
-  if (rc) return rc;
-  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
-  if (rc) return rc;
-  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
-  ++launches;
-  }
   } else {
   // ---- search ----
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
@@ -1139,19 +941,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     ++launches;
   }
   collect_kernel_times(ctx, st);
-  if (st && ctx->fused) {
-    // split the fused kernel's device time over its phases by their warp cycles
-    const double fused_ms = tm.ms(3, 4);
-    const double cyc = (double)stat_all[5] + (double)stat_all[6] + (double)stat_all[7];
-    for (int i = 0; i < 3; ++i) st->t_kernel_ms[i] = cyc > 0 ? fused_ms * (double)stat_all[5 + i] / cyc : 0.0;
-  }
   if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
-  if (st && ctx->mega && ctx->last_mega_ms > 0.0) st->t_kernel_ms[0] = ctx->last_mega_ms;
-  if (st && ctx->v3 && !ctx->fused) {
-    st->t_kernel_ms[0] = tm.ms(2, 3);
-    st->t_kernel_ms[1] = tm.ms(3, 4);
-    st->t_kernel_ms[2] = tm.ms(4, 5);
-  }
 
   // ---- stats, reference todo trace, error mapping ----
   const long long unconv = hist[max_it + 1];
@@ -1255,10 +1045,6 @@ int sph_ctx_create(sph_ctx **out, int device) {
   for (auto &e : c->kev) cudaEventCreate(&e);
   const char *dbg = getenv("SPH_DEBUG");
   c->debug = dbg && dbg[0] == '1';
-  if (const char *v = getenv("SPH_FUSED")) c->fused = v[0] == '1';
-  if (const char *v = getenv("SPH_MEGA")) c->mega = v[0] == '1';
-  if (const char *v = getenv("SPH_V3")) c->v3 = v[0] == '1';
-  if (const char *v = getenv("SPH_V3BAND")) c->v3band = v[0] == '1';
   if (const char *v = getenv("SPH_LISTS")) c->lists = v[0] == '1';
   if (const char *v = getenv("SPH_WARP")) c->warp = v[0] == '1';
   if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
@@ -1294,7 +1080,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->v3scratch.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);

@@ -152,54 +152,6 @@ struct PassArgs {
   int *fb_count;
 };
 
-// arguments of the fused search/select/density kernel (sph_fused.cu)
-struct FusedArgs {
-  int n, k, kernel_kind, dens64, periodic;
-  double box;
-  float rmax;
-  const float4 *nlo;
-  const float4 *nhi;
-  int n_nodes;
-  const void *pos;
-  const double *mass64;
-  const float *r0;
-  const int2 *tasks;
-  const uint32_t *members;
-  const int *task_count;
-  int *work_counter;
-  double *d2k;
-  double *rho;
-  uint8_t *state;
-  int *cell_lists;
-  unsigned long long *stats;  // [0] tests [1] accepted [2] bad index [3] search tests [4] unsettled
-  unsigned long long *dbg;
-};
-int fused_warps(int f32, int num_sms);
-size_t fused_cell_list_ints(int f32, int num_sms);
-void launch_fused(cudaStream_t s, int f32, const FusedArgs &a, int num_sms);
-void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
-void launch_form_only_keep(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
-void launch_mega(cudaStream_t s, int f32, const PassArgs &a, int n, int n_targets, int4 *items, int item_cap,
-                 uint32_t *pool, int pool_cap, int *qints, uint8_t *band_rounds, int num_sms);
-
-// "walk once, sweep narrow" kernels (sph_knn.cu)
-struct V3Args {
-  PassArgs a;
-  int f32;
-  int4 *sgs;                 // per group: member offset, member count, list offset (-1: none), list length
-  const int *sg_count;       // groups of this launch
-  int sg_begin;              // first group index of this launch
-  const uint32_t *members;   // member pool (all rounds)
-  int *owner;                // per target: group that found its bracket
-  int *scratch;              // per-warp recorded-cell scratch
-  int *list_pool;
-  int *list_cursor;
-  int list_cap;
-  int *legacy_count;
-};
-size_t v3_scratch_ints(int num_sms);
-void launch_v3(cudaStream_t s, int mode, const V3Args &v, int num_sms);
-
 // ---- launchers (sph_tree.cu) ----
 struct TreeBuffers {
   // sort / ordering

@@ -849,159 +849,6 @@ struct StateIs {
   __device__ __forceinline__ bool operator()(const uint32_t &p) const { return state[p] == want; }
 };
 
-
-// ---------------------------------------------------------------------------
-// The pass as one persistent kernel over a device-side work queue.  An item
-// is (phase, group of targets); a warp claims items in FIFO order, runs the
-// sweep of the item's phase, and pushes the follow-up groups itself:
-//   HIST -> BAND (lanes with a bracket) + HIST (lanes that must grow R)
-//   BAND -> DENS (lanes with the exact K-th d2) + BAND (brackets to split)
-//   DENS -> done
-// Follow-up groups are subsets of a spatially coherent group, so they stay
-// coherent.  No host round trip and no global barrier between rounds: the
-// retries of one group overlap the first sweeps of others, and a pass ends
-// when `remaining` (targets not yet final) reaches zero.
-// ---------------------------------------------------------------------------
-struct MegaQ {
-  int4 *items;        // (phase, member offset, count, ready)
-  int *head, *tail;
-  int *remaining;
-  uint32_t *pool;     // member lists
-  int *pool_cursor;
-  uint8_t *band_rounds;
-  int item_cap, pool_cap;
-  int *overflow;
-};
-
-constexpr int kMaxBandRoundsQ = 60;
-
-__device__ __forceinline__ void mega_push(const MegaQ &q, int phase, unsigned mask, int p) {
-  if (!mask) return;
-  const int lane = threadIdx.x & 31;
-  const int nm = __popc(mask);
-  int off = 0, slot = 0;
-  if (lane == 0) {
-    off = atomicAdd(q.pool_cursor, nm);
-    slot = atomicAdd(q.tail, 1);
-  }
-  off = __shfl_sync(FULL, off, 0);
-  slot = __shfl_sync(FULL, slot, 0);
-  if (off + nm > q.pool_cap || slot >= q.item_cap) {
-    if (lane == 0) atomicOr(q.overflow, 1);
-    return;
-  }
-  if ((mask >> lane) & 1u) q.pool[off + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)p;
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    q.items[slot] = make_int4(phase, off, nm, 0);
-    __threadfence();
-    atomicExch(&q.items[slot].w, 1);
-  }
-}
-
-template <bool F32>
-#ifndef SPH_MEGA_MINB
-#define SPH_MEGA_MINB 4
-#endif
-__global__ void __launch_bounds__(kWarps * 32, SPH_MEGA_MINB) k_mega(const PassArgs a, const MegaQ q) {
-  extern __shared__ __align__(32) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  unsigned char *wbase = smem_raw + wib * mode_smem_per_warp<MODE_BAND, F32>();
-  unsigned long long tests = 0, accepted = 0, tests_hist = 0;
-  for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(q.head, 1);
-    i = __shfl_sync(FULL, i, 0);
-    bool done = false;
-    for (;;) {
-      int ready = 0, rem = 1;
-      if (lane == 0) {
-        if (i < q.item_cap) ready = atomicAdd(&q.items[i].w, 0);
-        rem = atomicAdd(q.remaining, 0);
-        if (i >= q.item_cap) rem = 0;
-      }
-      ready = __shfl_sync(FULL, ready, 0);
-      rem = __shfl_sync(FULL, rem, 0);
-      if (ready) break;
-      if (rem <= 0) { done = true; break; }
-      __nanosleep(256);
-    }
-    if (done) break;
-    __threadfence();
-    const int4 it = q.items[i];
-    const int2 task = make_int2(it.y, it.z);
-    const bool member = lane < it.z;
-    const int p = (int)q.pool[it.y + (member ? lane : 0)];
-    if (it.x == MODE_HIST) {
-      const unsigned long long t0 = tests;
-      run_task<MODE_HIST, F32>(a, task, -1, wbase, tests, accepted);
-      tests_hist += tests - t0;
-      const uint8_t st = member ? a.state[p] : 255;
-      mega_push(q, MODE_BAND, __ballot_sync(FULL, st == ST_NEED_BAND), p);
-      mega_push(q, MODE_HIST, __ballot_sync(FULL, st == ST_NEED_HIST), p);
-      const int fin = __popc(__ballot_sync(FULL, st == ST_UNREACHABLE));
-      if (lane == 0 && fin) atomicSub(q.remaining, fin);
-    } else if (it.x == MODE_BAND) {
-      run_task<MODE_BAND, F32>(a, task, -1, wbase, tests, accepted);
-      uint8_t st = member ? a.state[p] : 255;
-      if (st == ST_NEED_BAND) {
-        const int r = ++q.band_rounds[p];
-        if (r > kMaxBandRoundsQ) { st = ST_FAILED; a.state[p] = ST_FAILED; a.d2k[p] = INFINITY; }
-      }
-      mega_push(q, MODE_DENS, __ballot_sync(FULL, st == ST_DONE), p);
-      mega_push(q, MODE_BAND, __ballot_sync(FULL, st == ST_NEED_BAND), p);
-      const int fin = __popc(__ballot_sync(FULL, st == ST_FAILED));
-      if (lane == 0 && fin) {
-        atomicSub(q.remaining, fin);
-        atomicAdd(&a.stats[4], (unsigned long long)fin);
-      }
-    } else {
-      run_task<MODE_DENS, F32>(a, task, -1, wbase, tests, accepted);
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicSub(q.remaining, it.z);
-      }
-    }
-  }
-  for (int o = 16; o; o >>= 1) accepted += __shfl_xor_sync(FULL, accepted, o);
-  if (lane == 0) {
-    atomicAdd(&a.stats[0], tests);
-    atomicAdd(&a.stats[1], accepted);
-    atomicAdd(&a.stats[3], tests_hist);
-  }
-}
-
-template <bool F32>
-int mega_blocks(int num_sms) {
-  static int bps = 0;
-  constexpr int smem = kWarps * mode_smem_per_warp<MODE_BAND, F32>();
-  if (!bps) {
-    cudaFuncSetAttribute(k_mega<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_mega<F32>, kWarps * 32, smem);
-    if (bps < 1) bps = 1;
-  }
-  return num_sms * bps;
-}
-
-// initial items: every task of a k_form run becomes a ready HIST item
-__global__ void k_mega_seed(const int2 *tasks, const int *task_count, const uint32_t *members, MegaQ q) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nt = *task_count;
-  if (t == 0) { *q.tail = nt; *q.head = 0; *q.pool_cursor = *q.pool_cursor; }
-  if (t < nt && t < q.item_cap) {
-    const int2 tk = tasks[t];
-    q.items[t] = make_int4(MODE_HIST, tk.x, tk.y, 1);
-  }
-}
-
-__global__ void k_copy_u32(int n, const uint32_t *in, uint32_t *out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = in[i];
-}
-
 }  // namespace
 
 template <int MODE, bool F32>
@@ -1034,56 +881,6 @@ void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count
     }
   }
 #undef SPH_PASS_CASE
-}
-
-// The work-queue pass: group all targets (k_form), seed the queue, run k_mega.
-// `pool` must hold pool_cap u32, `items` item_cap int4; ints: head, tail,
-// remaining, pool_cursor, overflow (5 ints, zeroed here except remaining).
-void launch_mega(cudaStream_t s, int f32, const PassArgs &a, int n, int n_targets, int4 *items, int item_cap,
-                 uint32_t *pool, int pool_cap, int *qints, uint8_t *band_rounds, int num_sms) {
-  MegaQ q;
-  q.items = items;
-  q.head = qints;
-  q.tail = qints + 1;
-  q.remaining = qints + 2;
-  q.pool_cursor = qints + 3;
-  q.overflow = qints + 4;
-  q.pool = pool;
-  q.pool_cap = pool_cap;
-  q.item_cap = item_cap;
-  q.band_rounds = band_rounds;
-  cudaMemsetAsync(qints, 0, 5 * sizeof(int), s);
-  cudaMemcpyAsync(q.remaining, &n_targets, sizeof(int), cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(items, 0, sizeof(int4) * (size_t)item_cap, s);
-  cudaMemsetAsync(band_rounds, 0, (size_t)n, s);
-  // initial grouping into the member pool's first n entries
-  PassArgs f = a;
-  f.members = pool;
-  f.member_cursor = q.pool_cursor;
-  cudaMemsetAsync(f.task_count, 0, sizeof(int), s);
-  if (f32) launch_form<MODE_HIST, true>(s, f, n, ST_NEED_HIST, num_sms);
-  else launch_form<MODE_HIST, false>(s, f, n, ST_NEED_HIST, num_sms);
-  k_mega_seed<<<(n + 255) / 256, 256, 0, s>>>(a.tasks, a.task_count, pool, q);
-  PassArgs m = a;
-  m.dbg = nullptr;
-  m.members = pool;  // item offsets index the member pool
-  if (f32)
-    k_mega<true><<<mega_blocks<true>(num_sms), kWarps * 32, kWarps * mode_smem_per_warp<MODE_BAND, true>(), s>>>(m, q);
-  else
-    k_mega<false><<<mega_blocks<false>(num_sms), kWarps * 32, kWarps * mode_smem_per_warp<MODE_BAND, false>(), s>>>(m, q);
-}
-
-// grouping only, appending to the member pool at *a.member_cursor (not reset)
-void launch_form_only_keep(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {
-  if (f32) launch_form<MODE_HIST, true>(s, a, count, want, num_sms);
-  else launch_form<MODE_HIST, false>(s, a, count, want, num_sms);
-}
-
-void launch_form_only(cudaStream_t s, int f32, const PassArgs &a, int count, uint8_t want, int num_sms) {
-  cudaMemsetAsync(a.task_count, 0, sizeof(int), s);
-  cudaMemsetAsync(a.member_cursor, 0, sizeof(int), s);
-  if (f32) launch_form<MODE_HIST, true>(s, a, count, want, num_sms);
-  else launch_form<MODE_HIST, false>(s, a, count, want, num_sms);
 }
 
 size_t select_temp_needed(int n) {

@@ -519,9 +519,18 @@ def decomposed_pass(x, y, z, mass, h0, gid, k: int, compute, *, periodic: bool =
         import torch.distributed as comm
     stream = getattr(compute, "stream", None)
     ctxm = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    caller = torch.cuda.current_stream(x.device) if stream is not None else None
     with ctxm:
-        return _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_iterations,
-                           group_particles, pair_chunk, comm)
+        res = _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_iterations,
+                          group_particles, pair_chunk, comm)
+    if caller is not None and caller.cuda_stream != stream.cuda_stream:
+        # the results were produced on the library's stream: order the caller's
+        # stream after it, and keep their memory from being reused too early
+        caller.wait_stream(stream)
+        for t in (res.gid, res.h, res.rho, res.bound):
+            if t is not None and t.is_cuda:
+                t.record_stream(caller)
+    return res
 
 
 class ThreadComm:
@@ -650,6 +659,7 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     mark("redistribute")
     okeys, o2 = torch.sort(compute.row_keys(recv), stable=True)
     owned = compute.gather_rows(recv, o2)
+
     n_own = owned.shape[0]
     mark("sort owned")
 
