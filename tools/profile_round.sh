@@ -1,5 +1,5 @@
 # Round profile capture on one GPU (run under gpurun): bench line, reference arm,
-# ncu launch list, one full-set capture of the dominant kernel.
+# ncu launch list, full-set captures of the two k_target launches (seeds, main).
 # usage: bash tools/profile_round.sh TAG [CONFIG]
 set -u
 TAG=${1:-rXX}; CFG=${2:-2}
@@ -10,3 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
   python bench.py --config $CFG --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_list.log 2>&1; echo list_rc=$?
 ncu --set full --import-source on --clock-control none -k regex:k_target -c 1 -o gpurun_out/${TAG}_k_target_c${CFG} \
   python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_full.log 2>&1; echo full_rc=$?
+ncu --set full --import-source on --clock-control none -k regex:k_target --launch-skip 1 --launch-count 1 \
+  -o gpurun_out/${TAG}_k_target_main_c${CFG} \
+  python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_main.log 2>&1; echo main_rc=$?
