@@ -7,6 +7,8 @@ distance, a pure function of positions); density within rel 1e-12 on the
 fp64 path (only the summation order differs from the reference) and within
 rel 1e-4 on the fp32 path (the stated fp32 tolerance; measured ~1e-6).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -286,3 +288,17 @@ def test_uniform_box_generated_on_device_bit_exact():
     assert array_digest(h.cpu().numpy()) == str(g["h_digest"])
     idx = g["sample_idx"]
     assert _rel(rho.cpu().numpy()[idx], g["sample_rho"]) <= RTOL_F64
+
+
+def test_snapshot_streamed_to_device_matches_reference():
+    # a reference-written SPHK workload (tests/golden/make_snapshot_golden.py)
+    # streamed into device memory and run there: the reference's own h
+    # (bit-exact), density and todo trace
+    from paper_1612_06090_b200 import snapshot as S
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "snap_uniform3000_k32.sphk")
+    g = np.load(path.replace(".sphk", ".npz"))
+    h, rho, flags, st = S.density_pass_snapshot(path)
+    assert np.array_equal(h, g["h"])
+    assert _rel(rho, g["rho"]) <= RTOL_F64
+    assert np.array_equal(st.todo_sizes, g["todo"])
+    assert not flags.any()
