@@ -326,10 +326,13 @@ def run_ours(args):
     achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
     peak = peak_ffma / 1e12
     traffic = None
+    issue = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{dom}_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic = pj.get(f"{dom}_bytes_per_launch")
+            issue = {"issue_slots_busy": pj.get("issue_slots_busy"), "note": pj.get("issue_note")}
         except Exception:
             traffic = None
 
@@ -345,7 +348,9 @@ def run_ours(args):
                          "traffic": traffic,
                          "peak_source": "measured FFMA issue rate on this B200 (sph_fp32_peak); MEASURED_PEAKS.json "
                                         "has no FP32 vector figure",
-                         "ops_model": "6 per pair test, +10 per accepted pair (density)"},
+                         "ops_model": "6 per pair test, +10 per accepted pair (density)",
+                         "traffic_unit": "DRAM bytes (read + write) of the k_target launches of one pass, ncu",
+                         "issue_bound": issue},
             "search_efficiency": n * k / (search_tests / args.steps) if search_tests else None,
             "pair_tests_per_step": tests / args.steps,
             "kernel_ms_per_step": {kk: v / args.steps for kk, v in kern.items()},
