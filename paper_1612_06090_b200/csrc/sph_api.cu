@@ -739,6 +739,11 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         }
       }
     }
+    if (!a.list && n_targets < n && ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
+      // ghosts in the set: walk the compacted targets (seeded above), not every position
+      a.list = ctx->tlist.p;
+      a.list_count = ctx->qints.p + 28;
+    }
     launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
     a.list = nullptr;  // the bundle pass's leftover list is for this launch only
     a.list_count = nullptr;

@@ -94,8 +94,10 @@ def main():
                 e.record()
             e.synchronize()
             ms.append(s.elapsed_time(e))
+        tk = c.last_stats["t_kernel_ms"]
         per_rank.append({"owned": out[r].n_owned, "ghosts": out[r].n_ghosts, "max_bound": out[r].max_bound,
-                         "final_pass_ms": min(ms)})
+                         "final_pass_ms": min(ms), "tree_ms": tk["tree"], "search_ms": tk["search"],
+                         "pair_tests": c.last_stats["pair_tests"]})
     # how tight are the bounds?  bound / h over all owned particles, and the
     # ghosts rank 0 would send with margins = the true h (the ideal)
     ratio = np.concatenate([(o.bound / o.h).cpu().numpy() for o in out])
