@@ -196,8 +196,10 @@ def run_reference(args):
     n, k = w["pos"].shape[0], int(w["k"])
     vals = []
     base = None
+    # each step a bounded sample; the whole run stays within ~2 minutes
+    per_step = max(0.5, min(args.cpu_seconds / 2, 120.0 / max(1, args.warmup + args.steps)))
     for step in range(args.warmup + args.steps):
-        base = cpu_sampled(w, target_seconds=args.cpu_seconds / 2, seed=step)
+        base = cpu_sampled(w, target_seconds=per_step, seed=step)
         if step >= args.warmup:
             vals.append(base["value"])
     value = statistics.median(vals)
