@@ -302,3 +302,29 @@ def test_snapshot_streamed_to_device_matches_reference():
     assert _rel(rho, g["rho"]) <= RTOL_F64
     assert np.array_equal(st.todo_sizes, g["todo"])
     assert not flags.any()
+
+
+def test_bench_json_contract():
+    # the driver's contract for our arm: one JSON line with value / e2e /
+    # roofline / cpu_baseline / clocks / gpu_launches
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "6", "--steps", "3", "--warmup", "3",
+                        "--cpu-seconds", "1"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "clocks", "roofline", "cpu_baseline"):
+        assert key in line, key
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["n_gpus"] == 1 and line["value"] > 0
+    assert line["gpu_launches"] > 0
+    e = line["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    rf = line["roofline"]
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in rf, key
+    assert 0 < rf["frac"] < 1
+    assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
+    assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]

@@ -147,3 +147,23 @@ def test_nfw_generator_shape_and_rules():
     assert np.array_equal(pos.astype(np.float32).astype(np.float64), pos)  # fp32-representable
     w = workload.config(1)
     assert w["pos"].shape == (32768, 3) and w["h0"][0] == 2.0 * 32768 ** (-1.0 / 3.0)
+
+
+def test_bench_reference_arm_json_contract():
+    # bench.py --impl reference (the CPU port of the reference pass) prints one
+    # JSON line with the driver's keys; tiny sample so it runs in seconds
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                        "--steps", "1", "--warmup", "0", "--cpu-seconds", "1"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert "workload" in line["config"]
