@@ -98,21 +98,9 @@ def main():
         per_rank.append({"owned": out[r].n_owned, "ghosts": out[r].n_ghosts, "max_bound": out[r].max_bound,
                          "final_pass_ms": min(ms), "tree_ms": tk["tree"], "search_ms": tk["search"],
                          "pair_tests": c.last_stats["pair_tests"]})
-    # how tight are the bounds?  bound / h over all owned particles, and the
-    # ghosts rank 0 would send with margins = the true h (the ideal)
+    # how tight are the bounds?  bound / h over all owned particles
     ratio = np.concatenate([(o.bound / o.h).cpu().numpy() for o in out])
     qs = np.quantile(ratio, [0.5, 0.9, 0.99, 0.999, 1.0]).tolist()
-    c0 = comps[0]
-    gd, gst, gct, rows, fd, fr, per, bx = c0.last_ghost_inputs
-    # rank 0's own groups with margins from its true h would need the peers' h: report the
-    # peers' bound tightness instead, and the ghost count rank 0 sends when every
-    # foreign margin shrinks by the median bound / h
-    fd2 = fd.clone()
-    fd2[:, 6] = fd2[:, 6] / qs[0]
-    ideal = c0.ghost_mask(gd, gst, gct, rows, fd2, fr, per, bx)
-    ideal_sent = int(sum(int(((ideal >> q) & 1).sum()) for q in range(world)))
-    real = c0.ghost_mask(*c0.last_ghost_inputs)
-    real_sent = int(sum(int(((real >> q) & 1).sum()) for q in range(world)))
     # rank 0's ghost marking alone
     c = comps[0]
     gm = []
@@ -126,7 +114,6 @@ def main():
         e.synchronize()
         gm.append(s.elapsed_time(e))
     res = {"config": args.config, "ghost_mask_ms_rank0": min(gm), "bound_over_h_quantiles_50_90_99_999_max": qs,
-           "rank0_ghosts_sent": real_sent, "rank0_ghosts_sent_margins_over_median_ratio": ideal_sent,
            "n_groups_rank0": int(c.last_ghost_inputs[0].shape[0]), "n_foreign_rank0": int(c.last_ghost_inputs[4].shape[0]), "world": world, "n": n, "h_mismatches": h_mis, "rho_max_rel": rho_rel,
            "single_gpu_pass_ms": t_single, "per_rank": per_rank,
            "final_pass_ms_max": max(p["final_pass_ms"] for p in per_rank),
