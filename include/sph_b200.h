@@ -176,6 +176,16 @@ int sph_neighbor_counts(sph_ctx *ctx, int32_t precision, int32_t periodic, doubl
                         int64_t n, const void *x, const void *y, const void *z,
                         const double *h, int32_t *counts_out, sph_stats *stats);
 
+/* The reference's range_query(tree, pos_i, h_i, exclude=i) (octree.py:179-227,
+ * 351-379) for every particle i at once, open boundary: the other particles
+ * with (dx*dx + dy*dy) + dz*dz <= h_i*h_i in unfused fp64, as CSR in the
+ * caller's particle order.  offsets (n + 1, host) = the exclusive prefix sum
+ * of sph_neighbor_counts for the same h; idx_out / d2_out (offsets[n] each,
+ * host) receive each list sorted by index (the reference lists candidates in
+ * tree order: the same sets).  SPH_INVALID if the offsets do not match. */
+int sph_range_query(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
+                    const double *h, const int64_t *offsets, int64_t *idx_out, double *d2_out);
+
 /* measured FP32-pipe FFMA issue rate of the context's device (FFMA/s): the
  * roofline denominator of the neighbour kernels */
 double sph_fp32_peak(sph_ctx *ctx);

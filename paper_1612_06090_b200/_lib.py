@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "sph_neighbor_counts", "sph_fnv1a64", "sph_ctx_stream", "sph_fp32_peak", "sph_uniform_box_device",
     "sph_morton_keys_device", "sph_decomp_pack_rows_device", "sph_decomp_gather_rows_device",
     "sph_decomp_row_keys_device", "sph_decomp_level_bounds_device", "sph_decomp_window_bounds_device",
-    "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device", "sph_bbox_device",
+    "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device", "sph_bbox_device", "sph_range_query",
 )
 
 
@@ -112,6 +112,7 @@ def load():
         L.sph_decomp_level_bounds_device.argtypes = [vp, i64, i32, vp, ctypes.c_double, vp]
         L.sph_decomp_window_bounds_device.argtypes = [vp, i64, i32, i32, vp, ctypes.c_double, vp]
         L.sph_bbox_device.argtypes = [vp, i32, i64, vp, vp, vp, vp]
+        L.sph_range_query.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]
         L.sph_decomp_ghost_mask_device.argtypes = [vp, i64, vp, vp, vp, i32, vp, i64, vp, vp, i32, ctypes.c_double,
                                                    vp]
         L.sph_decomp_group_boxes_device.argtypes = [vp, i64, vp, vp, i32, vp, vp, vp]

@@ -1251,6 +1251,84 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   return rc;
 }
 
+int sph_range_query(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
+                    const double *h, const int64_t *offsets, int64_t *idx_out, double *d2_out) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 1) return fail(ctx, SPH_INVALID, "need at least one particle");
+  if (n >= (1ll << 31) - 64) return fail(ctx, SPH_INVALID, "n must be < 2^31 per device");
+  if (precision < 0 || precision > 2) return fail(ctx, SPH_INVALID, "unknown precision");
+  if (!offsets || offsets[0] != 0) return fail(ctx, SPH_INVALID, "offsets must start at 0 (n + 1 entries)");
+  const int64_t total = offsets[n];
+  for (int64_t i = 0; i < n; ++i)
+    if (offsets[i + 1] < offsets[i]) return fail(ctx, SPH_INVALID, "offsets must be non-decreasing");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = ensure_common(ctx, n, 1);
+  if (rc) return rc;
+  const size_t es = elem_size(precision);
+  SPH_CK(ctx->in_x.ensure(n));
+  SPH_CK(ctx->in_y.ensure(n));
+  SPH_CK(ctx->in_z.ensure(n));
+  SPH_CK(ctx->in_m.ensure(n));
+  SPH_CK(ctx->io_h.ensure(n));
+  SPH_CK(ctx->hfix.ensure(n));
+  cudaStream_t s = ctx->stream;
+  SPH_CK(cudaMemcpyAsync(ctx->in_x.p, x, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_y.p, y, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_z.p, z, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->io_h.p, h, 8 * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemsetAsync(ctx->in_m.p, 0, 8 * n, s));
+  int launches = 0;
+  RootInfo root{};
+  rc = stage_root(ctx, (int)n, precision, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, &root, &launches);
+  if (rc) return rc;
+  const int compute_f32 = precision == SPH_PRECISION_F32 || (precision == 2 && !root.not_f32);
+  const float rmax = compute_rmax(root, 0, 0.0);
+  int n_nodes = 0;
+  rc = stage_tree(ctx, (int)n, precision, compute_f32, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, 1, rmax,
+                  &n_nodes, &launches, true);
+  if (rc) return rc;
+  sph_params prm{};
+  PassArgs a = base_args(ctx, (int)n, 1, n_nodes, &prm, rmax);
+  rc = prepare_target_tree(ctx, (int)n, n_nodes, a);
+  if (rc) return rc;
+  k_gather_sorted<double><<<nblk(n), kTB, 0, s>>>((int)n, ctx->perm.p, ctx->io_h.p, ctx->hfix.p);
+  struct Tmp {  // per-call workspace, freed on every return path
+    DevBuf<int64_t> d_off, idx_a, idx_b;
+    DevBuf<double> d2_a, d2_b;
+    DevBuf<unsigned char> temp;
+    DevBuf<int> err;
+    ~Tmp() { d_off.release(); idx_a.release(); idx_b.release(); d2_a.release(); d2_b.release(); temp.release(); err.release(); }
+  } tmp;
+  auto &d_off = tmp.d_off, &idx_a = tmp.idx_a, &idx_b = tmp.idx_b;
+  auto &d2_a = tmp.d2_a, &d2_b = tmp.d2_b;
+  auto &temp = tmp.temp;
+  auto &err = tmp.err;
+  const size_t tneed = range_sort_temp((int)n, total);
+  SPH_CK(d_off.ensure(n + 1));
+  SPH_CK(idx_a.ensure(total + 1));
+  SPH_CK(idx_b.ensure(total + 1));
+  SPH_CK(d2_a.ensure(total + 1));
+  SPH_CK(d2_b.ensure(total + 1));
+  SPH_CK(temp.ensure(tneed + 1));
+  SPH_CK(err.ensure(1));
+  SPH_CK(cudaMemcpyAsync(d_off.p, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+  if (range_fill(s, compute_f32, (int)n, ctx->perm.p, ctx->pos_sorted.p, ctx->hfix.p, a.tree, d_off.p, total,
+                 idx_b.p, d2_b.p, err.p, temp.p, tneed + 1, idx_a.p, d2_a.p, ctx->num_sms) != 0)
+    return fail(ctx, SPH_CUDA_ERROR, "range query: sort workspace too small");
+  int herr = 0;
+  SPH_CK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (total > 0) {
+    SPH_CK(cudaMemcpyAsync(idx_out, idx_b.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, s));
+    SPH_CK(cudaMemcpyAsync(d2_out, d2_b.p, sizeof(double) * total, cudaMemcpyDeviceToHost, s));
+  }
+  SPH_CK(cudaStreamSynchronize(s));
+  SPH_CK(cudaGetLastError());
+  if (herr) return fail(ctx, SPH_INVALID, "range query: the offsets do not match the fixed-h neighbour counts");
+  return SPH_OK;
+}
+
 int sph_morton_keys_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y,
                            const void *d_z, const double *centre, double half, uint64_t *d_keys) {
   if (!ctx) return SPH_INVALID;

@@ -192,6 +192,11 @@ void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const v
                  const void *z, unsigned long long *ord, RootInfo *root, int *launches);
 
 size_t cub_temp_needed(int n);
+// batched range query lists (sph_range.cu)
+int range_fill(cudaStream_t s, int f32, int n, const uint32_t *perm, const void *pos_sorted, const double *h_sorted,
+               const TreeView &tree, const int64_t *offsets, int64_t total, int64_t *idx_out, double *d2_out,
+               int *err, void *temp, size_t temp_bytes, int64_t *idx_tmp, double *d2_tmp, int num_sms);
+size_t range_sort_temp(int n, int64_t total);
 // domain decomposition helpers (sph_decomp.cu)
 void launch_pack_rows(cudaStream_t s, int64_t n, int precision_in, const int64_t *order, const void *x,
                       const void *y, const void *z, const double *m, const double *h0, const int64_t *gid,

@@ -76,3 +76,28 @@ def neighbor_counts(positions, h, periodic: bool = False, box: float = 0.0, devi
         msg = _lib.last_error(ctx)
         raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(msg)
     return (out, st.as_dict()) if return_stats else out
+
+
+def range_query_all(positions, h, device: int = 0):
+    """``range_query(tree, pos_i, h_i, exclude=i)`` (octree.py:351-379) for
+    every particle i at once, open boundary: CSR (offsets int64[n+1], idx
+    int64[total], d2 float64[total]); each list sorted by index (the
+    reference lists the same set in tree order)."""
+    x, y, z = _xyz(positions)
+    n = x.shape[0]
+    hh = np.ascontiguousarray(np.broadcast_to(np.asarray(h, dtype=np.float64), (n,)))
+    if n == 0:
+        return np.zeros(1, dtype=np.int64), np.zeros(0, dtype=np.int64), np.zeros(0)
+    counts = neighbor_counts((x, y, z), hh, device=device)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    idx = np.empty(int(offsets[-1]), dtype=np.int64)
+    d2 = np.empty(int(offsets[-1]), dtype=np.float64)
+    ctx = _lib.context(device)
+    prec = _lib.PRECISION["f32" if x.dtype == np.float32 else "auto"]
+    rc = _lib.load().sph_range_query(ctx, prec, n, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), _lib.ptr(hh),
+                                     _lib.ptr(offsets), _lib.ptr(idx), _lib.ptr(d2))
+    if rc != _lib.SPH_OK:
+        msg = _lib.last_error(ctx)
+        raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(msg)
+    return offsets, idx, d2

@@ -328,3 +328,27 @@ def test_bench_json_contract():
     assert 0 < rf["frac"] < 1
     assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
     assert "sm_mhz" in line["clocks"] and "reasons" in line["clocks"]
+
+
+def test_range_query_lists_match_brute_force():
+    # range_query(tree, pos_i, h_i, exclude=i) for every particle: the sets and
+    # unfused fp64 distances of a brute-force all-pairs check, fp64 and fp32 inputs
+    from paper_1612_06090_b200.octree import range_query_all
+    rng = np.random.default_rng(12)
+    n = 3000
+    pos = np.concatenate([rng.normal(0.5, 0.05, (n // 2, 3)), rng.random((n - n // 2, 3))])
+    h = rng.random(n) * 0.08 + 0.01
+    for arr in (pos, pos.astype(np.float32)):
+        p64 = arr.astype(np.float64)
+        off, idx, d2 = range_query_all(arr, h)
+        dx = p64[None, :, 0] - p64[:, None, 0]
+        dy = p64[None, :, 1] - p64[:, None, 1]
+        dz = p64[None, :, 2] - p64[:, None, 2]
+        dd = (dx * dx + dy * dy) + dz * dz
+        ok = dd <= (h * h)[:, None]
+        np.fill_diagonal(ok, False)
+        for i in range(0, n, 7):
+            want = np.nonzero(ok[i])[0]
+            got = idx[off[i]:off[i + 1]]
+            assert np.array_equal(got, want), i
+            assert np.array_equal(d2[off[i]:off[i + 1]], dd[i, want]), i
