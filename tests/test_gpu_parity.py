@@ -352,3 +352,33 @@ def test_range_query_lists_match_brute_force():
             got = idx[off[i]:off[i + 1]]
             assert np.array_equal(got, want), i
             assert np.array_equal(d2[off[i]:off[i + 1]], dd[i, want]), i
+
+
+@pytest.mark.parametrize("k", [1, 2, 200, 512])
+def test_extreme_k_against_oracle(k):
+    # very small and very large K (list capacities, collect / walking fallbacks)
+    rng = np.random.default_rng(100 + k)
+    n = 12000
+    pos = np.concatenate([rng.normal(5.0, 0.3, (n // 2, 3)), rng.random((n - n // 2, 3)) * 10.0]).astype(np.float32)
+    p64 = pos.astype(np.float64)
+    mass = rng.random(n) + 0.5
+    h0 = np.full(n, sph.initial_smoothing_length(10.0, n, k))
+    want = oracle.density_pass(p64[:, 0], p64[:, 1], p64[:, 2], mass, h0, k)
+    h, rho, flags, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k)
+    assert np.array_equal(h, want.h)
+    assert _rel(rho, want.rho) <= RTOL_F32
+    assert np.array_equal(st.todo_sizes, want.todo_sizes)
+
+
+@pytest.mark.parametrize("k,f32", [(256, True), (256, False), (3, True)])
+def test_extreme_k_periodic_against_oracle(k, f32):
+    n, box = 10000, 10.0
+    pos, _, _ = workload.nfw_halos(n, box, 12, seed=40 + k)
+    arr = pos.astype(np.float32) if f32 else pos
+    p64 = arr.astype(np.float64)
+    h0 = np.full(n, sph.initial_smoothing_length(box, n, k))
+    want = oracle.density_pass_periodic(p64[:, 0], p64[:, 1], p64[:, 2], np.ones(n), h0, k, box)
+    h, rho, _, st = sph.density_pass_soa(arr[:, 0], arr[:, 1], arr[:, 2], np.ones(n), h0, k, periodic=True, box=box)
+    assert np.array_equal(h, want.h)
+    assert _rel(rho, want.rho) <= (RTOL_F32 if f32 else RTOL_F64)
+    assert np.array_equal(st.todo_sizes, want.todo_sizes)
