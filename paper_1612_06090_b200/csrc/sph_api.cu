@@ -100,7 +100,7 @@ struct sph_ctx {
   cudaEvent_t ev_side_start = nullptr, ev_mass = nullptr, ev_h = nullptr;
   cudaEvent_t in_mass_ready = nullptr, in_h_ready = nullptr;  // set only during a host-API pass
   int cell_lists = 192;  // SPH_CLIST: neighbour-cell list capacity (0 = off)
-  DevBuf<float4> clist;
+  DevBuf<unsigned> clist;
   DevBuf<int> clen, cellidx, cellnode;
   DevBuf<float> crad2;
   DevBuf<int> cnear;
@@ -721,7 +721,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         // neighbour-cell lists for the radii the seeds imply
         const int cap = ctx->cell_lists;
         const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
-        if (ncell >= 0 && ctx->clist.ensure(2 * (size_t)ncell * cap) == cudaSuccess &&
+        if (ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
             ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
             ctx->cnear.ensure(ncell) == cudaSuccess) {
           launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,

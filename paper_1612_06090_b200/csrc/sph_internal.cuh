@@ -141,7 +141,7 @@ struct PassArgs {
   int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
   int static_sched;         // per-target kernel: strided static assignment instead of the atomic counter
   int tchunk;               // per-target kernel: consecutive targets per work grab (identity target order)
-  const float4 *clist;      // per-target kernel: neighbour-cell lists (child records) per cell, clcap each
+  const unsigned *clist;    // per-target kernel: neighbour-cell lists per cell (child-record indices into tree.crec), clcap each
   const int *clen;          // list length per cell (-1: none)
   const float *crad2;       // squared radius a cell's list covers
   const int *cellidx;       // cell index of each node (-1: internal)
@@ -231,7 +231,7 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes_dev, int max_nodes, int *cellidx,
                            int *cellnode, int *ncells);
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
-                       float4 *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
+                       unsigned *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
                        int num_sms);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof);

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           if (lbase >= 0) {  // 32 listed cells per step
             if (li + lane < llen) {
               const int e = li + lane;
-              rec = a.clist + 2 * ((size_t)lbase + (e < lnear ? e : e + lfar_off));
+              rec = a.tree.crec + 2 * (size_t)a.clist[(size_t)lbase + (e < lnear ? e : e + lfar_off)];
             }
             li += 32;
           } else {
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
                                                     const int *__restrict__ ncells, const uint8_t *__restrict__ state,
                                                     const float *__restrict__ r0, const int4 *__restrict__ anc4,
                                                     int n_nodes, int n, int root_start, int cap,
-                                                    float4 *__restrict__ clist, int *__restrict__ clen,
+                                                    unsigned *__restrict__ clist, int *__restrict__ clen,
                                                     float *__restrict__ crad2, int *__restrict__ cnear,
                                                     float near_frac, float d_pct) {
   __shared__ int s_stk[4][kStack];
@@ -920,10 +920,10 @@ __global__ void __launch_bounds__(128) k_cell_lists(const float4 *__restrict__ n
       const unsigned fm = __ballot_sync(FULL, hit && is_cell && far);
       if (len + __popc(cm) + __popc(fm) > cap) { over = true; break; }
       if (hit && is_cell) {
+        // the list holds the child-record index (parent * 8 + slot): 4 bytes
+        // per entry instead of the 32-byte record, so lists and records stay in L2
         const int slot = far ? cap - 1 - (nfar + __popc(fm & lt)) : nnear + __popc(cm & lt);
-        float4 *dst = clist + 2 * ((size_t)ci * cap + slot);
-        dst[0] = l4;
-        dst[1] = h4;
+        clist[(size_t)ci * cap + slot] = (unsigned)par * 8u + (unsigned)(lane & 7);
       }
       nnear += __popc(cm);
       nfar += __popc(fm);
@@ -978,7 +978,7 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 }
 
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
-                       float4 *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
+                       unsigned *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
                        int num_sms) {
   k_cell_lists<<<num_sms * 8, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
                                            a.tree.anc4, a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen,
