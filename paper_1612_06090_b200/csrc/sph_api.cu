@@ -106,7 +106,7 @@ struct sph_ctx {
   DevBuf<int> cnear;
   float near_frac = 0.5f;   // SPH_NEARF: cell-list records beyond near_frac * D go to the list's back
   float d_pct = 1.0f;       // SPH_DPCT: cell-list radius D = this quantile of the cell's target radii
-  int tshrink = 2;       // SPH_TSHRINK
+  int tshrink = 1;       // SPH_TSHRINK (shrink after every K >> tshrink new candidates; 1 measured best on C2/C5)
   int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
   int tchunk = 1;        // SPH_TCHUNK: consecutive targets per work grab of the per-target kernel (2-16 measured slower on C2)
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
