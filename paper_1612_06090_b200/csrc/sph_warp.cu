@@ -997,8 +997,9 @@ void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nod
 }
 
 int target_list_cap(int k) {
-  static const int mult = getenv("SPH_TLISTCAP") ? atoi(getenv("SPH_TLISTCAP")) : 3;
-  return std::min(std::max(mult * k, 128), 1024);
+  // per-target list entries (measured best: 4K = 256 at K = 64 on C2, 3K = 384 at K = 128 on C5)
+  static const int mult = getenv("SPH_TLISTCAP") ? atoi(getenv("SPH_TLISTCAP")) : 0;
+  return std::min(std::max((mult > 0 ? mult : k <= 64 ? 4 : 3) * k, 128), 1024);
 }
 
 template <bool F32, bool COLLECT>
