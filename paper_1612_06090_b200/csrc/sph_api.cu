@@ -725,7 +725,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
             ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
             ctx->cnear.ensure(ncell) == cudaSuccess) {
           launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
-                            ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms);
+                            ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms, ncell);
           a.cnear = ctx->cnear.p;
           a.near_frac2 = ctx->near_frac * ctx->near_frac;
           a.clist = ctx->clist.p;

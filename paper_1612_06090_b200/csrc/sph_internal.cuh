@@ -232,7 +232,7 @@ void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes
                            int *cellnode, int *ncells);
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
                        unsigned *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
-                       int num_sms);
+                       int num_sms, int ncell_host = -1);
 void launch_kids(cudaStream_t s, const float4 *nlo, const float4 *nhi, int n_nodes, int n, float4 *crec, int *parent,
                  int4 *anc4, int *cellof);
 // per-cell initial search radius from the node sizes and the parent chain

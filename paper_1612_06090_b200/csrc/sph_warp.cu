@@ -979,8 +979,11 @@ void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cell
 
 void launch_cell_lists(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int cap,
                        unsigned *clist, int *clen, float *crad2, int *cnear, float near_frac, float d_pct,
-                       int num_sms) {
-  k_cell_lists<<<num_sms * 8, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
+                       int num_sms, int ncell_host) {
+  // one warp per cell: each list is one latency-bound walk, so as many
+  // walks in flight as the cells (more blocks than resident slots balance too)
+  const int blocks = ncell_host > 0 ? (ncell_host + 3) / 4 : num_sms * 16;
+  k_cell_lists<<<blocks, 128, 0, s>>>(a.tree.nlo, a.tree.nhi, a.tree.crec, cellnode, ncells, a.state, a.radius,
                                            a.tree.anc4, a.tree.n_nodes, a.n, a.tree.root_start, cap, clist, clen,
                                            crad2, cnear, near_frac, d_pct);
 }
