@@ -616,13 +616,23 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   SPH_CK(ctx->rho_s.ensure(n));
   tm.mark(1);
   RootInfo root{};
-  int rc = stage_root(ctx, n, prm->precision, x, y, z, &root, &launches);
-  if (rc) return rc;
-  if (prm->periodic) {
-    if (!(prm->box > 0.0)) return fail(ctx, SPH_INVALID, "periodic box side must be > 0");
-    for (int a2 = 0; a2 < 3; ++a2)
-      if (root.lo[a2] < 0.0 || root.hi[a2] >= prm->box)
-        return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
+  int rc = SPH_OK;
+  if (prm->periodic && !(prm->box > 0.0)) return fail(ctx, SPH_INVALID, "periodic box side must be > 0");
+  // periodic with an explicit precision: nothing on the host depends on the
+  // root box (rmax is 0.999 box), so its checks are read with the results
+  // instead of costing a round trip here
+  const bool defer_root = prm->periodic && prm->precision != SPH_PRECISION_AUTO;
+  if (defer_root) {
+    launch_bbox(ctx->stream, n, prm->precision == SPH_PRECISION_F32 ? 1 : 0, x, y, z, ctx->bbox_ord.p, ctx->root.p,
+                &launches);
+  } else {
+    rc = stage_root(ctx, n, prm->precision, x, y, z, &root, &launches);
+    if (rc) return rc;
+    if (prm->periodic) {
+      for (int a2 = 0; a2 < 3; ++a2)
+        if (root.lo[a2] < 0.0 || root.hi[a2] >= prm->box)
+          return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
+    }
   }
   const int compute_f32 = prm->precision == SPH_PRECISION_F32 || (prm->precision == 2 && !root.not_f32);
   const float rmax = compute_rmax(root, prm->periodic, prm->box);
@@ -920,6 +930,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     int qd[32];
     SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
     SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
+    if (defer_root) SPH_CK(cudaMemcpyAsync(&root, ctx->root.p, sizeof(RootInfo), cudaMemcpyDeviceToHost, ctx->stream));
     if (warp_deferred) SPH_CK(cudaMemcpyAsync(qd, ctx->qints.p, sizeof(qd), cudaMemcpyDeviceToHost, ctx->stream));
     SPH_CK(cudaStreamSynchronize(ctx->stream));
     SPH_CK(cudaGetLastError());
@@ -946,6 +957,12 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     ++launches;
   }
   collect_kernel_times(ctx, st);
+  if (defer_root) {  // the checks stage_root would have made, on the root read with the results
+    if (root.nonfinite) return fail(ctx, SPH_INVALID, "positions must be finite");
+    for (int a2 = 0; a2 < 3; ++a2)
+      if (root.lo[a2] < 0.0 || root.hi[a2] >= prm->box)
+        return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
+  }
   if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
 
   // ---- stats, reference todo trace, error mapping ----

@@ -382,3 +382,24 @@ def test_extreme_k_periodic_against_oracle(k, f32):
     assert np.array_equal(h, want.h)
     assert _rel(rho, want.rho) <= (RTOL_F32 if f32 else RTOL_F64)
     assert np.array_equal(st.todo_sizes, want.todo_sizes)
+
+
+@pytest.mark.parametrize("f32", [True, False])
+def test_periodic_input_checks(f32):
+    # positions outside [0, box) or non-finite are rejected (checked with the
+    # results when the root box is not needed on the host)
+    rng = np.random.default_rng(3)
+    pos = rng.random((5000, 3)) * 10.0
+    pos = pos.astype(np.float32) if f32 else pos
+    bad = pos.copy()
+    bad[17, 1] = 10.5
+    with pytest.raises(ValueError, match="inside"):
+        sph.density_pass_soa(bad[:, 0], bad[:, 1], bad[:, 2], np.ones(5000), 0.5, 32, periodic=True, box=10.0)
+    nan = pos.copy()
+    nan[3, 0] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        sph.density_pass_soa(nan[:, 0], nan[:, 1], nan[:, 2], np.ones(5000), 0.5, 32, periodic=True, box=10.0)
+    # and the context still works afterwards
+    h, rho, _, _ = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], np.ones(5000), 0.5, 32, periodic=True,
+                                        box=10.0)
+    assert np.all(h > 0)
