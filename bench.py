@@ -84,9 +84,11 @@ def config_json(w, cfg, n_gpus, kernel):
         5: "C5: 8,388,608 particles, fp32, single NFW halo c=20 r_vir=1 + 5% background, periodic box 4, K=128",
         6: "diagnostic: 1,048,576 uniform particles, fp32, periodic box 100, K=64 (not a BASELINE config)",
     }[cfg]
-    if n_gpus > 1:
+    if n_gpus > 1 and cfg in (2, 3, 6):
         desc = (f"{desc.split(':')[0]} weak-scaled x{n_gpus}: {int(w['pos'].shape[0]):,} particles "
                 f"({n_gpus} x the 1-GPU set: same generator, {n_gpus}x halos, box side {float(w['box']):.1f})")
+    elif n_gpus > 1:
+        desc = f"{desc} (strong scaling: the one set over {n_gpus} GPUs)"
     return {"workload": desc, "config_index": cfg, "n_particles": int(w["pos"].shape[0]), "k_neighbors": int(w["k"]),
             "box": float(w["box"]), "periodic": bool(w["periodic"]), "positions": "f32" if w["fp32"] else "f64",
             "kernel": kernel,
@@ -523,8 +525,9 @@ def run_decomposed(args, world, rank, local):
         peak = float(compute.L.sph_fp32_peak(compute.ctx)) / 1e12
         ops = 6.0 * st.get("pair_tests", 0) + 10.0 * st.get("accepted_pairs", 0)
         achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
+        scaling = "weak" if args.config in (2, 3, 6) else "strong"  # workload.config_weak scales 2, 3, 6
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
                 "config": config_json(w, args.config, world, args.kernel),
                 "converged_particles_per_s": n_glob / (ms_max * 1e-3),
