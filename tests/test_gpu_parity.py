@@ -403,3 +403,53 @@ def test_periodic_input_checks(f32):
     h, rho, _, _ = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], np.ones(5000), 0.5, 32, periodic=True,
                                         box=10.0)
     assert np.all(h > 0)
+
+
+def test_sphlab_adapter_on_the_gpu():
+    # the adapter around the real GPU pass, with a stand-in for the reference
+    # package's types (the reference is not present on the GPU box)
+    import dataclasses
+    import types
+
+    from paper_1612_06090_b200 import sphlab_adapter
+
+    class CE(RuntimeError):
+        pass
+
+    class DE(RuntimeError):
+        pass
+
+    @dataclasses.dataclass
+    class PS:
+        iteration_count: int
+        todo_sizes: object
+        phase_times: dict
+        contention_time: float
+        items_per_worker: object
+        skipped_items: int = 0
+        t_total: float = 0.0
+
+    ref = types.SimpleNamespace(
+        density=types.SimpleNamespace(ConvergenceError=CE, DegenerateWorkloadError=DE, PassStats=PS,
+                                      DEFAULT_MAX_ITERATIONS=100),
+        bench=types.SimpleNamespace(compute_density_pass=None))
+    undo = sphlab_adapter.install(ref)
+    n, k = 4096, 64
+    pos = workload.uniform_box(n, 81)
+    p = sph.new_particle_array(n)
+    p["x"], p["y"], p["z"] = pos[:, 0], pos[:, 1], pos[:, 2]
+    p["mass"] = 1.0 / n
+    p["smoothing_length"] = sph.initial_smoothing_length(1.0, n, k)
+    want = oracle.density_pass(pos[:, 0], pos[:, 1], pos[:, 2], np.full(n, 1.0 / n),
+                               np.full(n, sph.initial_smoothing_length(1.0, n, k)), k)
+    rho, st = ref.bench.compute_density_pass(p, sph.preset_config("optimised", k_neighbors=k))
+    assert isinstance(st, PS) and np.array_equal(st.todo_sizes, want.todo_sizes)
+    assert np.array_equal(p["smoothing_length"], want.h) and _rel(rho, want.rho) <= RTOL_F64
+    small = sph.new_particle_array(10)
+    small["x"] = np.arange(10.0)
+    small["mass"] = 1.0
+    small["smoothing_length"] = 0.5
+    with pytest.raises(CE):
+        ref.bench.compute_density_pass(small, sph.preset_config("optimised", k_neighbors=32))
+    undo()
+    assert ref.bench.compute_density_pass is None
