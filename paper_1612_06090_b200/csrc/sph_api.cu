@@ -108,6 +108,7 @@ struct sph_ctx {
   float d_pct = 1.0f;       // SPH_DPCT: cell-list radius D = this quantile of the cell's target radii
   int tshrink = 1;       // SPH_TSHRINK (shrink after every K >> tshrink new candidates; 1 measured best on C2/C5)
   int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
+  int lists_early = 0;   // SPH_CLEARLY: 1 = cell lists for the seeds too (rebuilt after), 2 = one build before the seeds
   int tchunk = 1;        // SPH_TCHUNK: consecutive targets per work grab of the per-target kernel (2-16 measured slower on C2)
   float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
   int last_list_fallbacks = 0;
@@ -664,6 +665,30 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ctx->kev_mode[i] = MODE_HIST;
       cudaEventRecord(ctx->kev[2 * i], ctx->stream);
     }
+    // neighbour-cell lists for the radii currently in r0 (k_cell_lists); sets
+    // the list fields of dst, false when they could not be allocated
+    auto build_lists = [&](PassArgs &dst) -> bool {
+      const int cap = ctx->cell_lists;
+      const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
+      if (cap <= 0 || ncell < 0 || ctx->clist.ensure((size_t)ncell * cap) != cudaSuccess ||
+          ctx->clen.ensure(ncell) != cudaSuccess || ctx->crad2.ensure(ncell) != cudaSuccess ||
+          ctx->cnear.ensure(ncell) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
+                        ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms, ncell);
+      dst.cnear = ctx->cnear.p;
+      dst.near_frac2 = ctx->near_frac * ctx->near_frac;
+      dst.clist = ctx->clist.p;
+      dst.clen = ctx->clen.p;
+      dst.crad2 = ctx->crad2.p;
+      dst.cellidx = ctx->cellidx.p;
+      dst.clcap = cap;
+      launches += 1;  // (the cell index is counted by stage_tree)
+      return true;
+    };
+    bool lists_built = false;
     if (ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
       // seeds first (every seed_stride-th sorted position), then every other
       // target starts from its neighbouring seeds' converged h (sorted
@@ -673,6 +698,20 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       PassArgs sa = a;
       sa.list = ctx->seeds.p;
       sa.list_count = ctx->qints.p + 14;
+      if (ctx->lists_early > 0 && ctx->cell_lists > 0) {
+        // lists for the tree's radii, walked by the seeds too (and, with
+        // lists_early == 2, by the other targets instead of a second build)
+        lists_built = build_lists(sa);
+        if (lists_built && ctx->lists_early == 2) {
+          a.cnear = sa.cnear;
+          a.near_frac2 = sa.near_frac2;
+          a.clist = sa.clist;
+          a.clen = sa.clen;
+          a.crad2 = sa.crad2;
+          a.cellidx = sa.cellidx;
+          a.clcap = sa.clcap;
+        }
+      }
       const int outer = ctx->seed_stride * ctx->seed_outer;
       if (ctx->seed_outer > 1 && n >= 64 * outer) {
         // a sparser seed level first: every outer-th position from the tree's
@@ -727,26 +766,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
                   bq[2], bq[3]);
         }
       }
-      if (ctx->cell_lists > 0) {
+      if (ctx->cell_lists > 0 && !(lists_built && ctx->lists_early == 2)) {
         // neighbour-cell lists for the radii the seeds imply
-        const int cap = ctx->cell_lists;
-        const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
-        if (ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
-            ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
-            ctx->cnear.ensure(ncell) == cudaSuccess) {
-          launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
-                            ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms, ncell);
-          a.cnear = ctx->cnear.p;
-          a.near_frac2 = ctx->near_frac * ctx->near_frac;
-          a.clist = ctx->clist.p;
-          a.clen = ctx->clen.p;
-          a.crad2 = ctx->crad2.p;
-          a.cellidx = ctx->cellidx.p;
-          a.clcap = cap;
-          launches += 1;  // (the cell index is counted by stage_tree)
-        } else {
-          cudaGetLastError();
-        }
+        build_lists(a);
       }
     }
     if (!a.list && n_targets < n && ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
@@ -1081,6 +1103,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
   if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);
   if (const char *v = getenv("SPH_TCHUNK")) c->tchunk = atoi(v);
+  if (const char *v = getenv("SPH_CLEARLY")) c->lists_early = atoi(v);
   if (const char *v = getenv("SPH_NEARF")) c->near_frac = (float)atof(v);
   if (const char *v = getenv("SPH_DPCT")) c->d_pct = (float)atof(v);
   if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
