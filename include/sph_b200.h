@@ -22,6 +22,16 @@
  *                                                              bench.py:48-50
  *   sph_uniform_box_device <- workload.generate(UNIFORM_BOX) positions
  *                                                              workload.py:42-84
+ *   sph_range_query       <- range_query(tree, pos_i, h_i, exclude=i) for all i
+ *                                                              octree.py:179-227, 351-379
+ *   sph_density_pass_device, sph_ctx_*, sph_last_error, sph_fp32_peak,
+ *   sph_device_count      : device-resident form of the pass, context and
+ *                           diagnostics (no reference counterpart)
+ *   sph_morton_keys_device, sph_bbox_device, sph_decomp_*_device
+ *                         : multi-GPU domain decomposition helpers
+ *                           (paper_1612_06090_b200/distributed.py); the
+ *                           reference runs in one shared-memory process
+ *                           (scheduler.py), so they replace nothing
  * Status codes map to the reference's exceptions (density.py:69-74, 375-379,
  * 353-357; ValueError for invalid arguments, density.py:297-301).
  */
