@@ -72,7 +72,7 @@ __global__ void k_level_bounds(int64_t n, int k, const int64_t *__restrict__ key
 // bin holding the K-th is an upper bound.  fp32 arithmetic, made safe by a
 // relative 1e-5 and an absolute slack (fp32 rounding of the coordinates)
 constexpr int kWinTile = 128;
-constexpr int kWinBins = 32;
+constexpr int kWinBins = 64;
 __global__ void __launch_bounds__(kWinTile) k_window_bounds(int64_t n, int k, int w, int width,
                                                             const double *__restrict__ rows, float abs_slack,
                                                             double *__restrict__ bound) {
@@ -100,31 +100,29 @@ __global__ void __launch_bounds__(kWinTile) k_window_bounds(int64_t n, int k, in
   if (e > n - 1) e = n - 1;
   const int ls = (int)(s - base), le = (int)(e - base), lp = (int)(p - base);
   const float4 q = sp4[lp];
-  float d2max = 0.f;
-  for (int j = ls; j <= le; ++j) {
-    const float4 c = sp4[j];
-    const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
-    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    if (j != lp) d2max = fmaxf(d2max, d2);
-  }
-  if (!(d2max > 0.f)) return;  // coincident window: keep the cube bound
+  // one pass: bins over [0, b0^2] with b0 the bound already known (the key
+  // cube's); candidates beyond it cannot improve the bound and are dropped
+  const double b_in = bound[p];
+  const float d2top = (float)fmin(b_in * b_in, 3.0e38);
+  if (!(d2top > 0.f)) return;
   for (int b = 0; b < kWinBins; ++b) bins[b * kWinTile] = 0;
-  const float scale = (float)kWinBins / d2max;
+  const float scale = (float)kWinBins / d2top;
   for (int j = ls; j <= le; ++j) {
     const float4 c = sp4[j];
     const float dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    if (j != lp) ++bins[min((int)(d2 * scale), kWinBins - 1) * kWinTile];
+    const int bq = (int)(d2 * scale);
+    if (j != lp && bq < kWinBins) ++bins[bq * kWinTile];
   }
-  int cum = 0, bq = kWinBins - 1;
+  int cum = 0, bq = kWinBins;
   for (int b = 0; b < kWinBins; ++b) {
     cum += bins[b * kWinTile];
     if (cum >= k) { bq = b; break; }
   }
-  if (cum < k) return;  // fewer than K others in the window
+  if (bq >= kWinBins - 1) return;  // the K-th of the window is not below the known bound
   // upper edge of the bin (a bin index may be one too low from rounding: +1 bin)
-  const double e2 = (double)min(bq + 2, kWinBins) / (double)kWinBins * (double)d2max;
-  bound[p] = fmin(bound[p], sqrt(e2) * (1.0 + 1e-5) + (double)abs_slack);
+  const double e2 = (double)(bq + 2) / (double)kWinBins * (double)d2top;
+  bound[p] = fmin(b_in, sqrt(e2) * (1.0 + 1e-5) + (double)abs_slack);
 }
 
 // per group of consecutive records: tight box of the positions and the
