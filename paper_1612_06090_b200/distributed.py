@@ -421,11 +421,12 @@ def level_bounds(keys_sorted, k: int, half: float):
     return side * (_SQRT3 * (1.0 + 1e-9))
 
 
-def window_bounds(rows, bound, k: int, bins: int = 32):
+def window_bounds(rows, bound, k: int, bins: int = 64):
     """min(bound, an upper bound of the K-th neighbour distance from the 2W
-    key-consecutive records around p, W = 3K/2): the upper edge of the
-    linear d2/d2max bin holding their K-th smallest -- torch restatement of
-    k_window_bounds (csrc/sph_decomp.cu), bit for bit."""
+    key-consecutive records around p, W = 3K/2): the d2 of those records
+    binned linearly over [0, bound^2] (records beyond dropped), the upper
+    edge of the bin holding their K-th smallest, one bin of rounding margin --
+    the algorithm of k_window_bounds (csrc/sph_decomp.cu) in fp64."""
     import torch
     n = rows.shape[0]
     if n <= k:
@@ -443,19 +444,19 @@ def window_bounds(rows, bound, k: int, bins: int = 32):
         d2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
         cols.append(torch.where(valid, d2, torch.full_like(d2, -1.0)))
     d2 = torch.stack(cols, dim=1)
-    d2max = d2.max(dim=1).values
-    ok = d2max > 0
-    safe = torch.where(ok, d2max, torch.ones_like(d2max))
-    bq = torch.clamp(((d2 / safe[:, None]) * float(bins)).to(torch.int64), max=bins - 1)
-    bq = torch.where(d2 >= 0, bq, torch.full_like(bq, bins))  # excluded slots
+    top = torch.clamp(bound * bound, max=3.0e38)
+    ok = top > 0
+    safe = torch.where(ok, top, torch.ones_like(top))
+    bq = torch.clamp((d2 / safe[:, None] * float(bins)).to(torch.int64), max=bins)
+    bq = torch.where(d2 >= 0, bq, torch.full_like(bq, bins))  # excluded slots and records beyond the bound
     counts = torch.zeros((n, bins + 1), dtype=torch.int64, device=rows.device)
     counts.scatter_add_(1, bq, torch.ones_like(bq))
     cum = torch.cumsum(counts[:, :bins], dim=1)
-    enough = cum[:, -1] >= k
-    first = torch.argmax((cum >= k).to(torch.int64), dim=1)
-    e2 = ((first + 1).to(torch.float64) / float(bins)) * d2max
+    first = torch.where(cum[:, -1] >= k, torch.argmax((cum >= k).to(torch.int64), dim=1),
+                        torch.full_like(cum[:, -1], bins))
+    e2 = ((first + 2).to(torch.float64) / float(bins)) * top
     cand = torch.sqrt(e2) * (1.0 + 1e-9)
-    use = ok & enough
+    use = ok & (first < bins - 1)
     return torch.where(use, torch.minimum(bound, cand), bound)
 
 
