@@ -335,7 +335,9 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            traffic = pj.get(f"{dom}_bytes_per_launch")
+            # measured on one config only: attached to that config's line
+            if int(pj.get("config_index", 2)) == int(args.config):
+                traffic = pj.get(f"{dom}_bytes_per_launch")
             issue = {"issue_slots_busy": pj.get("issue_slots_busy"), "note": pj.get("issue_note")}
         except Exception:
             traffic = None

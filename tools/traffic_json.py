@@ -17,10 +17,13 @@ def dram(rep):
 
 if __name__ == "__main__":
     tag = sys.argv[1]
-    seed = dram(f"gpurun_out/{tag}_k_target_c2.ncu-rep")
-    main = dram(f"gpurun_out/{tag}_k_target_main_c2.ncu-rep")
-    json.dump({"k_target_bytes_per_launch": seed + main, "seed_launch_bytes": seed, "main_launch_bytes": main,
+    cfg_ = sys.argv[2] if len(sys.argv) > 2 else "2"
+    seed = dram(f"gpurun_out/{tag}_k_target_c{cfg_}.ncu-rep")
+    main = dram(f"gpurun_out/{tag}_k_target_main_c{cfg_}.ncu-rep")
+    cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    json.dump({"config_index": cfg, "k_target_bytes_per_launch": seed + main, "seed_launch_bytes": seed,
+               "main_launch_bytes": main,
                "unit": "bytes of DRAM traffic (read + write) of the k_target launches of one pass",
-               "source": f"ncu --set full, k_target seed + main launches of config 2 ({tag})"},
+               "source": f"ncu --set full, k_target seed + main launches of config {cfg} ({tag})"},
               open("profiles/ncu_traffic.json", "w"), indent=1)
     print(seed, main)
