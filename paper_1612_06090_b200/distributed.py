@@ -630,12 +630,9 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     else:
         lo = torch.full((3,), big, dtype=f64, device=dev)
         hi = torch.full((3,), -big, dtype=f64, device=dev)
-    mm = torch.cat([-lo, hi, torch.tensor([float(n_local)], dtype=f64, device=dev)]).to(cdev)
-    nl = mm[6:].clone()
+    mm = torch.cat([-lo, hi]).to(cdev)
     dist.all_reduce(mm, op=dist.ReduceOp.MAX)
-    dist.all_reduce(nl)
-    mm = torch.cat([mm[:6], nl]).cpu().numpy()  # one host round trip
-    n_total = int(mm[6])
+    mm = mm.cpu().numpy()  # one host round trip (the particle count travels with the key samples)
     centre, half = root_cube(-mm[:3], mm[3:6])
     mark("bbox")
 
@@ -647,14 +644,18 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
         mine = sk[idx]
     else:
         mine = torch.full((samples,), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
-    gathered = [torch.empty(samples, dtype=torch.int64, device=cdev) for _ in range(world)]
+    mine = torch.cat([mine, torch.full((1,), n_local, dtype=torch.int64, device=dev)])
+    gathered = [torch.empty(samples + 1, dtype=torch.int64, device=cdev) for _ in range(world)]
     dist.all_gather(gathered, mine.to(cdev))
-    allk = torch.sort(torch.cat(gathered)).values.to(dev)
+    gk = torch.stack(gathered)
+    n_total_d = gk[:, samples].sum()
+    allk = torch.sort(gk[:, :samples].reshape(-1)).values.to(dev)
     splitters = allk[(torch.arange(1, world, device=dev) * allk.numel()) // world]
     cuts = torch.searchsorted(sk, splitters)  # rank q owns keys in [splitter[q-1], splitter[q])
     edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts,
                        torch.full((1,), n_local, dtype=torch.int64, device=dev)])
     rows = compute.pack_rows(order, x, y, z, mass.to(f64), h0.to(f64), gid.to(torch.int64), keys)
+    n_total = int(n_total_d)
     mark("keys+pack")
     recv = _exchange(dist, rows, edges[1:] - edges[:-1])
     mark("redistribute")
