@@ -85,7 +85,7 @@ struct sph_ctx {
   bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
   int list_mult = 4;
   int lshrink = 1;       // SPH_LSHRINK
-  int seed_stride = 8;   // SPH_SEED: per-target pass seeds (0/1 = off)
+  int seed_stride = 12;  // SPH_SEED: per-target pass seeds (0/1 = off; 12 beat 6/8/16 on C1-C5, r01l)
   int seed_outer = 0;    // SPH_SEED2: a sparser seed level at seed_stride x seed_outer first (0/1 = off; measured slower on C2: launch tails)
   int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
   DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel

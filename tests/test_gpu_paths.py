@@ -22,6 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CONFIGS = {
     "per_target": {},
     "per_target_small_lists": {"SPH_TLISTCAP": "1"},
+    "per_target_seed_stride_8": {"SPH_SEED": "8"},
     "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
     "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
     "bundle_after_seeds": {"SPH_BUNDLE": "1"},
