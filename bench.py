@@ -5,12 +5,14 @@
 
 A step is one full density pass (ordering + search tree + h search + exact
 K-th neighbour + density + write-back) over one synthetic particle set of
-BASELINE.json config C (default 2: 1,048,576 fp32 particles, 80% in 200 NFW
-halos + 20% uniform background, periodic box of side 100, DesNumNgb = 64).
+BASELINE.json config C (default 3, the largest clustered config that fits one
+GPU: 16,777,216 fp32 particles, 80% in 20,000 NFW halos + 20% uniform
+background, periodic box of side 252, DesNumNgb = 64).
 
 value   : useful particle-pair interactions / s = N*K / t_pass, inputs already
           resident in HBM, t_pass = CUDA-event time on the library's stream,
-          L2 flushed (256 MiB write) before every step, max over ranks.
+          L2 flushed (256 MiB write) before every step; median over the K
+          timed steps, max over ranks.
 e2e     : the same metric through the public API (density_pass_soa) with
           pinned host buffers; host->device inputs and device->host results
           inside the timed region.
@@ -20,7 +22,10 @@ roofline: the dominant kernel (by device time) against the measured FP32-pipe
 cpu_baseline: the CPU oracle (a C restatement of the reference pass, OpenMP
           on all host cores) on a bounded random target sample of the same
           workload, extrapolated: t = t_tree + t_sample * N / S.
---impl reference times that CPU implementation alone (rank 0 only).
+--impl reference times that CPU implementation alone (rank 0 only): the
+          whole pass over the whole set per step where that fits the run
+          (C1 always, C2 when the steps fit ~6 minutes), otherwise a bounded
+          target sample per step, extrapolated and labelled "extrapolated".
 Multi-GPU (torchrun, N > 1): weak scaling over ONE global set of N x the
 1-GPU config (same generator, N x the halos and volume), each rank starting
 from an interleaved slice; a step is the whole decomposed pass (key-range
@@ -56,7 +61,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time")
@@ -66,10 +71,30 @@ def parse():
     return ap.parse_args()
 
 
-def workload_config(cfg: int, seed: int | None, n_ranks: int = 1):
+def workload_config(cfg: int, seed: int | None, n_ranks: int = 1, device: int | None = None):
+    """Config ``cfg``'s inputs.  Clustered configs (2-5) are generated on the
+    GPU when ``device`` is given (workload.config_device; the host copy in
+    ``pos`` feeds e2e and the CPU baseline), else by the numpy restatement
+    of the same generator (the reference arm touches no library kernel)."""
     from paper_1612_06090_b200 import workload
     t0 = time.perf_counter()
-    w = workload.config_weak(cfg, n_ranks, seed)
+    ranks = n_ranks if cfg in (2, 3) else 1  # 4 and 5 scale strongly
+    if cfg in (2, 3, 4, 5) and device is not None:
+        w = workload.config_device(cfg, seed, device=device, n_ranks=ranks, host_positions=True)
+    elif cfg in (2, 3, 4, 5):
+        n, box, n_halos, k, conc, x_max = workload._config_table(cfg, ranks)
+        seed_ = cfg if seed is None else seed
+        if cfg == 5:
+            n_bg = int(round(0.05 * n))
+            start = np.array([0, n - n_bg], dtype=np.int64)
+            halo = np.array([[0.5 * box, 0.5 * box, 0.5 * box, 1.0, 1.0]])
+        else:
+            start, halo = workload.halo_table(n, box, n_halos, seed_)
+        pos = workload.nfw_host_restatement(n, box, start, halo, seed_, conc, x_max).astype(np.float64)
+        w = dict(pos=pos, mass=np.full(n, 1.0 / n), h0=np.full(n, workload._initial_h(box, n, k)), k=k, box=box,
+                 periodic=True, fp32=True)
+    else:
+        w = workload.config_weak(cfg, n_ranks, seed)
     w["gen_s"] = time.perf_counter() - t0
     return w
 
@@ -95,7 +120,10 @@ def config_json(w, cfg, n_gpus, kernel):
             "parallelism": (f"{n_gpus} GPUs: key-range domain decomposition, NCCL all-to-all redistribution + "
                             "ghost exchange" if n_gpus > 1 else "1 GPU"),
             "l2": "flushed before every step (256 MiB device write)",
-            "h0": "reference initial_smoothing_length rule" if cfg != 1 else "2*N^(-1/3)"}
+            "h0": "reference initial_smoothing_length rule" if cfg != 1 else "2*N^(-1/3)",
+            "generator": ("splitmix64 counter NFW generator on the device (sph_nfw_positions_device; halo table "
+                          "from the host rules)" if cfg in (2, 3, 4, 5) else
+                          "reference UniformBox stream (splitmix64)" if cfg == 1 else "numpy uniform")}
 
 
 # ---------------------------------------------------------------------------
@@ -187,7 +215,26 @@ def cpu_sampled(w, target_seconds: float, seed: int = 0):
     return {"value": n * k / t_full, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{tg.size} random targets of {n} (full tree build {t_tree:.2f}s, sample {t_sample:.2f}s), "
                       f"extrapolated to all targets: t = t_tree + t_sample*N/S = {t_full:.1f}s",
+            "extrapolated": True, "measured_s": t_tree + t_sample,
             "converged_particles_per_s": n / t_full, "cpu_count": os.cpu_count()}
+
+
+def cpu_full(w):
+    """The CPU port over the whole set (every target): one full pass."""
+    import oracle
+    pos = w["pos"]
+    n, k = pos.shape[0], int(w["k"])
+    x, y, z = pos[:, 0], pos[:, 1], pos[:, 2]
+    threads = oracle.nthreads()
+    t0 = time.perf_counter()
+    if w["periodic"]:
+        oracle.density_pass_periodic(x, y, z, w["mass"], w["h0"], k, float(w["box"]), threads=threads)
+    else:
+        oracle.density_pass(x, y, z, w["mass"], w["h0"], k, threads=threads)
+    t = time.perf_counter() - t0
+    return {"value": n * k / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"full pass over all {n} particles ({t:.2f}s)", "extrapolated": False,
+            "measured_s": t, "converged_particles_per_s": n / t, "cpu_count": os.cpu_count()}
 
 
 def run_reference(args):
@@ -196,22 +243,39 @@ def run_reference(args):
         return
     w = workload_config(args.config, args.seed, max(1, args.gpus))
     n, k = w["pos"].shape[0], int(w["k"])
-    vals = []
+    steps_total = args.warmup + args.steps
+    # full passes when the whole run fits ~6 minutes: C1 always; C2 is
+    # probed once (its full pass takes ~20 s on 16 cores)
+    full = args.config == 1
+    probe = None
+    if args.config == 2:
+        probe = cpu_full(w)
+        full = probe["measured_s"] * steps_total <= 360.0
+    vals, measured = [], []
     base = None
-    # each step a bounded sample; the whole run stays within ~2 minutes
-    per_step = max(0.5, min(args.cpu_seconds / 2, 120.0 / max(1, args.warmup + args.steps)))
-    for step in range(args.warmup + args.steps):
-        base = cpu_sampled(w, target_seconds=per_step, seed=step)
+    per_step = max(0.5, min(args.cpu_seconds / 2, 120.0 / max(1, steps_total)))
+    for step in range(steps_total):
+        if full:
+            base = probe if (probe is not None and step == 0) else cpu_full(w)
+        else:
+            base = cpu_sampled(w, target_seconds=per_step, seed=step)
         if step >= args.warmup:
             vals.append(base["value"])
+            measured.append(base["measured_s"])
     value = statistics.median(vals)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": n * k / value * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_json(w, args.config, args.gpus, "wendland_c6"), "impl": "reference",
+            "extrapolated": not full,
+            "measured_ms_per_step": statistics.median(measured) * 1e3,
             "cpu_baseline": dict(base, value=value),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "converged_particles_per_s": n / (n * k / value)}
+    if not full:
+        line["note"] = ("each step times a bounded random target sample of the full set (plus the full tree "
+                        "build); ms_per_step is the extrapolated time of a whole pass, measured_ms_per_step the "
+                        "wall time actually spent per step")
     print(json.dumps(line), flush=True)
 
 
@@ -239,14 +303,17 @@ def run_ours(args):
     device = local
     torch.cuda.set_device(device)
     seed = (args.seed if args.seed is not None else args.config) + 1000 * rank
-    w = workload_config(args.config, seed)
+    w = workload_config(args.config, seed, device=device)
     n, k = w["pos"].shape[0], int(w["k"])
     pos = w["pos"]
     f32 = bool(w["fp32"])
     pdt = torch.float32 if f32 else torch.float64
-    dx = torch.from_numpy(np.ascontiguousarray(pos[:, 0])).to(device=device, dtype=pdt)
-    dy = torch.from_numpy(np.ascontiguousarray(pos[:, 1])).to(device=device, dtype=pdt)
-    dz = torch.from_numpy(np.ascontiguousarray(pos[:, 2])).to(device=device, dtype=pdt)
+    if "x" in w:  # generated on the device
+        dx, dy, dz = w["x"], w["y"], w["z"]
+    else:
+        dx = torch.from_numpy(np.ascontiguousarray(pos[:, 0])).to(device=device, dtype=pdt)
+        dy = torch.from_numpy(np.ascontiguousarray(pos[:, 1])).to(device=device, dtype=pdt)
+        dz = torch.from_numpy(np.ascontiguousarray(pos[:, 2])).to(device=device, dtype=pdt)
     dm = torch.from_numpy(w["mass"]).to(device)
     dh0 = torch.from_numpy(w["h0"]).to(device)
     dh = dh0.clone()
@@ -311,7 +378,7 @@ def run_ours(args):
         last = d
     torch.cuda.synchronize(device)
     clk = clocks.stop()
-    ms_per_step = sum(step_ms) / len(step_ms)
+    ms_per_step = statistics.median(step_ms)
     t_local = torch.tensor([ms_per_step], dtype=torch.float64, device=device)
     n_total = torch.tensor([float(n)], dtype=torch.float64, device=device)
     if dist:
@@ -387,7 +454,7 @@ def run_ours(args):
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 e2e_ms.append(dt * 1e3)
-        e2e_local = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=device)
+        e2e_local = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=device)
         if dist:
             tdist.all_reduce(e2e_local, op=tdist.ReduceOp.MAX)
         e_ms = float(e2e_local.item())
@@ -446,7 +513,7 @@ def run_decomposed(args, world, rank, local):
         if h is not t:
             t.copy_(h)
 
-    w = workload_config(args.config, args.seed, world)
+    w = workload_config(args.config, args.seed, world, device=local)
     n_glob, k = w["pos"].shape[0], int(w["k"])
     sel = np.arange(rank, n_glob, world)
     f32 = bool(w["fp32"])
@@ -486,7 +553,7 @@ def run_decomposed(args, world, rank, local):
     tdist.barrier()
     clk = clocks.stop()
     st = compute.last_stats or {}
-    t_local = torch.tensor([sum(step_ms) / len(step_ms)], dtype=torch.float64, device=device)
+    t_local = torch.tensor([statistics.median(step_ms)], dtype=torch.float64, device=device)
     red(t_local, tdist.ReduceOp.MAX)
     ms_max = float(t_local.item())
     info = torch.tensor([r.n_owned, r.n_ghosts, r.n_owned, r.n_owned], dtype=torch.float64, device=device)
@@ -513,7 +580,7 @@ def run_decomposed(args, world, rank, local):
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 e2e_ms.append(dt * 1e3)
-        el = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=device)
+        el = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=device)
         red(el, tdist.ReduceOp.MAX)
         es = 4 if f32 else 8
         e2e = {"value": n_glob * k / (float(el.item()) * 1e-3), "unit": UNIT,

@@ -24,6 +24,9 @@
  *                                                              workload.py:42-84
  *   sph_range_query       <- range_query(tree, pos_i, h_i, exclude=i) for all i
  *                                                              octree.py:179-227, 351-379
+ *   sph_nfw_positions_device: the clustered inputs of BASELINE configs 2-5
+ *                           (the reference has no such generator; it follows
+ *                           the UniformBox counter pattern, workload.py:42-84)
  *   sph_density_pass_device, sph_ctx_*, sph_last_error, sph_fp32_peak,
  *   sph_device_count      : device-resident form of the pass, context and
  *                           diagnostics (no reference counterpart)
@@ -80,7 +83,9 @@ typedef struct {
 typedef struct {
     int32_t iterations;                 /* PassStats.iteration_count */
     int32_t n_todo;                     /* valid entries of todo_sizes */
-    int64_t todo_sizes[SPH_MAX_TODO];   /* PassStats.todo_sizes (reference growth-only trace) */
+    int64_t todo_sizes[SPH_MAX_TODO];   /* PassStats.todo_sizes (reference growth-only trace): the
+                                           first min(iterations, SPH_MAX_TODO) rounds (h grows by 2^(1/3)
+                                           per round, so round 128 is h0 * 2^42) */
     double t_stage_ms[8];               /* 0 h2d, 1 tree, 2 search, 3 select, 4 density, 5 finalize, 6 d2h, 7 total */
     int64_t pair_tests;                 /* target x candidate distance evaluations, all kernels */
     int64_t accepted_pairs;             /* pairs inside support in the density kernel */
@@ -139,7 +144,8 @@ int sph_morton_keys_device(sph_ctx *ctx, int32_t precision, int64_t n, const voi
                            const void *d_z, const double *centre, double half, uint64_t *d_keys);
 
 /* Domain-decomposition helpers (device pointers, the context's stream):
- *  pack_rows    : rows[i] = (x, y, z, m, h0, gid, key >> 32, key & 0xffffffff)
+ *  pack_rows    : rows[i] = (x, y, z, m, h0, gid bits, key >> 32, key & 0xffffffff)
+ *                 (gid as its int64 bit pattern, exact for any id)
  *                 of particle order[i], 8 doubles per record (the all-to-all payload)
  *  gather_rows  : dst row i = src row idx[i], width doubles per row
  *  row_keys     : keys of packed records (columns 6, 7) back to int64
@@ -211,6 +217,20 @@ uint64_t sph_fnv1a64(const uint8_t *data, size_t len);
  * (values at box clamp to nextafter(box, 0)).  Runs on the context's stream. */
 int sph_uniform_box_device(sph_ctx *ctx, int64_t n, uint64_t seed, double box, double *d_x, double *d_y,
                            double *d_z);
+
+/* On-device clustered generator (BASELINE configs 2-5):
+ * particles [halo_start[h], halo_start[h+1]) of halo h follow an NFW profile
+ * (concentration c, truncated at x_max = r / r_s) around its centre, the rest
+ * [halo_start[n_halos], n) are uniform in the box.  d_halo holds 5 doubles
+ * per halo: centre x, y, z, r_vir, velocity sigma.  Every draw is the
+ * splitmix64 counter stream of sph_uniform_box_device (draw 8i + j for
+ * particle i), so the set is a pure function of the seed and the halo table.
+ * Positions wrap into [0, box) and are written as fp32; d_vel (3 floats per
+ * particle, may be NULL) receives Gaussian velocities (never read by the
+ * pass).  Device pointers, the context's stream. */
+int sph_nfw_positions_device(sph_ctx *ctx, int64_t n, int64_t n_halos, const int64_t *d_halo_start,
+                             const double *d_halo, double concentration, double x_max, uint64_t seed, double box,
+                             float *d_x, float *d_y, float *d_z, float *d_vel);
 
 #ifdef __cplusplus
 }

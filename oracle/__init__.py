@@ -204,6 +204,42 @@ def periodic_images(x, y, z, box: float, margin: float):
             np.concatenate(src))
 
 
+def periodic_crop(x, y, z, box: float, targets, margin: float) -> np.ndarray:
+    """Sorted indices of every particle whose minimum-image Chebyshev distance
+    to some target is at most ``margin`` (a superset: whole grid cells of side
+    >= margin around each target's cell, wrapped).  Each target's h and rho
+    depend only on the particles within its h (reference density.py:11-13),
+    so the periodic oracle over the crop, with every target's search radius
+    below ``margin``, gives the full set's answer for the targets; the crop
+    keeps the originals' relative order, so (d2, index) ties break alike."""
+    ncell = int(box // margin)
+    if ncell < 3:
+        return np.arange(np.asarray(x).shape[0])
+    cell = box / ncell
+    tg = np.asarray(targets)
+
+    def cid(ax, ay, az):
+        ix = np.minimum((np.asarray(ax) / cell).astype(np.int64), ncell - 1)
+        iy = np.minimum((np.asarray(ay) / cell).astype(np.int64), ncell - 1)
+        iz = np.minimum((np.asarray(az) / cell).astype(np.int64), ncell - 1)
+        return ix, iy, iz
+
+    tx, ty, tz = cid(np.asarray(x)[tg], np.asarray(y)[tg], np.asarray(z)[tg])
+    need = set()
+    for dx in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                c = (((tx + dx) % ncell) * ncell + (ty + dy) % ncell) * ncell + (tz + dz) % ncell
+                need.update(c.tolist())
+    need = np.array(sorted(need), dtype=np.int64)
+    keep = np.zeros(x.shape[0], dtype=bool)
+    step = 1 << 24
+    for a in range(0, x.shape[0], step):
+        ix, iy, iz = cid(x[a:a + step], y[a:a + step], z[a:a + step])
+        keep[a:a + step] = np.isin((ix * ncell + iy) * ncell + iz, need)
+    return np.nonzero(keep)[0]
+
+
 def density_pass_periodic(x, y, z, mass, h0, k: int, box: float,
                           max_iterations: int = 100, threads: int = 0,
                           margin: float | None = None, targets=None) -> OracleResult:

@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = (
     "sph_morton_keys_device", "sph_decomp_pack_rows_device", "sph_decomp_gather_rows_device",
     "sph_decomp_row_keys_device", "sph_decomp_level_bounds_device", "sph_decomp_window_bounds_device",
     "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device", "sph_bbox_device", "sph_range_query",
+    "sph_nfw_positions_device",
 )
 
 
@@ -104,6 +105,8 @@ def load():
         L.sph_fnv1a64.argtypes = [vp, ctypes.c_size_t]
         L.sph_fnv1a64.restype = ctypes.c_uint64
         L.sph_uniform_box_device.argtypes = [vp, i64, ctypes.c_uint64, ctypes.c_double, vp, vp, vp]
+        L.sph_nfw_positions_device.argtypes = [vp, i64, i64, vp, vp, ctypes.c_double, ctypes.c_double,
+                                               ctypes.c_uint64, ctypes.c_double, vp, vp, vp, vp]
         L.sph_morton_keys_device.argtypes = [vp, i32, i64, vp, vp, vp, ctypes.POINTER(ctypes.c_double),
                                              ctypes.c_double, vp]
         L.sph_decomp_pack_rows_device.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]

@@ -231,13 +231,21 @@ __global__ void k_iota(int n, uint32_t *a) {
 // reference todo trace per particle: round j (1-based) searches with
 // h_{j-1} = h0 * g^(j-1) (sequential fp64 products, density.py:227) and
 // converges when count(h) >= K  <=>  d2_K <= h*h (octree.py:185, 215)
+constexpr int kFinalizeSmemBins = 8192;  // 32 KB of round counters per block
+
 __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ perm, const uint8_t *__restrict__ state,
                            const double *__restrict__ d2k, const double *__restrict__ rho_s,
                            const double *__restrict__ h0, int max_it, double *__restrict__ h_out,
                            double *__restrict__ rho_out, uint8_t *__restrict__ flags_out, int *rounds_hist,
                            unsigned long long *bad) {
-  extern __shared__ int sh[];
-  for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x) sh[i] = 0;
+  // per-block round histogram in shared memory when it fits (kFinalizeSmemBins),
+  // otherwise straight into the global one
+  extern __shared__ int sh_[];
+  const bool local = max_it + 2 <= kFinalizeSmemBins;
+  int *sh = local ? sh_ : rounds_hist;
+  if (local) {
+    for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x) sh[i] = 0;
+  }
   __syncthreads();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n && (int)perm[p] < n_targets) {  // ghosts (original index >= n_targets) are candidates only
@@ -260,8 +268,10 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
     flags_out[o] = conv ? 0 : 1;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x)
-    if (sh[i]) atomicAdd(&rounds_hist[i], sh[i]);
+  if (local) {
+    for (int i = threadIdx.x; i < max_it + 2; i += blockDim.x)
+      if (sh[i]) atomicAdd(&rounds_hist[i], sh[i]);
+  }
 }
 
 template <typename T>
@@ -944,7 +954,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     const unsigned long long bad_init = ~0ull;
     SPH_CK(cudaMemcpyAsync(ctx->stats.p + 2, &bad_init, sizeof(bad_init), cudaMemcpyHostToDevice, ctx->stream));
     if (ctx->in_h_ready) cudaStreamWaitEvent(ctx->stream, ctx->in_h_ready, 0);  // h0 copied on the side stream
-    k_finalize<<<nblk(n), kTB, sizeof(int) * (max_it + 2), ctx->stream>>>(
+    k_finalize<<<nblk(n), kTB, max_it + 2 <= kFinalizeSmemBins ? sizeof(int) * (max_it + 2) : 0, ctx->stream>>>(
         n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out,
         rounds_hist, ctx->stats.p + 2);
     ++launches;
@@ -1179,6 +1189,22 @@ int sph_uniform_box_device(sph_ctx *ctx, int64_t n, uint64_t seed, double box, d
   k_uniform_box<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(n, seed, box, d_x, d_y, d_z);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, SPH_CUDA_ERROR, std::string("k_uniform_box: ") + cudaGetErrorString(e));
+  return SPH_OK;
+}
+
+int sph_nfw_positions_device(sph_ctx *ctx, int64_t n, int64_t n_halos, const int64_t *d_halo_start,
+                             const double *d_halo, double concentration, double x_max, uint64_t seed, double box,
+                             float *d_x, float *d_y, float *d_z, float *d_vel) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 0 || n_halos < 0 || !(box > 0.0) || !(concentration > 0.0) || !(x_max > 0.0) || !d_halo_start ||
+      (n_halos > 0 && !d_halo) || (n > 0 && (!d_x || !d_y || !d_z)))
+    return fail(ctx, SPH_INVALID, "invalid NFW generator request");
+  if (n == 0) return SPH_OK;
+  cudaSetDevice(ctx->device);
+  launch_nfw_positions(ctx->stream, n, n_halos, d_halo_start, d_halo, concentration, x_max, seed, box, d_x, d_y, d_z,
+                       d_vel);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, SPH_CUDA_ERROR, std::string("k_nfw_positions: ") + cudaGetErrorString(e));
   return SPH_OK;
 }
 

@@ -11,7 +11,8 @@ namespace {
 constexpr int kDT = 256;
 
 // row i of the record buffer = (x, y, z, m, h0, gid, key_hi, key_lo) of
-// particle order[i]; the key travels as two exact 32-bit halves
+// particle order[i]; the key travels as two exact 32-bit halves and the
+// global id as its int64 bit pattern (exact for any id)
 template <typename PosT>
 __global__ void k_pack_rows(int64_t n, const int64_t *__restrict__ order, const PosT *__restrict__ x,
                             const PosT *__restrict__ y, const PosT *__restrict__ z, const double *__restrict__ m,
@@ -23,7 +24,7 @@ __global__ void k_pack_rows(int64_t n, const int64_t *__restrict__ order, const 
   const long long key = keys[j];
   double4 *o = reinterpret_cast<double4 *>(rows + 8 * i);
   o[0] = make_double4((double)x[j], (double)y[j], (double)z[j], m[j]);
-  o[1] = make_double4(h0[j], (double)gid[j], (double)(key >> 32), (double)(key & 0xFFFFFFFFll));
+  o[1] = make_double4(h0[j], __longlong_as_double((long long)gid[j]), (double)(key >> 32), (double)(key & 0xFFFFFFFFll));
 }
 
 // dst row i = src row idx[i] (width doubles per row)

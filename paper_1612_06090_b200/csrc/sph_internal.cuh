@@ -241,5 +241,9 @@ void launch_r0(cudaStream_t s, const float4 *nlo, const float4 *nhi, const int *
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes);
 size_t select_temp_needed(int n);
+// clustered workload generator (sph_workload.cu)
+void launch_nfw_positions(cudaStream_t s, int64_t n, int64_t n_halos, const int64_t *start, const double *halo,
+                          double conc, double x_max, uint64_t seed, double box, float *x, float *y, float *z,
+                          float *vel);
 
 }  // namespace sph

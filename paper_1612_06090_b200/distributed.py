@@ -108,7 +108,8 @@ class TorchOps:
         import torch
         k = keys[order]
         return torch.stack([x[order].double(), y[order].double(), z[order].double(), m[order], h0[order],
-                            gid[order].double(), (k >> 32).double(), (k & 0xFFFFFFFF).double()], dim=1)
+                            gid[order].contiguous().view(torch.float64), (k >> 32).double(),
+                            (k & 0xFFFFFFFF).double()], dim=1)
 
     def gather_rows(self, rows, idx):
         return rows[idx]
@@ -521,6 +522,14 @@ def decomposed_pass(x, y, z, mass, h0, gid, k: int, compute, *, periodic: bool =
     stream = getattr(compute, "stream", None)
     ctxm = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
     caller = torch.cuda.current_stream(x.device) if stream is not None else None
+    if caller is not None and caller.cuda_stream != stream.cuda_stream:
+        # the inputs may still be in flight on the caller's stream (e.g. a
+        # non_blocking host copy): the library's stream waits for them, and
+        # their memory is not reused before the library's stream is done
+        stream.wait_stream(caller)
+        for t in (x, y, z, mass, h0, gid):
+            if t.is_cuda:
+                t.record_stream(stream)
     with ctxm:
         res = _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_iterations,
                           group_particles, pair_chunk, comm)
@@ -649,8 +658,14 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
     dist.all_gather(gathered, mine.to(cdev))
     gk = torch.stack(gathered)
     n_total_d = gk[:, samples].sum()
-    allk = torch.sort(gk[:, :samples].reshape(-1)).values.to(dev)
-    splitters = allk[(torch.arange(1, world, device=dev) * allk.numel()) // world]
+    # count-weighted splitters: each of rank q's samples stands for n_q /
+    # samples particles, so uneven (or empty) ranks do not bias the cuts
+    sk_all, so = torch.sort(gk[:, :samples].reshape(-1))
+    wts = (gk[:, samples].to(f64) / samples).view(-1, 1).expand(-1, samples).reshape(-1)[so]
+    cum = torch.cumsum(wts, 0)
+    goal = torch.arange(1, world, device=cum.device, dtype=f64) * (n_total_d.to(f64) / world)
+    pick = torch.clamp(torch.searchsorted(cum, goal), max=max(sk_all.numel() - 1, 0))
+    splitters = sk_all[pick].to(dev)
     cuts = torch.searchsorted(sk, splitters)  # rank q owns keys in [splitter[q-1], splitter[q])
     edges = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), cuts,
                        torch.full((1,), n_local, dtype=torch.int64, device=dev)])
@@ -721,7 +736,8 @@ def _decomposed(x, y, z, mass, h0, gid, k, compute, periodic, box, samples, max_
                                      for i in range(1, len(_tm))), flush=True)
     hist = hist_from_todo_sizes(np.asarray(todo, dtype=np.int64), max_iterations)
     mb = float(bound.max().item()) if n_own else 0.0
-    return DecompResult(gid=owned[:, 5].to(torch.int64), h=h, rho=rho, todo_hist=hist, n_owned=n_own,
+    # the global id rides in column 5 as its int64 bit pattern (exact for any id)
+    return DecompResult(gid=owned[:, 5].contiguous().view(torch.int64), h=h, rho=rho, todo_hist=hist, n_owned=n_own,
                         n_ghosts=int(ghosts.shape[0]), max_bound=mb, bound=bound)
 
 

@@ -239,14 +239,19 @@ def density_pass_snapshot(path, k: int | None = None, device: int = 0, max_itera
     import torch
 
     from . import _lib
-    from .density import _raise_for, _stats_from
+    from .density import DEFAULT_K, _raise_for, _stats_from, initial_smoothing_length
 
     f, meta = load_particles_device(path, device)
     n = f["x"].numel()
-    k = int(k if k is not None else meta.get("k_neighbors", 64))
     L = _lib.load()
     ctx = _lib.context(device)
     h = f["smoothing_length"].clone()
+    # the reference CLI (cli.py:159-163): K defaults to the snapshot's
+    # k_neighbors, else DEFAULT_K; an explicit K that differs from it resets
+    # every h0 to initial_smoothing_length(box_side, n, K)
+    if k is not None and k != meta.get("k_neighbors"):
+        h.fill_(initial_smoothing_length(float(meta.get("box_side", 1.0)), n, int(k)))
+    k = int(k if k is not None else meta.get("k_neighbors", DEFAULT_K))
     rho = torch.empty(n, dtype=torch.float64, device=h.device)
     flags = torch.empty(n, dtype=torch.uint8, device=h.device)
     prm = _lib.SphParams(n=n, k=k, max_iterations=max_iterations, precision=_lib.PRECISION["auto"], periodic=0,

@@ -5,7 +5,13 @@
   per particle, x-y-z order) is ``mix(seed + (t+1)*GAMMA) >> 11`` scaled by
   2^-53 and by the box side.  The sequential stream is a pure function of
   the counter, so it vectorises.
-* ``nfw_halos`` is the clustered generator of BASELINE configs 2-5, which
+* ``config_device`` generates configs 2-5 on the GPU (C ABI
+  ``sph_nfw_positions_device``; the bench and the full-size tests use it):
+  the host draws only the halo table (``halo_table``: the same rules as
+  below), every per-particle draw is the splitmix64 counter stream (draw
+  8i + j of particle i), so 134M particles take milliseconds.
+  ``nfw_host_restatement`` is its numpy restatement (test infrastructure).
+* ``nfw_halos`` is the host clustered generator (small CPU tests), which
   the reference does not have.  Rules chosen and recorded here:
   halo particle counts are drawn from dN/dM ~ M^-1.9 on [100, 50000] and
   rescaled (largest remainder) to sum to round(f_halo * N); r_vir from an
@@ -194,6 +200,145 @@ def config(number: int, seed: int | None = None):
                     h0=np.full(n, _initial_h(box, n, 64)), k=64, box=box, periodic=True, fp32=True,
                     name="uniform 1048576 fp32 (diagnostic)")
     raise ValueError(f"unknown config {number}")
+
+
+# ---------------------------------------------------------------------------
+# on-device clustered generator (C ABI sph_nfw_positions_device)
+# ---------------------------------------------------------------------------
+def halo_table(n: int, box: float, n_halos: int, seed: int, halo_fraction: float = 0.8,
+               m_min: float = 100.0, m_max: float = 50000.0, slope: float = -1.9):
+    """Halo counts, centres, r_vir and velocity sigma of ``nfw_halos`` (the
+    same host rules: power-law masses rescaled by largest remainder, r_vir
+    at 200x the mean density); the per-particle draws are the device's.
+    Returns (start int64[n_halos + 1], halo float64[n_halos, 5])."""
+    rng = np.random.default_rng(seed)
+    n_halo_total = int(round(halo_fraction * n))
+    a = slope + 1.0
+    u = rng.random(n_halos)
+    masses = (m_min ** a + u * (m_max ** a - m_min ** a)) ** (1.0 / a)
+    counts = _largest_remainder(masses, n_halo_total) if n_halos else np.zeros(0, np.int64)
+    centres = rng.random((n_halos, 3)) * box
+    mean_density = n / box ** 3
+    r_vir = (3.0 * counts / (4.0 * math.pi * 200.0 * mean_density)) ** (1.0 / 3.0)
+    sigma = counts.astype(np.float64) ** (1.0 / 3.0) * 0.1
+    start = np.zeros(n_halos + 1, dtype=np.int64)
+    np.cumsum(counts, out=start[1:])
+    halo = np.ascontiguousarray(np.column_stack([centres, r_vir, sigma]), dtype=np.float64)
+    return start, halo
+
+
+def nfw_device(n: int, box: float, start, halo, seed: int, concentration: float = 10.0, x_max: float | None = None,
+               device: int = 0, velocities: bool = False):
+    """Positions (three fp32 cuda tensors, and optionally (n, 3) fp32
+    velocities) of the clustered set generated on the GPU."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    L = _lib.load()
+    ctx = _lib.context(device)
+    dev = f"cuda:{device}"
+    d_start = torch.from_numpy(np.ascontiguousarray(start, dtype=np.int64)).to(dev)
+    d_halo = torch.from_numpy(np.ascontiguousarray(halo, dtype=np.float64).reshape(-1)).to(dev)
+    torch.cuda.synchronize(device)
+    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)]
+    vel = torch.empty((n, 3), dtype=torch.float32, device=dev) if velocities else None
+    n_halos = len(start) - 1
+    rc = L.sph_nfw_positions_device(ctx, n, n_halos, ctypes.c_void_p(d_start.data_ptr()),
+                                    ctypes.c_void_p(d_halo.data_ptr() if n_halos else 0), float(concentration),
+                                    float(concentration if x_max is None else x_max),
+                                    ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), float(box),
+                                    *[ctypes.c_void_p(t.data_ptr()) for t in out],
+                                    ctypes.c_void_p(vel.data_ptr() if vel is not None else 0))
+    if rc != _lib.SPH_OK:
+        raise RuntimeError(f"sph_nfw_positions_device failed ({rc}): {_lib.last_error(ctx)}")
+    torch.cuda.ExternalStream(_lib.stream_handle(ctx), device=dev).synchronize()
+    return (tuple(out), vel) if velocities else tuple(out)
+
+
+def nfw_host_restatement(n: int, box: float, start, halo, seed: int, concentration: float = 10.0,
+                         x_max: float | None = None) -> np.ndarray:
+    """numpy restatement of the device generator (same counters and formulas;
+    libm may differ from the device's in the last bits of log1p / sincos, so
+    a few fp32 positions can differ by an ulp).  Test infrastructure."""
+    x_max = concentration if x_max is None else x_max
+    i = np.arange(n, dtype=np.uint64)
+
+    def u(j):
+        t = i * np.uint64(8) + np.uint64(j + 1)
+        with np.errstate(over="ignore"):
+            s = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + t * _GAMMA
+            z = (s ^ (s >> np.uint64(30))) * _MIX1
+            z = (z ^ (z >> np.uint64(27))) * _MIX2
+            z = z ^ (z >> np.uint64(31))
+        return (z >> np.uint64(11)).astype(np.float64) * _TO_UNIT
+
+    start = np.asarray(start, dtype=np.int64)
+    halo = np.asarray(halo, dtype=np.float64).reshape(-1, 5)
+    nh = int(start[-1])
+    pos = np.empty((n, 3))
+    if nh:
+        hid = np.searchsorted(start, np.arange(nh), side="right") - 1
+        hp = halo[hid]
+        um = u(0)[:nh] * nfw_enclosed(x_max)
+        a = np.zeros(nh)
+        b = np.full(nh, x_max)
+        for _ in range(60):
+            mid = 0.5 * (a + b)
+            below = nfw_enclosed(mid) < um
+            a = np.where(below, mid, a)
+            b = np.where(below, b, mid)
+        r = 0.5 * (a + b) * (hp[:, 3] / concentration)
+        mu = 2.0 * u(1)[:nh] - 1.0
+        phi = 6.283185307179586 * u(2)[:nh]
+        s = np.sqrt(np.maximum(0.0, 1.0 - mu * mu))
+        pos[:nh, 0] = hp[:, 0] + r * (s * np.cos(phi))
+        pos[:nh, 1] = hp[:, 1] + r * (s * np.sin(phi))
+        pos[:nh, 2] = hp[:, 2] + r * mu
+    for ax in range(3):
+        pos[nh:, ax] = u(ax)[nh:] * box
+    pos = np.mod(pos, box).astype(np.float32)
+    top = np.nextafter(np.float32(box), np.float32(0.0))
+    pos[pos.astype(np.float64) >= box] = top
+    return pos
+
+
+def _config_table(number: int, n_ranks: int = 1):
+    """(n, box, n_halos, K, concentration, x_max, halo fraction) of config 2-5."""
+    g = n_ranks ** (1.0 / 3.0)
+    if number in (2, 3, 4):
+        n, box, halos = {2: (1 << 20, 100.0, 200), 3: (1 << 24, 100.0 * 16 ** (1.0 / 3.0), 20000),
+                         4: (1 << 27, 400.0, 150000)}[number]
+        return n * n_ranks, box * g, halos * n_ranks, 64, 10.0, 10.0
+    if number == 5:
+        return (1 << 23) * n_ranks, 4.0 * g, 1, 128, 20.0, 40.0
+    raise ValueError(f"config {number} is not a clustered config")
+
+
+def config_device(number: int, seed: int | None = None, device: int = 0, n_ranks: int = 1,
+                  host_positions: bool = False):
+    """Config ``number`` (2-5) with its positions generated on the GPU: a dict
+    with ``x, y, z`` (fp32 cuda tensors), ``mass`` / ``h0`` (numpy fp64), K,
+    box; ``pos`` (numpy (n, 3) fp64 of the fp32 values) when
+    ``host_positions``.  ``n_ranks > 1`` is the weak-scaled set (n_ranks x
+    particles, halos and volume)."""
+    seed = number if seed is None else seed
+    n, box, n_halos, k, conc, x_max = _config_table(number, n_ranks)
+    if number == 5:
+        n_bg = int(round(0.05 * n))
+        start = np.array([0, n - n_bg], dtype=np.int64)
+        halo = np.array([[0.5 * box, 0.5 * box, 0.5 * box, 1.0, 1.0]])
+    else:
+        start, halo = halo_table(n, box, n_halos, seed)
+    x, y, z = nfw_device(n, box, start, halo, seed, conc, x_max, device=device)
+    w = dict(x=x, y=y, z=z, mass=np.full(n, 1.0 / n), h0=np.full(n, _initial_h(box, n, k)), k=k, box=box,
+             periodic=True, fp32=True, halo_start=start, halo=halo, seed=seed, concentration=conc, x_max=x_max,
+             name=f"C{number} device-generated {n} fp32")
+    if host_positions:
+        w["pos"] = np.stack([t.cpu().numpy() for t in (x, y, z)], axis=1).astype(np.float64)
+    return w
 
 
 def config_weak(number: int, n_ranks: int, seed: int | None = None):

@@ -13,6 +13,9 @@ from paper_1612_06090_b200 import distributed as D
 from paper_1612_06090_b200 import workload
 
 
+GID_BASE = (1 << 60) + 7  # ids far above 2^53: not representable as doubles
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -153,10 +156,14 @@ def test_key_halves_roundtrip():
     assert torch.equal(back, keys)
 
 
-@pytest.mark.parametrize("world,periodic", [(4, True), (5, False)])
-def test_thread_ranks_match_single_process(world, periodic):
+@pytest.mark.parametrize("world,periodic,split", [(4, True, "interleaved"), (5, False, "interleaved"),
+                                                 (4, False, "one_rank")])
+def test_thread_ranks_match_single_process(world, periodic, split):
     # in-process ranks (ThreadComm) over the oracle: the same decomposition at
-    # world sizes beyond what process spawning makes cheap
+    # world sizes beyond what process spawning makes cheap.  "one_rank": every
+    # particle starts on rank 0 (the others pass empty tensors): the
+    # count-weighted splitters must still balance ownership; global ids above
+    # 2^53 must come back exactly (they ride as int64 bit patterns)
     import threading
 
     import torch
@@ -168,10 +175,12 @@ def test_thread_ranks_match_single_process(world, periodic):
 
     def run(r):
         try:
-            sel = np.arange(r, n, world)
+            sel = np.arange(r, n, world) if split == "interleaved" else (np.arange(n) if r == 0 else
+                                                                          np.arange(0))
             t = [torch.from_numpy(np.ascontiguousarray(pos[sel, i])) for i in range(3)]
             res = D.decomposed_pass(*t, torch.from_numpy(mass[sel]), torch.from_numpy(h0[sel]),
-                                    torch.from_numpy(sel.astype(np.int64)), k, D.NumpyCompute(oracle_local_pass),
+                                    torch.from_numpy(sel.astype(np.int64) + GID_BASE), k,
+                                    D.NumpyCompute(oracle_local_pass),
                                     periodic=periodic, box=box, samples=64, comm=D.ThreadComm(W, r))
             out[r] = res
         except Exception as e:  # pragma: no cover - surfaced below
@@ -182,8 +191,10 @@ def test_thread_ranks_match_single_process(world, periodic):
     [t.start() for t in th]
     [t.join() for t in th]
     assert not errs, errs
-    gid = np.concatenate([o.gid.numpy() for o in out])
+    gid = np.concatenate([o.gid.numpy() for o in out]) - GID_BASE
     assert np.array_equal(np.sort(gid), np.arange(n))
+    owned = [o.n_owned for o in out]
+    assert max(owned) <= 2 * n / world, owned  # balanced whatever the initial split
     h = np.empty(n)
     rho = np.empty(n)
     h[gid] = np.concatenate([o.h.numpy() for o in out])

@@ -453,3 +453,23 @@ def test_sphlab_adapter_on_the_gpu():
         ref.bench.compute_density_pass(small, sph.preset_config("optimised", k_neighbors=32))
     undo()
     assert ref.bench.compute_density_pass is None
+
+
+def test_snapshot_k_override_resets_h0_like_the_cli():
+    # sphlab run --k K with K != the snapshot's k_neighbors resets every h0 to
+    # initial_smoothing_length(box_side, n, K) (reference cli.py:159-163): the
+    # todo trace of the GPU pass must be the one that h0 produces
+    from paper_1612_06090_b200 import snapshot as S
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "snap_uniform3000_k32.sphk")
+    import json
+    secs = S.load(path)
+    f = S.decode_particles(secs["particles"])
+    meta = json.loads(secs["meta"]) if "meta" in secs else {}
+    k = 20
+    assert meta.get("k_neighbors") != k
+    h0 = np.full(f["x"].shape[0], sph.initial_smoothing_length(float(meta.get("box_side", 1.0)), f["x"].shape[0], k))
+    want = oracle.density_pass(f["x"], f["y"], f["z"], f["mass"], h0, k)
+    h, rho, flags, st = S.density_pass_snapshot(path, k=k)
+    assert np.array_equal(h, want.h)
+    assert np.array_equal(st.todo_sizes, want.todo_sizes)
+    assert _rel(rho, want.rho) <= RTOL_F64
