@@ -186,36 +186,49 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (reference algorithm restated in C) on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_sampled(w, target_seconds: float, seed: int = 0):
+def cpu_sampled(w, target_seconds: float, seed: int = 0, fixed_s: float | None = None):
+    """The CPU port on random target samples of the full set.  One call of
+    the oracle costs a fixed part (periodic images + its single-threaded
+    octree over the whole set) plus a per-target part (search, select,
+    density on all host cores), so the whole pass is extrapolated as
+    t = t_fixed + (t_S - t_fixed) * N / S, with t_fixed the time of a call
+    for a handful of targets (``fixed_s`` reuses an earlier measurement)."""
     import oracle
     pos = w["pos"]
     n = pos.shape[0]
     k = int(w["k"])
     x, y, z = pos[:, 0], pos[:, 1], pos[:, 2]
     threads = oracle.nthreads()
-    t0 = time.perf_counter()
-    oracle.perm(x, y, z)  # single-threaded tree build, as in the reference
-    t_tree = time.perf_counter() - t0
     rng = np.random.default_rng(seed)
-    s = 256
-    t_sample = 0.0
-    while True:
+
+    def run(s):
         tg = np.sort(rng.choice(n, size=min(s, n), replace=False))
         t0 = time.perf_counter()
         if w["periodic"]:
             oracle.density_pass_periodic(x, y, z, w["mass"], w["h0"], k, float(w["box"]), threads=threads, targets=tg)
         else:
             oracle.density_pass(x, y, z, w["mass"], w["h0"], k, threads=threads, targets=tg)
-        t_sample = time.perf_counter() - t0 - (t_tree if True else 0.0)
-        t_sample = max(t_sample, 1e-6)
-        if t_sample * 4 > target_seconds or s >= n:
+        return time.perf_counter() - t0, tg.size
+
+    s0 = min(64, n)
+    if fixed_s is None:
+        fixed_s, _ = run(s0)
+    s = min(n, 4096)
+    spent = 0.0
+    while True:
+        t_s, size = run(s)
+        spent += t_s
+        per = max(t_s - fixed_s, 1e-9)
+        if per >= 0.5 * target_seconds or size >= n or spent > 4 * target_seconds:
             break
-        s = min(n, int(s * max(2.0, min(16.0, 0.5 * target_seconds / t_sample))))
-    t_full = t_tree + t_sample * n / tg.size
+        s = min(n, int(s * max(2.0, min(16.0, 0.6 * target_seconds / per))))
+    b = per / max(size - s0, 1)
+    t_full = t_s if size >= n else fixed_s + b * (n - s0)
     return {"value": n * k / t_full, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{tg.size} random targets of {n} (full tree build {t_tree:.2f}s, sample {t_sample:.2f}s), "
-                      f"extrapolated to all targets: t = t_tree + t_sample*N/S = {t_full:.1f}s",
-            "extrapolated": True, "measured_s": t_tree + t_sample,
+            "sample": (f"{size} random targets of {n}: {t_s:.2f}s per call, of which {fixed_s:.2f}s is the fixed "
+                       f"part (images + octree over all {n}, timed with {s0} targets); extrapolated "
+                       f"t = t_fixed + (t_S - t_fixed) * N / S = {t_full:.1f}s"),
+            "extrapolated": size < n, "measured_s": t_s, "fixed_s": fixed_s,
             "converged_particles_per_s": n / t_full, "cpu_count": os.cpu_count()}
 
 
@@ -254,11 +267,13 @@ def run_reference(args):
     vals, measured = [], []
     base = None
     per_step = max(0.5, min(args.cpu_seconds / 2, 120.0 / max(1, steps_total)))
+    fixed = None
     for step in range(steps_total):
         if full:
             base = probe if (probe is not None and step == 0) else cpu_full(w)
         else:
-            base = cpu_sampled(w, target_seconds=per_step, seed=step)
+            base = cpu_sampled(w, target_seconds=per_step, seed=step, fixed_s=fixed)
+            fixed = base["fixed_s"]
         if step >= args.warmup:
             vals.append(base["value"])
             measured.append(base["measured_s"])

@@ -97,6 +97,8 @@ typedef struct {
     int32_t select_rounds;              /* band rounds */
     int32_t n_nodes;                    /* search-tree nodes */
     double t_kernel_ms[4];              /* device time of: 0 search, 1 select, 2 density, 3 tree build */
+    double t_known_ms;                  /* device time of the known-radius kernel (inside t_kernel_ms[0]) */
+    int64_t known_fallbacks;            /* targets it left to the general kernel (-1: it did not run) */
 } sph_stats;
 
 /* context: owns a CUDA stream and device buffers, grown on demand and

@@ -47,7 +47,8 @@ class SphStats(ctypes.Structure):
                 ("search_pair_tests", ctypes.c_int64), ("bad_index", ctypes.c_int64),
                 ("unconverged", ctypes.c_int64), ("gpu_launches", ctypes.c_int32),
                 ("search_rounds", ctypes.c_int32), ("select_rounds", ctypes.c_int32),
-                ("n_nodes", ctypes.c_int32), ("t_kernel_ms", ctypes.c_double * 4)]
+                ("n_nodes", ctypes.c_int32), ("t_kernel_ms", ctypes.c_double * 4),
+                ("t_known_ms", ctypes.c_double), ("known_fallbacks", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {
@@ -66,6 +67,8 @@ class SphStats(ctypes.Structure):
             "n_nodes": int(self.n_nodes),
             "t_kernel_ms": {name: float(self.t_kernel_ms[i]) for i, name in enumerate(
                 ("search", "select", "density", "tree"))},
+            "t_known_ms": float(self.t_known_ms),
+            "known_fallbacks": int(self.known_fallbacks),
         }
 
 

@@ -67,7 +67,6 @@ struct sph_ctx {
   DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4] task count [5] member cursor [6..] rounds hist
   DevBuf<int2> tasks;
   DevBuf<uint32_t> members;
-  DevBuf<int> cells;
   DevBuf<int> noff;
   DevBuf<int> node_p;
   DevBuf<float4> nlo, nhi;
@@ -79,21 +78,18 @@ struct sph_ctx {
   DevBuf<int32_t> counts_s, counts_o;
   DevBuf<unsigned long long> stats;  // [0] tests [1] accepted [2] bad index (ord)
   DevBuf<unsigned long long> dbg;    // SPH_DEBUG=1: per-bundle diagnostics
-  bool debug = false;
-  bool warp = true;    // SPH_WARP=0: bundle histogram pass first (SPH_HYBRID) or bundle rounds
-  bool hybrid = true;  // SPH_HYBRID=0: bundle histogram rounds until settled
-  bool lists = true;   // SPH_LISTS=0: select + density by re-walking (MODE_BAND / MODE_DENS) only
-  int list_mult = 4;
-  int lshrink = 1;       // SPH_LSHRINK
-  int seed_stride = 12;  // SPH_SEED: per-target pass seeds (0/1 = off; 12 beat 6/8/16 on C1-C5, r01l)
-  int seed_outer = 0;    // SPH_SEED2: a sparser seed level at seed_stride x seed_outer first (0/1 = off; measured slower on C2: launch tails)
-  int bundle = 0;        // SPH_BUNDLE=1: bundle pass (sph_bundle.cu) between the seeds and the per-target kernel (experimental)
-  DevBuf<uint32_t> left; // targets the bundle pass leaves to the per-target kernel
+  bool debug = false;     // SPH_DEBUG=1: fallback counters on stderr
+  int seed_stride = 12;   // SPH_SEED: seed stride of the per-target pass (12 beat 6/8/16 on C1-C5, r01l; 0/1 = off)
+  float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
+  bool known = true;      // SPH_KNOWN=0: no known-radius kernel (the general kernel takes every non-seed target)
+  bool known_ran = false;
+  cudaEvent_t kev_known[2];
+  DevBuf<uint32_t> kn_list;   // targets the known-radius kernel leaves to the general kernel
+  DevBuf<float4> posj;        // fp32 path: (x, y, z, sorted index bits) per sorted position
   DevBuf<double> dscratch;  // decomposition helpers: super boxes of the ghost marking
   DevBuf<int> ncell_dev;    // cells of the search tree (counted with the tree, read with n_nodes)
   DevBuf<uint32_t> tlist;   // compacted target positions (ghost-aware seeding)
   int last_ncell = -1;
-  float seed_margin = 1.1f;  // SPH_SEEDM
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
   cudaStream_t stream2 = nullptr;  // side stream for host-to-device copies the first kernels do not need
@@ -105,33 +101,15 @@ struct sph_ctx {
   DevBuf<float> crad2;
   DevBuf<int> cnear;
   float near_frac = 0.5f;   // SPH_NEARF: cell-list records beyond near_frac * D go to the list's back
-  float d_pct = 1.0f;       // SPH_DPCT: cell-list radius D = this quantile of the cell's target radii
   int tshrink = 1;       // SPH_TSHRINK (shrink after every K >> tshrink new candidates; 1 measured best on C2/C5)
-  int static_sched = 0;  // SPH_STATIC=1: strided static target assignment (imbalanced; off)
-  int lists_early = 0;   // SPH_CLEARLY: 1 = cell lists for the seeds too (rebuilt after), 2 = one build before the seeds
-  int tchunk = 1;        // SPH_TCHUNK: consecutive targets per work grab of the per-target kernel (2-16 measured slower on C2)
-  float lcompact = 2.0f; // SPH_LCOMPACT (units of K)   // SPH_LISTCAP: neighbour-list capacity per target in units of K
-  int last_list_fallbacks = 0;
-  DevBuf<uint2> nlists;
   DevBuf<float4> crec;
   DevBuf<int4> anc4;
   DevBuf<int> parent, cellof;
   bool crec_ready = false;
   int tb_emit_r0 = 1;    // did the last tree build compute R0 (k_node_emit)?
   DevBuf<int> ncount;
-  int last_legacy = 0;
-  DevBuf<uint32_t> mpool;
-  DevBuf<int4> sgs;
-  DevBuf<int> owner, lpool;
-  DevBuf<int4> items;
-  DevBuf<uint32_t> pool;
-  DevBuf<uint8_t> band_rounds;
   DevBuf<int> qints;
-  float sub_d = 2.0f;
-  float sub_d_retry = 2.0f;  // task extent of retry rounds (SPH_SUBD_RETRY)
-  float r0_scale = 1.15f;
-  float c0_scale = 1e30f;  // SPH_C0SCALE: cap R0 by c0 x the cell's tight-box estimate (off by default)
-  int shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
+  float r0_scale = 1.15f;  // SPH_R0SCALE: tree-estimate radius scale (seeds)
   size_t cub_bytes = 0;
 };
 
@@ -370,7 +348,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.root = ctx->root.p;
   tb.bbox_ord = ctx->bbox_ord.p;
   tb.r0_scale = ctx->r0_scale;
-  tb.c0_scale = ctx->c0_scale;
+  tb.c0_scale = 1e30f;
   tb.emit_r0 = 1;
   tb.node_p = ctx->node_p.p;
   return tb;
@@ -393,14 +371,18 @@ int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *
                const double *mass, int k, float rmax, int *n_nodes, int *launches, bool search_tree) {
   TreeBuffers tb = tree_buffers(ctx);
   tb.mass_ready = ctx->in_mass_ready;
+  if (search_tree && compute_f32) {  // the known-radius kernel stages (x, y, z, index) records
+    SPH_CK(ctx->posj.ensure(n));
+    tb.posj = ctx->posj.p;
+  }
   // the per-target path derives R0 from the node sizes (k_r0) instead
-  tb.emit_r0 = (ctx->warp && n <= (1 << 27)) ? 0 : 1;
+  tb.emit_r0 = 0;
   ctx->tb_emit_r0 = tb.emit_r0;
   const int in32 = precision == SPH_PRECISION_F32 ? 1 : 0;
   tree_build(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, launches);
   if (search_tree) tree_build_search(ctx->stream, tb, n, in32, compute_f32, x, y, z, mass, k, rmax, launches);
   int host[3] = {0, 0, -1};
-  const bool index_cells = search_tree && ctx->warp && ctx->cell_lists > 0;
+  const bool index_cells = search_tree && ctx->cell_lists > 0;
   if (index_cells) {
     // cell index of every node, counted before the one sync of this stage
     // (the node count is still on the device: a grid over its upper bound)
@@ -463,15 +445,14 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.box = prm ? prm->box : 0.0;
   a.rmax = rmax;
   a.dbg = nullptr;
-  a.sub_d = ctx->sub_d;
+  a.sub_d = 2.0f;  // walking fallback passes: task extent in units of the leader's radius
   a.tasks = ctx->tasks.p;
   a.members = ctx->members.p;
   a.task_count = ctx->ints.p + 4;
   a.member_cursor = ctx->ints.p + 5;
-  a.shortcut = ctx->shortcut;
+  a.shortcut = (1 << MODE_BAND) | (1 << MODE_COUNT);
   a.tshrink = ctx->tshrink;
-  a.static_sched = ctx->static_sched;
-  a.tchunk = ctx->tchunk;
+  a.tchunk = 1;
   if (ctx->debug && ctx->dbg.ensure(8 * ((size_t)n + 32)) == cudaSuccess) a.dbg = ctx->dbg.p;
   return a;
 }
@@ -566,7 +547,6 @@ int run_rounds(sph_ctx *ctx, int mode, int f32, PassArgs a, uint8_t want, int ma
       return fail(ctx, SPH_CUDA_ERROR, "neighbour search did not settle (internal round limit)");
     }
     a.list = ctx->list.p;
-    a.sub_d = ctx->sub_d_retry;
     timed_pass(ctx, mode, f32, a, remaining, want);
     debug_report(ctx, mode, remaining);
     ++*launches;
@@ -651,11 +631,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
   if (rc) return rc;
   tm.mark(2);
-  int hist_rounds = 0, band_rounds = 0;
-  bool warp_deferred = false;  // per-target path: fallback counters checked with the results
-  PassArgs warp_args{};
-  if (ctx->warp && n <= (1 << 27)) {
-  // ---- one warp per target: search, exact select and density in one kernel ----
+  int hist_rounds = 1, band_rounds = 0;
+  // ---- search, exact select and density (per-target kernels) ----
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
@@ -669,145 +646,96 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   a.fb_list = ctx->list.p;          // compacted targets for the collect instance
   a.fb_count = ctx->qints.p + 15;
   SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-  {
-    const int i = ctx->n_kev;
-    if (i < 64) {
-      ctx->kev_mode[i] = MODE_HIST;
-      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
-    }
-    // neighbour-cell lists for the radii currently in r0 (k_cell_lists); sets
-    // the list fields of dst, false when they could not be allocated
-    auto build_lists = [&](PassArgs &dst) -> bool {
-      const int cap = ctx->cell_lists;
-      const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
-      if (cap <= 0 || ncell < 0 || ctx->clist.ensure((size_t)ncell * cap) != cudaSuccess ||
-          ctx->clen.ensure(ncell) != cudaSuccess || ctx->crad2.ensure(ncell) != cudaSuccess ||
-          ctx->cnear.ensure(ncell) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-      }
-      launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
-                        ctx->crad2.p, ctx->cnear.p, ctx->near_frac, ctx->d_pct, ctx->num_sms, ncell);
-      dst.cnear = ctx->cnear.p;
-      dst.near_frac2 = ctx->near_frac * ctx->near_frac;
-      dst.clist = ctx->clist.p;
-      dst.clen = ctx->clen.p;
-      dst.crad2 = ctx->crad2.p;
-      dst.cellidx = ctx->cellidx.p;
-      dst.clcap = cap;
-      launches += 1;  // (the cell index is counted by stage_tree)
-      return true;
-    };
-    bool lists_built = false;
-    if (ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
-      // seeds first (every seed_stride-th sorted position), then every other
-      // target starts from its neighbouring seeds' converged h (sorted
-      // neighbours are spatial neighbours): fewer regrows, tighter radii
-      const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
-      SPH_CK(ctx->seeds.ensure(ns));
-      PassArgs sa = a;
-      sa.list = ctx->seeds.p;
-      sa.list_count = ctx->qints.p + 14;
-      if (ctx->lists_early > 0 && ctx->cell_lists > 0) {
-        // lists for the tree's radii, walked by the seeds too (and, with
-        // lists_early == 2, by the other targets instead of a second build)
-        lists_built = build_lists(sa);
-        if (lists_built && ctx->lists_early == 2) {
-          a.cnear = sa.cnear;
-          a.near_frac2 = sa.near_frac2;
-          a.clist = sa.clist;
-          a.clen = sa.clen;
-          a.crad2 = sa.crad2;
-          a.cellidx = sa.cellidx;
-          a.clcap = sa.clcap;
-        }
-      }
-      const int outer = ctx->seed_stride * ctx->seed_outer;
-      if (ctx->seed_outer > 1 && n >= 64 * outer) {
-        // a sparser seed level first: every outer-th position from the tree's
-        // estimate, then the seeds from those seeds' h (the next launch skips
-        // the outer seeds already settled)
-        const int no = (n + outer - 1) / outer;
-        k_seed_list<<<nblk(no), kTB, 0, ctx->stream>>>(no, outer, ctx->seeds.p, ctx->qints.p + 14);
-        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-        k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, outer, ctx->seed_stride, ctx->state.p, ctx->d2k.p,
-                                                        ctx->seed_margin, rmax, ctx->r0.p);
-        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-        launches += 3;
-      }
-      if (n_targets < n) {
-        // ghosts in the set: seed along the target order (compacted targets)
-        SPH_CK(ctx->tlist.ensure(n));
-        launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->tlist.p, ctx->qints.p + 28,
-                      ctx->cub_temp.p, ctx->cub_bytes);
-        const int nst = (n_targets + ctx->seed_stride - 1) / ctx->seed_stride;
-        k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
-                                                             ctx->qints.p + 14);
-        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-        k_seed_radius_from<<<nblk(n_targets), kTB, 0, ctx->stream>>>(n_targets, ctx->seed_stride, ctx->tlist.p,
-                                                                     ctx->state.p, ctx->d2k.p, ctx->seed_margin,
-                                                                     rmax, ctx->r0.p);
-        launches += 2;
-      } else {
-        k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
-        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-        k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, 1, ctx->state.p, ctx->d2k.p,
-                                                        ctx->seed_margin, rmax, ctx->r0.p);
-      }
-      SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-      launches += 3;
-      if (ctx->bundle && compute_f32) {
-        // the bundle pass (sph_bundle.cu): 32 sorted targets per warp with the
-        // seeds' radii; what it leaves goes to the per-target kernel as a list
-        SPH_CK(ctx->left.ensure(n));
-        SPH_CK(cudaMemsetAsync(ctx->qints.p + 24, 0, 4 * sizeof(int), ctx->stream));
-        launch_bundle(ctx->stream, a, ctx->qints.p + 24, ctx->num_sms);
-        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-        launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->left.p, ctx->qints.p + 27,
-                      ctx->cub_temp.p, ctx->cub_bytes);
-        a.list = ctx->left.p;
-        a.list_count = ctx->qints.p + 27;
-        launches += 3;
-        if (ctx->debug) {
-          int bq[4];
-          cudaStreamSynchronize(ctx->stream);
-          cudaMemcpy(bq, ctx->qints.p + 24, sizeof(bq), cudaMemcpyDeviceToHost);
-          fprintf(stderr, "[sph bundle] %d bundles failed, %d lanes failed, %d targets done, %d left\n", bq[0], bq[1],
-                  bq[2], bq[3]);
-        }
-      }
-      if (ctx->cell_lists > 0 && !(lists_built && ctx->lists_early == 2)) {
-        // neighbour-cell lists for the radii the seeds imply
-        build_lists(a);
-      }
-    }
-    if (!a.list && n_targets < n && ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride) {
-      // ghosts in the set: walk the compacted targets (seeded above), not every position
-      a.list = ctx->tlist.p;
-      a.list_count = ctx->qints.p + 28;
-    }
-    launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-    a.list = nullptr;  // the bundle pass's leftover list is for this launch only
-    a.list_count = nullptr;
-    if (i < 64) {
-      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
-      ctx->n_kev = i + 1;
-    }
+  launches += 2;
+  const int kv0 = ctx->n_kev;
+  if (kv0 + 2 < 64) {
+    ctx->kev_mode[kv0] = MODE_HIST;
+    cudaEventRecord(ctx->kev[2 * kv0], ctx->stream);
   }
+  bool known_run = false;
+  const bool seeded = ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride;
+  if (seeded) {
+    // seeds first (every seed_stride-th sorted position, the general kernel
+    // from the tree's radius estimate), then every other target starts from
+    // its neighbouring seeds' converged h (sorted neighbours are spatial
+    // neighbours): the known-radius kernel takes them
+    const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
+    SPH_CK(ctx->seeds.ensure(ns));
+    PassArgs sa = a;
+    sa.list = ctx->seeds.p;
+    sa.list_count = ctx->qints.p + 14;
+    if (n_targets < n) {
+      // ghosts in the set: seed along the target order (compacted targets)
+      SPH_CK(ctx->tlist.ensure(n));
+      launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->tlist.p, ctx->qints.p + 28,
+                    ctx->cub_temp.p, ctx->cub_bytes);
+      const int nst = (n_targets + ctx->seed_stride - 1) / ctx->seed_stride;
+      k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
+                                                           ctx->qints.p + 14);
+      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+      k_seed_radius_from<<<nblk(n_targets), kTB, 0, ctx->stream>>>(n_targets, ctx->seed_stride, ctx->tlist.p,
+                                                                   ctx->state.p, ctx->d2k.p, ctx->seed_margin, rmax,
+                                                                   ctx->r0.p);
+      launches += 5;
+      a.list = ctx->tlist.p;  // walk the compacted targets, not every position
+      a.list_count = ctx->qints.p + 28;
+    } else {
+      k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
+      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+      k_seed_radius<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->seed_stride, 1, ctx->state.p, ctx->d2k.p,
+                                                      ctx->seed_margin, rmax, ctx->r0.p);
+      launches += 3;
+    }
+    SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+    // neighbour-cell lists for the radii the seeds imply
+    const int cap = ctx->cell_lists;
+    const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
+    if (cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
+        ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
+        ctx->cnear.ensure(ncell) == cudaSuccess) {
+      launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
+                        ctx->crad2.p, ctx->cnear.p, ctx->near_frac, 1.0f, ctx->num_sms, ncell);
+      a.cnear = ctx->cnear.p;
+      a.near_frac2 = ctx->near_frac * ctx->near_frac;
+      a.clist = ctx->clist.p;
+      a.clen = ctx->clen.p;
+      a.crad2 = ctx->crad2.p;
+      a.cellidx = ctx->cellidx.p;
+      a.clcap = cap;
+      launches += 1;
+      if (compute_f32 && ctx->known && cap <= known_max_cells() && ctx->kn_list.ensure(n) == cudaSuccess) {
+        // the known-radius kernel (sph_known.cu); what it leaves, the general kernel takes
+        const int kv = ctx->n_kev;
+        if (kv + 2 < 64) cudaEventRecord(ctx->kev_known[0], ctx->stream);
+        PassArgs ka = a;
+        ka.posj = ctx->posj.p;
+        ka.fb_list = ctx->kn_list.p;
+        ka.fb_count = ctx->qints.p + 21;
+        ka.kn_counters = ctx->qints.p + 10;
+        launch_known(ctx->stream, ka, known_list_cap(k), ctx->num_sms);
+        cudaEventRecord(ctx->kev_known[1], ctx->stream);
+        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+        a.list = ctx->kn_list.p;
+        a.list_count = ctx->qints.p + 21;
+        launches += 1;
+        known_run = true;
+      }
+    }
+    cudaGetLastError();  // an allocation failure above only skips the lists
+  }
+  ctx->known_ran = known_run;
+  launch_target(ctx->stream, compute_f32, a, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
   ++launches;
-  hist_rounds = 1;
+  a.list = nullptr;
+  a.list_count = nullptr;
   if (ctx->debug) {
-    int fbk[4] = {0, 0, 0, 0};
+    int fbk[32];
     cudaStreamSynchronize(ctx->stream);
-    cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses; %d walks\n", fbk[0], fbk[1], fbk[3]);
-    std::vector<uint8_t> hs(n);
-    cudaMemcpy(hs.data(), ctx->state.p, n, cudaMemcpyDeviceToHost);
-    int cnt[16] = {0};
-    for (int i = 0; i < n; ++i) cnt[hs[i] & 15]++;
-    fprintf(stderr, "[sph warp] states:");
-    for (int i = 0; i < 16; ++i) if (cnt[i]) fprintf(stderr, " %d:%d", i, cnt[i]);
-    fprintf(stderr, "\n");
+    cudaMemcpy(fbk, ctx->qints.p, sizeof(fbk), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[sph known] %d targets to the general kernel: image %d, list full %d, < K %d, select %d\n",
+            fbk[21], fbk[10], fbk[11], fbk[12], fbk[13]);
+    fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses; %d walks\n",
+            fbk[5], fbk[6], fbk[8]);
   }
   // the collect instance for overflowed lists is enqueued unconditionally: it
   // reads its target count on the device ([15], appended by the main kernel)
@@ -823,132 +751,24 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     c.list_count = ctx->qints.p + 15;
     c.fb_list = nullptr;
     launch_target(ctx->stream, compute_f32, c, ctx->collect_cap, ctx->qints.p + 16, ctx->num_sms, true);
-    ++launches;
+    launches += 2;
+  }
+  if (kv0 + 2 < 64) {
+    cudaEventRecord(ctx->kev[2 * kv0 + 1], ctx->stream);
+    ctx->n_kev = kv0 + 1;
   }
   SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
                          ctx->stream));
   tm.mark(3);
-  warp_deferred = true;
-  warp_args = a;
+  const bool warp_deferred = true;
+  PassArgs warp_args = a;
   tm.mark(4);
   tm.mark(5);
-  } else {
-  // ---- search ----
-  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
-  SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
-  k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);
-  ++launches;
-  PassArgs a = base_args(ctx, n, k, n_nodes, prm, rmax);
-  // neighbour lists recorded by the histogram pass (entry index field: 27 bits)
-  bool use_lists = false;
-  if (ctx->lists && ctx->list_mult > 0 && n <= (1 << 27)) {
-    const size_t cap = std::min((size_t)ctx->list_mult * (size_t)k, (size_t)lists_max_cap());
-    if (ctx->nlists.ensure(cap * (size_t)n) == cudaSuccess && ctx->ncount.ensure(n) == cudaSuccess &&
-        ctx->qints.ensure(32) == cudaSuccess) {
-      a.nlists = ctx->nlists.p;
-      a.ncount = ctx->ncount.p;
-      a.ncap = (int)cap;
-      a.lshrink = ctx->lshrink;
-      a.lcompact = (int)(ctx->lcompact * k);
-      use_lists = true;
-    } else {
-      cudaGetLastError();  // allocation failure: walk-based select/density instead
-    }
-  }
-  if (ctx->hybrid && n <= (1 << 27)) {
-    // bundle histogram pass once; the targets it could not settle go to the
-    // per-target kernel (own radius growth, no further rounds)
-    timed_pass(ctx, MODE_HIST, compute_f32, a, n, ST_NEED_HIST);
-    ++launches;
-    launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->list.p, ctx->ints.p + 2,
-                  ctx->cub_temp.p, ctx->cub_bytes);
-    launches += 2;
-    PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
-    rc = prepare_target_tree(ctx, n, n_nodes, t);
-    if (rc) return rc;
-    t.list = ctx->list.p;
-    t.ncount = a.ncount;
-    SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-    SPH_CK(ctx->qints.ensure(32));
-    const int i = ctx->n_kev;
-    if (i < 64) {
-      ctx->kev_mode[i] = MODE_HIST;
-      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
-    }
-    SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
-    launch_target(ctx->stream, compute_f32, t, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-    if (i < 64) {
-      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
-      ctx->n_kev = i + 1;
-    }
-    if (ctx->debug) {
-      int fbk[2] = {0, 0}, nrem = 0;
-      cudaStreamSynchronize(ctx->stream);
-      cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
-      cudaMemcpy(&nrem, ctx->ints.p + 2, sizeof(int), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "[sph hybrid] %d targets to the per-target kernel; fall back: %d overflowed lists, %d bracket misses\n",
-              nrem, fbk[0], fbk[1]);
-    }
-    launches += 2;
-    hist_rounds = 2;
-    // stack overflows (rare) stay NEED_HIST: bundle rounds
-    int hr = 0;
-    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hr);
-  } else {
-    rc = run_rounds(ctx, MODE_HIST, compute_f32, a, ST_NEED_HIST, 64, &launches, &hist_rounds);
-  }
-  if (rc) return rc;
-  // search pair tests so far -> stats[3]
-  SPH_CK(cudaMemcpyAsync(ctx->stats.p + 3, ctx->stats.p, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
-                         ctx->stream));
-  tm.mark(3);
-  // ---- select (+ density) ----
-  if (use_lists) {
-    SPH_CK(cudaMemsetAsync(ctx->qints.p + 5, 0, 3 * sizeof(int), ctx->stream));
-    SPH_CK(cudaMemsetAsync(ctx->qints.p + 7, 0, sizeof(int), ctx->stream));
-    const int i = ctx->n_kev;
-    if (i < 64) {
-      ctx->kev_mode[i] = MODE_BAND;
-      cudaEventRecord(ctx->kev[2 * i], ctx->stream);
-    }
-    launch_lists(ctx->stream, compute_f32, a, ctx->qints.p + 5, ctx->num_sms);
-    if (i < 64) {
-      cudaEventRecord(ctx->kev[2 * i + 1], ctx->stream);
-      ctx->n_kev = i + 1;
-    }
-    ++launches;
-    if (ctx->debug) {
-      int fbk[3] = {0, 0, 0};
-      cudaStreamSynchronize(ctx->stream);
-      cudaMemcpy(fbk, ctx->qints.p + 5, sizeof(fbk), cudaMemcpyDeviceToHost);
-      ctx->last_list_fallbacks = fbk[0] + fbk[1] + fbk[2];
-      fprintf(stderr, "[sph lists] fall back to the walking select: %d overflowed lists, %d bracket misses, %d crowded brackets\n",
-              fbk[0], fbk[1], fbk[2]);
-    }
-    a.nlists = nullptr;
-    if (ctx->hybrid && ctx->crec_ready) {
-      // overflowed lists (bundle pass or per-target kernel): collect up to the bracket top
-      PassArgs t = base_args(ctx, n, k, n_nodes, prm, rmax);
-      use_target_tree(ctx, n_nodes, t);
-      t.ncount = ctx->ncount.p;
-      SPH_CK(cudaMemsetAsync(t.work_counter, 0, sizeof(int), ctx->stream));
-      launch_target(ctx->stream, compute_f32, t, ctx->collect_cap, nullptr, ctx->num_sms, true);
-      ++launches;
-    }
-  }
-  rc = run_rounds(ctx, MODE_BAND, compute_f32, a, ST_NEED_BAND, 64, &launches, &band_rounds);
-  if (rc) return rc;
-  tm.mark(4);
-  // ---- interact ----
-  timed_pass(ctx, MODE_DENS, compute_f32, a, n, ST_DONE);
-  debug_report(ctx, MODE_DENS, n);
-  ++launches;
-  tm.mark(5);
-  }
   // ---- finalize ----
   int *rounds_hist = ctx->ints.p + kIntsFixed;
   std::vector<int> hist(max_it + 2);
   unsigned long long stat_all[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int qd[32] = {0};
   for (int attempt = 0;; ++attempt) {
     SPH_CK(cudaMemsetAsync(rounds_hist, 0, sizeof(int) * (max_it + 2), ctx->stream));
     const unsigned long long bad_init = ~0ull;
@@ -959,7 +779,6 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         rounds_hist, ctx->stats.p + 2);
     ++launches;
     tm.mark(6);
-    int qd[32];
     SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
     SPH_CK(cudaMemcpyAsync(stat_all, ctx->stats.p, sizeof(stat_all), cudaMemcpyDeviceToHost, ctx->stream));
     if (defer_root) SPH_CK(cudaMemcpyAsync(&root, ctx->root.p, sizeof(RootInfo), cudaMemcpyDeviceToHost, ctx->stream));
@@ -995,7 +814,17 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       if (root.lo[a2] < 0.0 || root.hi[a2] >= prm->box)
         return fail(ctx, SPH_INVALID, "periodic mode needs every position inside [0, box)");
   }
-  if (st) st->t_kernel_ms[3] = tm.ms(1, 2);
+  if (st) {
+    st->t_kernel_ms[3] = tm.ms(1, 2);
+    if (ctx->known_ran) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ctx->kev_known[0], ctx->kev_known[1]);
+      st->t_known_ms = t;
+      st->known_fallbacks = qd[21];
+    } else {
+      st->known_fallbacks = -1;
+    }
+  }
 
   // ---- stats, reference todo trace, error mapping ----
   const long long unconv = hist[max_it + 1];
@@ -1099,29 +928,16 @@ int sph_ctx_create(sph_ctx **out, int device) {
   for (auto &e : c->kev) cudaEventCreate(&e);
   const char *dbg = getenv("SPH_DEBUG");
   c->debug = dbg && dbg[0] == '1';
-  if (const char *v = getenv("SPH_LISTS")) c->lists = v[0] == '1';
-  if (const char *v = getenv("SPH_WARP")) c->warp = v[0] == '1';
-  if (const char *v = getenv("SPH_HYBRID")) c->hybrid = v[0] == '1';
-  if (const char *v = getenv("SPH_LISTCAP")) c->list_mult = atoi(v);
-  if (const char *v = getenv("SPH_LSHRINK")) c->lshrink = atoi(v);
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
-  if (const char *v = getenv("SPH_SEED2")) c->seed_outer = atoi(v);
-  if (const char *v = getenv("SPH_BUNDLE")) c->bundle = atoi(v);
+  if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
+  if (const char *v = getenv("SPH_KNOWN")) c->known = v[0] != '0';
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
-  if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
-  if (const char *v = getenv("SPH_STATIC")) c->static_sched = atoi(v);
-  if (const char *v = getenv("SPH_TCHUNK")) c->tchunk = atoi(v);
-  if (const char *v = getenv("SPH_CLEARLY")) c->lists_early = atoi(v);
   if (const char *v = getenv("SPH_NEARF")) c->near_frac = (float)atof(v);
-  if (const char *v = getenv("SPH_DPCT")) c->d_pct = (float)atof(v);
-  if (const char *v = getenv("SPH_LCOMPACT")) c->lcompact = (float)atof(v);
-  if (const char *v = getenv("SPH_SUBD")) c->sub_d = (float)atof(v);
-  if (const char *v = getenv("SPH_SUBD_RETRY")) c->sub_d_retry = (float)atof(v);
   if (const char *v = getenv("SPH_R0SCALE")) c->r0_scale = (float)atof(v);
-  if (const char *v = getenv("SPH_C0SCALE")) c->c0_scale = (float)atof(v);
-  if (const char *v = getenv("SPH_SHORTCUT")) c->shortcut = atoi(v);
+  cudaEventCreate(&c->kev_known[0]);
+  cudaEventCreate(&c->kev_known[1]);
   *out = c;
   return SPH_OK;
 }
@@ -1135,8 +951,14 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->cells.release(); c->items.release(); c->pool.release(); c->mpool.release(); c->sgs.release(); c->owner.release(); c->lpool.release(); c->nlists.release(); c->seeds.release(); c->left.release(); c->node_p.release(); c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release(); c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release(); c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->band_rounds.release(); c->qints.release(); c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->seeds.release(); c->node_p.release();
+  c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release();
+  c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release();
+  c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->qints.release();
+  c->root.release(); c->t_lo.release(); c->t_hi.release(); c->d2k.release(); c->kn_list.release(); c->posj.release();
   c->rho_s.release(); c->hfix.release(); c->mass_s.release(); c->counts_s.release(); c->counts_o.release(); c->stats.release();
+  cudaEventDestroy(c->kev_known[0]);
+  cudaEventDestroy(c->kev_known[1]);
   for (auto &e : c->ev) cudaEventDestroy(e);
   for (auto &e : c->kev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);

@@ -150,6 +150,8 @@ struct PassArgs {
   int clcap;
   uint32_t *fb_list;        // per-target kernel: targets left for the collect instance (+ counter)
   int *fb_count;
+  const float4 *posj;       // sorted (x, y, z, sorted index bits) per position (fp32 path; k_known stages it)
+  int *kn_counters;         // k_known fallback reasons (image, list full, < K within R, select) or nullptr
 };
 
 // ---- launchers (sph_tree.cu) ----
@@ -169,6 +171,7 @@ struct TreeBuffers {
   int *nsize;                           // particles per node subtree
   float *r0;                            // per sorted position initial radius
   void *pos_sorted;                     // float4 or double[4] per position
+  float4 *posj;                         // fp32 path: (x, y, z, sorted index bits) per position (or nullptr)
   double *mass_sorted;                  // fp64 masses per position
   void *cub_temp;
   size_t cub_temp_bytes;
@@ -218,15 +221,15 @@ void launch_keys_at(cudaStream_t s, int n, int precision_in, const void *x, cons
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
 void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
-// exact select + density from the histogram pass's neighbour lists (sph_lists.cu)
-void launch_lists(cudaStream_t s, int f32, const PassArgs &a, int *fallbacks, int num_sms);
-int lists_max_cap();
+// known-radius pass: cell-list cull, cp.async.bulk staging, list, select, density (sph_known.cu)
+int known_max_cells();
+int known_list_cap(int k);
+size_t known_smem_bytes(int lcap);
+void launch_known(cudaStream_t s, const PassArgs &a, int lcap, int num_sms);
 // fused per-target search + select + density (sph_warp.cu)
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,
                    bool collect = false);
-// bundle pass: 32 consecutive sorted targets per warp (sph_bundle.cu)
-void launch_bundle(cudaStream_t s, const PassArgs &a, int *counters, int num_sms);
 void launch_cell_index(cudaStream_t s, const float4 *nlo, int n_nodes, int *cellidx, int *cellnode, int *ncells);
 void launch_cell_index_dev(cudaStream_t s, const float4 *nlo, const int *n_nodes_dev, int max_nodes, int *cellidx,
                            int *cellnode, int *ncells);

@@ -230,13 +230,15 @@ template <typename PosT>
 __global__ void k_gather_f32(int n, const uint32_t *__restrict__ perm, const PosT *__restrict__ x,
                              const PosT *__restrict__ y, const PosT *__restrict__ z,
                              const double *__restrict__ mass, float4 *__restrict__ out,
-                             double *__restrict__ mass_out) {
+                             double *__restrict__ mass_out, float4 *__restrict__ posj) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t o = perm[p];
   const double m = mass[o];
-  out[p] = make_float4((float)x[o], (float)y[o], (float)z[o], (float)m);
+  const float fx = (float)x[o], fy = (float)y[o], fz = (float)z[o];
+  out[p] = make_float4(fx, fy, fz, (float)m);
   mass_out[p] = m;
+  if (posj) posj[p] = make_float4(fx, fy, fz, __uint_as_float((unsigned)p));
 }
 
 template <typename PosT>
@@ -560,10 +562,12 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
   if (compute_f32) {
     if (in32)
       k_gather_f32<float><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const float *)x, (const float *)y,
-                                                  (const float *)z, mass, (float4 *)tb.pos_sorted, tb.mass_sorted);
+                                                  (const float *)z, mass, (float4 *)tb.pos_sorted, tb.mass_sorted,
+                                                  tb.posj);
     else
       k_gather_f32<double><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const double *)x, (const double *)y,
-                                                   (const double *)z, mass, (float4 *)tb.pos_sorted, tb.mass_sorted);
+                                                   (const double *)z, mass, (float4 *)tb.pos_sorted, tb.mass_sorted,
+                                                   tb.posj);
   } else {
     if (in32)
       k_gather_f64<float><<<nblk(n), kTB, 0, s>>>(n, tb.perm, (const float *)x, (const float *)y,

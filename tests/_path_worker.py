@@ -21,6 +21,8 @@ def cases():
     n = 30000
     pos = np.concatenate([rng.normal(10.0 + 8 * b, 0.6, (n // 5, 3)) for b in range(5)])
     yield "blobs_f32_k64", np.abs(pos).astype(np.float32), rng.random(n) + 0.5, 64, None
+    # fp64 positions that are fp32 values: fp32 search, fp64 term-for-term densities
+    yield "blobs_auto_k48", np.abs(pos).astype(np.float32).astype(np.float64), rng.random(n) + 0.5, 48, None
     pos, _ = workload.single_halo(20000, 4.0, 23)
     yield "halo_f32_k128", pos.astype(np.float32), np.ones(20000), 128, None
     pos, _, _ = workload.nfw_halos(12000, 10.0, 20, seed=5)
@@ -40,7 +42,8 @@ def main():
             h, rho, _, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, periodic=True, box=box)
         else:
             want = oracle.density_pass(p64[:, 0], p64[:, 1], p64[:, 2], mass, h0, k)
-            h, rho, _, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k)
+            prec = "auto" if "_auto_" in name else None
+            h, rho, _, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, precision=prec)
         out[name] = {"h_exact": bool(np.array_equal(h, want.h)),
                      "rho_rel": float(np.max(np.abs(rho - want.rho) / want.rho)),
                      "todo_exact": bool(np.array_equal(st.todo_sizes, want.todo_sizes))}

@@ -1,12 +1,13 @@
 """Every pipeline of the library against the CPU oracle.
 
-The default pass is the per-target kernel; its fallbacks (collect instance for
-overflowed neighbour lists, walking select/density kernels) only run on a
-few targets of large inputs, so they are forced here with a small list
-capacity.  The bundle pipelines (``SPH_WARP=0``: hybrid, bundle rounds with
-recorded lists, pure walking passes) stay selectable and are checked the
-same way.  Each configuration runs in a fresh process because the pipeline
-switches are read when the library context is created.
+The default pass: seeds through the general per-target kernel, every other
+target through the known-radius kernel (sph_known.cu), whose leftovers go
+back to the general kernel.  The fallbacks (the general kernel for targets
+the known-radius kernel cannot finish, the collect instance for overflowed
+neighbour lists, the walking select/density kernels) only run on a few
+targets of large inputs, so they are forced here with margins and list
+capacities.  Each configuration runs in a fresh process because the switches
+are read when the library context is created.
 """
 import json
 import os
@@ -20,16 +21,15 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 CONFIGS = {
-    "per_target": {},
-    "per_target_small_lists": {"SPH_TLISTCAP": "1"},
+    "default": {},
+    "known_radius_off": {"SPH_KNOWN": "0"},
+    "known_radius_tight_margin": {"SPH_SEEDM": "1.0"},   # many targets with < K within R: the general kernel
+    "known_radius_wide_margin": {"SPH_SEEDM": "1.7"},    # many full lists: the general kernel
+    "known_radius_far_records": {"SPH_NEARF": "0.3"},
+    "per_target_small_lists": {"SPH_TLISTCAP": "1", "SPH_KNOWN": "0"},
     "per_target_seed_stride_8": {"SPH_SEED": "8"},
-    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
+    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48", "SPH_KNOWN": "0"},
     "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
-    "bundle_after_seeds": {"SPH_BUNDLE": "1"},
-    "hybrid_bundle_then_per_target": {"SPH_WARP": "0", "SPH_HYBRID": "1"},
-    "hybrid_small_lists": {"SPH_WARP": "0", "SPH_HYBRID": "1", "SPH_LISTCAP": "1", "SPH_TLISTCAP": "1"},
-    "bundle_rounds_with_lists": {"SPH_WARP": "0", "SPH_HYBRID": "0"},
-    "bundle_rounds_walking_select": {"SPH_WARP": "0", "SPH_HYBRID": "0", "SPH_LISTS": "0"},
 }
 
 
