@@ -81,7 +81,11 @@ struct sph_ctx {
   bool debug = false;     // SPH_DEBUG=1: fallback counters on stderr
   int seed_stride = 12;   // SPH_SEED: seed stride of the per-target pass (12 beat 6/8/16 on C1-C5, r01l; 0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
-  bool known = true;      // SPH_KNOWN=0: no known-radius kernel (the general kernel takes every non-seed target)
+  int known = 0;          // SPH_KNOWN: 0 seeds + per-target kernel (measured fastest), 2 per-cell group kernel from R0, 3 seeds + group kernel
+  int group_g = 8;        // SPH_GROUP_G: targets per group
+  int group_lcap = 0;     // SPH_GROUP_LCAP: list entries per target (0: group_list_cap(k))
+  float group_r0f = 1.35f;  // SPH_GROUP_R0F: first radius = this x the tree estimate R0
+  int group_first = 2;    // SPH_GROUP_FIRST: targets in a cell's first group (longer lists)      // SPH_KNOWN=0: no known-radius kernel (the general kernel takes every non-seed target)
   bool known_ran = false;
   cudaEvent_t kev_known[2];
   DevBuf<uint32_t> kn_list;   // targets the known-radius kernel leaves to the general kernel
@@ -600,6 +604,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   int launches = 0;
   ctx->crec_ready = false;
   ctx->n_kev = 0;
+  if (prm->n > (int64_t(1) << 27))
+    return fail(ctx, SPH_UNSUPPORTED,
+                "more than 2^27 particles on one device (list entries carry a 27-bit sorted index and a 5-bit "
+                "image shift): split the set across devices (distributed.decomposed_pass)");
   { int rc0 = ensure_common(ctx, n, max_it); if (rc0) return rc0; }
   SPH_CK(ctx->t_lo.ensure(n));
   SPH_CK(ctx->t_hi.ensure(n));
@@ -654,7 +662,25 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   bool known_run = false;
   const bool seeded = ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride;
-  if (seeded) {
+  if (compute_f32 && ctx->known == 2 && ctx->last_ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
+    // the per-cell group kernel (sph_group.cu) takes every target from the
+    // tree's radius estimate; what it leaves, the general kernel takes
+    cudaEventRecord(ctx->kev_known[0], ctx->stream);
+    PassArgs ka = a;
+    ka.posj = ctx->posj.p;
+    ka.fb_list = ctx->kn_list.p;
+    ka.fb_count = ctx->qints.p + 21;
+    ka.kn_counters = ctx->qints.p + 10;
+    launch_group(ctx->stream, ka, ctx->cellnode.p, ctx->ncell_dev.p,
+                 ctx->group_lcap > 0 ? ctx->group_lcap : group_list_cap(k), ctx->seed_margin, ctx->group_r0f,
+                 ctx->group_first, ctx->num_sms, ctx->group_g);
+    cudaEventRecord(ctx->kev_known[1], ctx->stream);
+    SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+    a.list = ctx->kn_list.p;
+    a.list_count = ctx->qints.p + 21;
+    launches += 2;
+    known_run = true;
+  } else if (seeded) {
     // seeds first (every seed_stride-th sorted position, the general kernel
     // from the tree's radius estimate), then every other target starts from
     // its neighbouring seeds' converged h (sorted neighbours are spatial
@@ -690,7 +716,24 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     // neighbour-cell lists for the radii the seeds imply
     const int cap = ctx->cell_lists;
     const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
-    if (cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
+    if (compute_f32 && ctx->known == 3 && ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
+      // the per-cell group kernel from the seeds' radii
+      cudaEventRecord(ctx->kev_known[0], ctx->stream);
+      PassArgs ka = a;
+      ka.posj = ctx->posj.p;
+      ka.fb_list = ctx->kn_list.p;
+      ka.fb_count = ctx->qints.p + 21;
+      ka.kn_counters = ctx->qints.p + 10;
+      launch_group(ctx->stream, ka, ctx->cellnode.p, ctx->ncell_dev.p,
+                   ctx->group_lcap > 0 ? ctx->group_lcap : group_list_cap(k), ctx->seed_margin, 1.0f, ctx->group_g,
+                   ctx->num_sms, ctx->group_g);
+      cudaEventRecord(ctx->kev_known[1], ctx->stream);
+      SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+      a.list = ctx->kn_list.p;
+      a.list_count = ctx->qints.p + 21;
+      launches += 2;
+      known_run = true;
+    } else if (cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
         ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
         ctx->cnear.ensure(ncell) == cudaSuccess) {
       launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
@@ -703,23 +746,6 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       a.cellidx = ctx->cellidx.p;
       a.clcap = cap;
       launches += 1;
-      if (compute_f32 && ctx->known && cap <= known_max_cells() && ctx->kn_list.ensure(n) == cudaSuccess) {
-        // the known-radius kernel (sph_known.cu); what it leaves, the general kernel takes
-        const int kv = ctx->n_kev;
-        if (kv + 2 < 64) cudaEventRecord(ctx->kev_known[0], ctx->stream);
-        PassArgs ka = a;
-        ka.posj = ctx->posj.p;
-        ka.fb_list = ctx->kn_list.p;
-        ka.fb_count = ctx->qints.p + 21;
-        ka.kn_counters = ctx->qints.p + 10;
-        launch_known(ctx->stream, ka, known_list_cap(k), ctx->num_sms);
-        cudaEventRecord(ctx->kev_known[1], ctx->stream);
-        SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-        a.list = ctx->kn_list.p;
-        a.list_count = ctx->qints.p + 21;
-        launches += 1;
-        known_run = true;
-      }
     }
     cudaGetLastError();  // an allocation failure above only skips the lists
   }
@@ -732,8 +758,14 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     int fbk[32];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(fbk, ctx->qints.p, sizeof(fbk), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[sph known] %d targets to the general kernel: image %d, list full %d, < K %d, select %d\n",
-            fbk[21], fbk[10], fbk[11], fbk[12], fbk[13]);
+    if (ctx->known >= 2)
+      fprintf(stderr, "[sph group] %d targets to the general kernel: walk overflow (groups) %d, retries %d, "
+              "retries exhausted %d, select %d; first tries from R0: few %d full %d edge %d; from the cell's h: "
+              "few %d full %d edge %d; (target, chunk) pairs %u, chunks %u, groups %u\n", fbk[21], fbk[10], fbk[11],
+              fbk[12], fbk[13], fbk[23], fbk[24], fbk[25], fbk[26], fbk[27], fbk[28], (unsigned)fbk[29],
+              (unsigned)fbk[30], (unsigned)fbk[31]);
+    else
+      fprintf(stderr, "[sph seeds] %d seeds to the general kernel\n", fbk[14]);
     fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses; %d walks\n",
             fbk[5], fbk[6], fbk[8]);
   }
@@ -930,7 +962,11 @@ int sph_ctx_create(sph_ctx **out, int device) {
   c->debug = dbg && dbg[0] == '1';
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
-  if (const char *v = getenv("SPH_KNOWN")) c->known = v[0] != '0';
+  if (const char *v = getenv("SPH_KNOWN")) c->known = atoi(v);
+  if (const char *v = getenv("SPH_GROUP_G")) c->group_g = atoi(v);
+  if (const char *v = getenv("SPH_GROUP_LCAP")) c->group_lcap = atoi(v);
+  if (const char *v = getenv("SPH_GROUP_R0F")) c->group_r0f = (float)atof(v);
+  if (const char *v = getenv("SPH_GROUP_FIRST")) c->group_first = atoi(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);

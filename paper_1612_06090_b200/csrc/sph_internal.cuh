@@ -221,11 +221,10 @@ void launch_keys_at(cudaStream_t s, int n, int precision_in, const void *x, cons
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
 void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
-// known-radius pass: cell-list cull, cp.async.bulk staging, list, select, density (sph_known.cu)
-int known_max_cells();
-int known_list_cap(int k);
-size_t known_smem_bytes(int lcap);
-void launch_known(cudaStream_t s, const PassArgs &a, int lcap, int num_sms);
+// known-radius pass, one warp per cell and its targets in groups (sph_group.cu)
+int group_list_cap(int k);
+void launch_group(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int lcap, float margin,
+                  float r0f, int first_g, int num_sms, int g);
 // fused per-target search + select + density (sph_warp.cu)
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,

@@ -66,7 +66,7 @@ template <> struct Pos<false> { using T = D4; };
 constexpr int kStack = SPH_STACK;  // traversal stack (node ids) per warp
 
 __host__ __device__ constexpr int warp_smem_bytes(int cap) {
-  return (32 + kHistRegion + cap * 8 + 2 * 32 * 4 + kStack * 4 + cap + 15) & ~15;
+  return (32 + kHistRegion + cap * 8 + 2 * 32 * 4 + kStack * 4 + 15) & ~15;
 }
 
 
@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
   int *spfx = reinterpret_cast<int *>(wbase + kHistRegion + cap * 8);
   int *sbase = spfx + 32;
   int *stk = sbase + 32;
-  uint8_t *lsh = reinterpret_cast<uint8_t *>(stk + kStack);  // image shift of each list entry
   const PT *__restrict__ pos = reinterpret_cast<const PT *>(a.pos);
   const float4 *__restrict__ nlo = a.tree.nlo;
   const float4 *__restrict__ nhi = a.tree.nhi;
@@ -239,18 +238,11 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               for (int i0 = 0; i0 < ne; i0 += 32) {
                 const int i = i0 + lane;
                 uint2 e = make_uint2(0u, kNaNf);
-                uint8_t sh = 0;
-                if (i < ne) {
-                  e = list[i];
-                  sh = lsh[i];
-                }
+                if (i < ne) e = list[i];
                 const bool keep = i < ne && __uint_as_float(e.y) <= edge;
                 const unsigned km = __ballot_sync(FULL, keep);
                 __syncwarp();
-                if (keep) {
-                  list[w + __popc(km & lt_mask)] = e;
-                  lsh[w + __popc(km & lt_mask)] = sh;
-                }
+                if (keep) list[w + __popc(km & lt_mask)] = e;
                 w += __popc(km);
                 __syncwarp();
               }
@@ -470,10 +462,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
             }
             if (!over) {
               const unsigned lm = __ballot_sync(FULL, lst);
-              if (lst) {
-                list[ne + __popc(lm & lt_mask)] = make_uint2((unsigned)j, __float_as_uint(af));
-                lsh[ne + __popc(lm & lt_mask)] = (uint8_t)sidx;
-              }
+              if (lst) list[ne + __popc(lm & lt_mask)] = make_uint2((unsigned)j | ((unsigned)sidx << 27), __float_as_uint(af));
               ne += __popc(lm);
             }
           }
@@ -592,8 +581,8 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           if (i < ne) {
             const uint2 le = list[i];
             const float af = __uint_as_float(le.y);
-            const int j = (int)le.x;
-            const int sidx = lsh[i];
+            const int j = (int)(le.x & ((1u << 27) - 1u));
+            const int sidx = (int)(le.x >> 27);
             if (!(j == p && sidx == center)) {
               if (af < lo_f) {
                 ++below;
@@ -670,7 +659,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
           const float af = __uint_as_float(le.y);
           if (!(af < d2k_f)) continue;
           ++accepted;
-          const int j = (int)le.x;
+          const int j = (int)(le.x & ((1u << 27) - 1u));
           const PT c = pos[j];
           if (f32sum) {
             if constexpr (F32) {
@@ -680,7 +669,7 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
               if (q < 1.f) accf = fmaf(c.w, wv, accf);
             }
           } else {
-            const double e = image_d2(c, (int)lsh[i]);
+            const double e = image_d2(c, (int)(le.x >> 27));
             if (e < d2k) {
               const double r_ = __dsqrt_rn(e);
               double wv;

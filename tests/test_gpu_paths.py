@@ -1,13 +1,16 @@
 """Every pipeline of the library against the CPU oracle.
 
-The default pass: seeds through the general per-target kernel, every other
-target through the known-radius kernel (sph_known.cu), whose leftovers go
-back to the general kernel.  The fallbacks (the general kernel for targets
-the known-radius kernel cannot finish, the collect instance for overflowed
-neighbour lists, the walking select/density kernels) only run on a few
-targets of large inputs, so they are forced here with margins and list
-capacities.  Each configuration runs in a fresh process because the switches
-are read when the library context is created.
+The default pass: seeds (every 12th sorted target) through the general
+per-target kernel, then neighbour-cell lists sized by the seeds' radii and
+the per-target kernel for every other target.  The alternative pipelines are
+the per-cell group kernel (sph_group.cu) started from the tree estimate
+(SPH_KNOWN=2) or from the seeds (SPH_KNOWN=3), whose leftovers go back to the
+general kernel.  The fallbacks (the collect instance for overflowed neighbour
+lists, the walking select/density kernels, the general kernel for targets the
+group kernel cannot finish) only run on a few targets of large inputs, so
+they are forced here with margins and list capacities.  Each configuration
+runs in a fresh process because the switches are read when the library
+context is created.
 """
 import json
 import os
@@ -22,13 +25,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 CONFIGS = {
     "default": {},
-    "known_radius_off": {"SPH_KNOWN": "0"},
-    "known_radius_tight_margin": {"SPH_SEEDM": "1.0"},   # many targets with < K within R: the general kernel
-    "known_radius_wide_margin": {"SPH_SEEDM": "1.7"},    # many full lists: the general kernel
-    "known_radius_far_records": {"SPH_NEARF": "0.3"},
-    "per_target_small_lists": {"SPH_TLISTCAP": "1", "SPH_KNOWN": "0"},
+    "group_from_tree_estimate": {"SPH_KNOWN": "2"},
+    "group_from_seeds": {"SPH_KNOWN": "3"},
+    "group_g8_short_lists": {"SPH_KNOWN": "2", "SPH_GROUP_G": "8", "SPH_GROUP_LCAP": "96"},  # retries, full lists
+    "group_tight_margin": {"SPH_KNOWN": "3", "SPH_SEEDM": "1.0"},   # many targets with < K within R: retries
+    "group_wide_margin": {"SPH_KNOWN": "3", "SPH_SEEDM": "1.7"},    # many full lists: retries / general kernel
+    "cell_lists_far_records": {"SPH_NEARF": "0.3"},
+    "per_target_small_lists": {"SPH_TLISTCAP": "1"},
     "per_target_seed_stride_8": {"SPH_SEED": "8"},
-    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48", "SPH_KNOWN": "0"},
+    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
     "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
 }
 
