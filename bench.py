@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ref-python", action="store_true", help="skip the reference Python/numba timing")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU sample time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default="wendland_c6", choices=("wendland_c6", "m4"))
@@ -250,6 +251,60 @@ def cpu_full(w):
             "measured_s": t, "converged_particles_per_s": n / t, "cpu_count": os.cpu_count()}
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # pip install --target baseline/_ref (offline, git-ignored)
+
+_REF_PY = r"""
+import json, os, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import sphlab
+n, k = 32768, 64
+p = sphlab.generate(sphlab.WorkloadSpec(kind=sphlab.WorkloadKind.UNIFORM_BOX, n_particles=n, box_side=1.0, seed=1),
+                    k_neighbors=k)
+p["mass"] = 1.0 / n
+p["smoothing_length"] = 2.0 * n ** (-1.0 / 3.0)       # BASELINE config 1: h0 = 2 x mean spacing
+cores = os.cpu_count() or 1
+runs = []
+for preset in ("optimised", "original"):
+    cfg = sphlab.preset_config(preset, k_neighbors=k)
+    sphlab.compute_density_pass(p.copy(), cfg, cores)  # JIT warm-up
+    for threads in sorted({1, cores}):
+        best = None
+        for _ in range(2):
+            q = p.copy()
+            t0 = time.perf_counter()
+            rho, st = sphlab.compute_density_pass(q, cfg, threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        runs.append({"preset": preset, "threads": threads, "seconds": best, "pairs_per_s": n * k / best,
+                     "iterations": int(st.iteration_count),
+                     "checksum": sphlab.bench.density_checksum(rho) if hasattr(sphlab.bench, "density_checksum") else None})
+print(json.dumps({"workload": "C1: 32,768 uniform particles (reference generate(UNIFORM_BOX, seed=1)), mass 1/N, "
+                              "h0 = 2 N^(-1/3), open boundary (the reference has no periodic mode), K = 64",
+                  "numba_version": __import__("numba").__version__, "cpu_count": cores, "runs": runs}))
+"""
+
+
+def reference_python():
+    """The reference's own Python/numba compute_density_pass (density.py:286)
+    on BASELINE config 1, presets `optimised` (fastest rung) and `original`
+    (the paper's baseline), 1 and all host threads, best of 2 after a JIT
+    warm-up (SURVEY 8d CPU baseline).  Needs the reference installed in
+    baseline/_ref; otherwise reports why it is absent."""
+    if not os.path.isdir(os.path.join(REF_PKG, "sphlab")):
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    env = dict(os.environ)
+    env.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    try:
+        r = subprocess.run([sys.executable, "-c", _REF_PY, REF_PKG], env=env, capture_output=True, text=True,
+                           timeout=900)
+        if r.returncode != 0:
+            return {"error": r.stderr.strip().splitlines()[-1:] or ["exit %d" % r.returncode]}
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001 - reported, not fatal
+        return {"error": repr(exc)}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -291,6 +346,8 @@ def run_reference(args):
         line["note"] = ("each step times a bounded random target sample of the full set (plus the full tree "
                         "build); ms_per_step is the extrapolated time of a whole pass, measured_ms_per_step the "
                         "wall time actually spent per step")
+    if not args.no_ref_python:
+        line["reference_python"] = reference_python()
     print(json.dumps(line), flush=True)
 
 
