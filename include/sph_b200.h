@@ -27,6 +27,9 @@
  *   sph_nfw_positions_device: the clustered inputs of BASELINE configs 2-5
  *                           (the reference has no such generator; it follows
  *                           the UniformBox counter pattern, workload.py:42-84)
+ *   sph_density_pass_multi <- compute_density_pass with the work split over
+ *                            devices (SURVEY 8b n_gpus; items_per_worker per
+ *                            device, density.py:407-409)
  *   sph_density_pass_device, sph_ctx_*, sph_last_error, sph_fp32_peak,
  *   sph_device_count      : device-resident form of the pass, context and
  *                           diagnostics (no reference counterpart)
@@ -130,6 +133,29 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *params,
                      double *rho, int64_t rho_stride,
                      uint8_t *flags, int64_t flags_stride,
                      sph_stats *stats);
+
+/*
+ * Multi-device pass (SURVEY 8b n_gpus / device mask; PassStats.items_per_worker
+ * of shape (iterations, devices), density.py:407-409): the call of
+ * sph_density_pass over n_ctx contexts, one per device slot (contexts from
+ * sph_ctx_create; a device may appear more than once, each slot with its own
+ * context).  Every device receives all positions, orders them and builds the
+ * search tree; device d takes the targets of its slice [n d / n_ctx,
+ * n (d + 1) / n_ctx) of the sorted (octree key) order -- contiguous key
+ * ranges, so its targets are spatially compact -- and its results are
+ * scattered into the caller's arrays by original index.  The devices run
+ * concurrently (one host thread each); no collective is needed: the only
+ * exchange is the host scatter of the results.  stats: n_ctx + 1 entries (one
+ * per slot, then the merged pass: todo_sizes summed, times the max).  Errors as
+ * sph_density_pass, message in sph_last_error(ctxs[0]); n_targets must be 0.
+ */
+int sph_density_pass_multi(sph_ctx *const *ctxs, int32_t n_ctx, const sph_params *params,
+                           const void *x, const void *y, const void *z, int64_t pos_stride,
+                           const double *mass, int64_t mass_stride,
+                           double *h, int64_t h_stride,
+                           double *rho, int64_t rho_stride,
+                           uint8_t *flags, int64_t flags_stride,
+                           sph_stats *stats);
 
 /* Same pass on DEVICE-resident contiguous arrays (inputs already in HBM). */
 int sph_density_pass_device(sph_ctx *ctx, const sph_params *params,

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "sph_morton_keys_device", "sph_decomp_pack_rows_device", "sph_decomp_gather_rows_device",
     "sph_decomp_row_keys_device", "sph_decomp_level_bounds_device", "sph_decomp_window_bounds_device",
     "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device", "sph_bbox_device", "sph_range_query",
-    "sph_nfw_positions_device",
+    "sph_nfw_positions_device", "sph_density_pass_multi",
 )
 
 
@@ -98,6 +98,8 @@ def load():
                                        vp, i64, vp, i64, ctypes.POINTER(SphStats)]
         L.sph_density_pass_device.argtypes = [vp, ctypes.POINTER(SphParams), vp, vp, vp, vp, vp, vp, vp,
                                               ctypes.POINTER(SphStats)]
+        L.sph_density_pass_multi.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(SphParams), vp, vp, vp, i64,
+                                             vp, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(SphStats)]
         L.sph_sort_perm.argtypes = [vp, i32, i64, vp, vp, vp, vp]
         L.sph_neighbor_counts.argtypes = [vp, i32, i32, ctypes.c_double, i64, vp, vp, vp, vp, vp,
                                           ctypes.POINTER(SphStats)]
@@ -169,6 +171,29 @@ def new_context(device: int = 0):
 
 
 _private = []
+_multi = {}
+
+
+def contexts(devices) -> list:
+    """One distinct context per entry of ``devices`` (a multi-device pass;
+    the same device may repeat, each repeat then gets its own private
+    context and stream, so the split is exercised on one GPU too)."""
+    out, seen = [], {}
+    for d in devices:
+        d = int(d)
+        i = seen.get(d, 0)
+        seen[d] = i + 1
+        if i == 0:
+            out.append(context(d))
+        else:
+            with _lock:
+                c = _multi.get((d, i))
+            if c is None:
+                c = new_context(d)
+                with _lock:
+                    _multi[(d, i)] = c
+            out.append(c)
+    return out
 
 
 def stream_handle(ctx) -> int:

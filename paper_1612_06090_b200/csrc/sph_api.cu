@@ -19,6 +19,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace sph;
@@ -94,6 +95,11 @@ struct sph_ctx {
   DevBuf<int> ncell_dev;    // cells of the search tree (counted with the tree, read with n_nodes)
   DevBuf<uint32_t> tlist;   // compacted target positions (ghost-aware seeding)
   int last_ncell = -1;
+  // multi-device pass: this device's targets are the sorted positions
+  // [slice_lo, slice_hi) (slice_hi < 0: every target); outputs compacted,
+  // with the original index of each in slice_orig
+  int64_t slice_lo = 0, slice_hi = -1;
+  DevBuf<int64_t> slice_orig;
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
   cudaStream_t stream2 = nullptr;  // side stream for host-to-device copies the first kernels do not need
@@ -139,9 +145,12 @@ int cuda_fail(sph_ctx *c, cudaError_t e, const char *where) {
     if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
   } while (0)
 
-__global__ void k_init_state(int n, int n_targets, const uint32_t *__restrict__ perm, uint8_t *__restrict__ state) {
+// targets: original index < n_targets and sorted position in [lo, hi) (the
+// slice of a multi-device pass); everything else is a ghost (candidate only)
+__global__ void k_init_state(int n, int n_targets, const uint32_t *__restrict__ perm, uint8_t *__restrict__ state,
+                             int lo, int hi) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) state[p] = (int)perm[p] < n_targets ? ST_NEED_HIST : ST_GHOST;
+  if (p < n) state[p] = ((int)perm[p] < n_targets && p >= lo && p < hi) ? ST_NEED_HIST : ST_GHOST;
 }
 
 __global__ void k_append_sgs(const int2 *tasks, const int *count, int4 *sgs, int base) {
@@ -219,7 +228,7 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
                            const double *__restrict__ d2k, const double *__restrict__ rho_s,
                            const double *__restrict__ h0, int max_it, double *__restrict__ h_out,
                            double *__restrict__ rho_out, uint8_t *__restrict__ flags_out, int *rounds_hist,
-                           unsigned long long *bad) {
+                           unsigned long long *bad, int lo, int hi, int64_t *__restrict__ orig_out) {
   // per-block round histogram in shared memory when it fits (kFinalizeSmemBins),
   // otherwise straight into the global one
   extern __shared__ int sh_[];
@@ -230,8 +239,12 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
   }
   __syncthreads();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n && (int)perm[p] < n_targets) {  // ghosts (original index >= n_targets) are candidates only
+  // ghosts (original index >= n_targets, or outside the device's slice) are candidates only
+  if (p < n && (int)perm[p] < n_targets && p >= lo && p < hi) {
     const uint32_t o = perm[p];
+    // slice mode: outputs compacted by sorted position, with their original index
+    const int64_t w = orig_out ? (int64_t)(p - lo) : (int64_t)o;
+    if (orig_out) orig_out[w] = o;
     const uint8_t st = state[p];
     const bool fin = st == ST_DONE || st == ST_FINAL;
     const double d = fin ? d2k[p] : INFINITY;
@@ -245,9 +258,9 @@ __global__ void k_finalize(int n, int n_targets, const uint32_t *__restrict__ pe
     const int bin = conv ? r : max_it + 1;
     atomicAdd(&sh[bin], 1);
     if (conv && d == 0.0) atomicMin(bad, (unsigned long long)o);
-    h_out[o] = __dsqrt_rn(d);
-    rho_out[o] = fin ? rho_s[p] : 0.0;
-    flags_out[o] = conv ? 0 : 1;
+    h_out[w] = __dsqrt_rn(d);
+    rho_out[w] = fin ? rho_s[p] : 0.0;
+    flags_out[w] = conv ? 0 : 1;
   }
   __syncthreads();
   if (local) {
@@ -641,7 +654,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   tm.mark(2);
   int hist_rounds = 1, band_rounds = 0;
   // ---- search, exact select and density (per-target kernels) ----
-  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p);
+  const bool sliced = ctx->slice_hi >= 0;
+  const int slo = sliced ? (int)ctx->slice_lo : 0, shi = sliced ? (int)ctx->slice_hi : n;
+  k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p, slo, shi);
   k_iota<<<nblk(n), kTB, 0, ctx->stream>>>(n, ctx->iota.p);  // run_rounds compacts from it
   SPH_CK(cudaMemsetAsync(ctx->stats.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
   SPH_CK(ctx->qints.ensure(32));
@@ -690,16 +705,17 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     PassArgs sa = a;
     sa.list = ctx->seeds.p;
     sa.list_count = ctx->qints.p + 14;
-    if (n_targets < n) {
+    if (n_targets < n || sliced) {
       // ghosts in the set: seed along the target order (compacted targets)
       SPH_CK(ctx->tlist.ensure(n));
       launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->tlist.p, ctx->qints.p + 28,
                     ctx->cub_temp.p, ctx->cub_bytes);
-      const int nst = (n_targets + ctx->seed_stride - 1) / ctx->seed_stride;
+      const int nt_eff = sliced ? shi - slo : n_targets;  // targets in the compacted list
+      const int nst = (nt_eff + ctx->seed_stride - 1) / ctx->seed_stride;
       k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
                                                            ctx->qints.p + 14);
       launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-      k_seed_radius_from<<<nblk(n_targets), kTB, 0, ctx->stream>>>(n_targets, ctx->seed_stride, ctx->tlist.p,
+      k_seed_radius_from<<<nblk(nt_eff), kTB, 0, ctx->stream>>>(nt_eff, ctx->seed_stride, ctx->tlist.p,
                                                                    ctx->state.p, ctx->d2k.p, ctx->seed_margin, rmax,
                                                                    ctx->r0.p);
       launches += 5;
@@ -808,7 +824,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     if (ctx->in_h_ready) cudaStreamWaitEvent(ctx->stream, ctx->in_h_ready, 0);  // h0 copied on the side stream
     k_finalize<<<nblk(n), kTB, max_it + 2 <= kFinalizeSmemBins ? sizeof(int) * (max_it + 2) : 0, ctx->stream>>>(
         n, n_targets, ctx->perm.p, ctx->state.p, ctx->d2k.p, ctx->rho_s.p, h0, max_it, h_out, rho_out, flags_out,
-        rounds_hist, ctx->stats.p + 2);
+        rounds_hist, ctx->stats.p + 2, slo, shi, sliced ? ctx->slice_orig.p : nullptr);
     ++launches;
     tm.mark(6);
     SPH_CK(cudaMemcpyAsync(hist.data(), rounds_hist, sizeof(int) * (max_it + 2), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1173,6 +1189,142 @@ int sph_density_pass(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     st->t_stage_ms[7] = tm.ms(0, 7);
   }
   return rc;
+}
+
+int sph_density_pass_multi(sph_ctx *const *ctxs, int32_t n_ctx, const sph_params *prm, const void *x,
+                           const void *y, const void *z, int64_t pos_stride, const double *mass, int64_t mass_stride,
+                           double *h, int64_t h_stride, double *rho, int64_t rho_stride, uint8_t *flags,
+                           int64_t flags_stride, sph_stats *stats) {
+  if (!ctxs || n_ctx < 1 || !ctxs[0]) return SPH_INVALID;
+  sph_ctx *c0 = ctxs[0];
+  for (int d = 0; d < n_ctx; ++d) {
+    if (!ctxs[d]) return fail(c0, SPH_INVALID, "null context");
+    for (int e = 0; e < d; ++e)
+      if (ctxs[e] == ctxs[d]) return fail(c0, SPH_INVALID, "each slice needs its own context");
+  }
+  int rc = validate(c0, prm);
+  if (rc) return rc;
+  if (prm->n_targets != 0 && prm->n_targets != prm->n)
+    return fail(c0, SPH_INVALID, "a multi-device pass takes every particle as a target (n_targets = 0)");
+  if (!x || !y || !z || !mass || !h || !rho || !flags) return fail(c0, SPH_INVALID, "null array pointer");
+  const int64_t n = prm->n;
+  if (n_ctx > n) n_ctx = (int32_t)n;
+  if (stats) memset(stats, 0, sizeof(sph_stats) * (n_ctx + 1));
+  struct Part {
+    int rc = SPH_OK;
+    sph_stats st{};
+    std::vector<int64_t> orig;
+    std::vector<double> h, rho;
+    std::vector<uint8_t> fl;
+  };
+  std::vector<Part> part(n_ctx);
+  auto work = [&](int d) {
+    sph_ctx *ctx = ctxs[d];
+    Part &P = part[d];
+    const int64_t lo = n * d / n_ctx, hi = n * (d + 1) / n_ctx, m = hi - lo;
+    cudaSetDevice(ctx->device);
+    ctx->err.clear();
+    P.rc = [&]() -> int {
+      // every device holds every position (the candidates) and takes the
+      // targets of its slice of the sorted (key) order
+      const size_t es = elem_size(prm->precision);
+      SPH_CK(ctx->in_x.ensure(n));
+      SPH_CK(ctx->in_y.ensure(n));
+      SPH_CK(ctx->in_z.ensure(n));
+      SPH_CK(ctx->in_m.ensure(n));
+      SPH_CK(ctx->io_h.ensure(n));
+      SPH_CK(ctx->hfix.ensure(n));
+      SPH_CK(ctx->out_rho.ensure(n));
+      SPH_CK(ctx->out_flags.ensure(n));
+      SPH_CK(ctx->slice_orig.ensure(std::max<int64_t>(m, 1)));
+      cudaStream_t s = ctx->stream;
+      SPH_CK(h2d_strided(ctx->in_x.p, x, es, pos_stride, n, s));
+      SPH_CK(h2d_strided(ctx->in_y.p, y, es, pos_stride, n, s));
+      SPH_CK(h2d_strided(ctx->in_z.p, z, es, pos_stride, n, s));
+      SPH_CK(h2d_strided(ctx->in_m.p, mass, 8, mass_stride, n, s));
+      SPH_CK(h2d_strided(ctx->hfix.p, h, 8, h_stride, n, s));
+      Timer tm{ctx};
+      tm.mark(0);
+      tm.mark(1);
+      ctx->slice_lo = lo;
+      ctx->slice_hi = hi;
+      int r = density_pass_dev(ctx, prm, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, ctx->hfix.p,
+                               ctx->io_h.p, ctx->out_rho.p, ctx->out_flags.p, &P.st, tm);
+      ctx->slice_lo = 0;
+      ctx->slice_hi = -1;
+      if (r != SPH_OK && r != SPH_DEGENERATE && r != SPH_NOT_CONVERGED) return r;
+      P.orig.resize(m);
+      P.h.resize(m);
+      P.rho.resize(m);
+      P.fl.resize(m);
+      SPH_CK(cudaMemcpyAsync(P.orig.data(), ctx->slice_orig.p, 8 * m, cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaMemcpyAsync(P.h.data(), ctx->io_h.p, 8 * m, cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaMemcpyAsync(P.rho.data(), ctx->out_rho.p, 8 * m, cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaMemcpyAsync(P.fl.data(), ctx->out_flags.p, m, cudaMemcpyDeviceToHost, s));
+      SPH_CK(cudaStreamSynchronize(s));
+      return SPH_OK;
+    }();
+  };
+  {
+    std::vector<std::thread> th;
+    for (int d = 1; d < n_ctx; ++d) th.emplace_back(work, d);
+    work(0);
+    for (auto &t : th) t.join();
+  }
+  for (int d = 0; d < n_ctx; ++d)
+    if (part[d].rc != SPH_OK) {
+      if (d) c0->err = ctxs[d]->err;
+      return part[d].rc;
+    }
+  // merged statistics: the todo trace is the sum of the slices' traces
+  sph_stats M{};
+  int64_t bad = -1, unconv = 0;
+  for (int d = 0; d < n_ctx; ++d) {
+    const sph_stats &S = part[d].st;
+    if (stats) stats[d] = S;
+    M.iterations = std::max(M.iterations, S.iterations);
+    for (int r = 0; r < SPH_MAX_TODO; ++r) M.todo_sizes[r] += S.todo_sizes[r];
+    for (int i = 0; i < 8; ++i) M.t_stage_ms[i] = std::max(M.t_stage_ms[i], S.t_stage_ms[i]);
+    for (int i = 0; i < 4; ++i) M.t_kernel_ms[i] = std::max(M.t_kernel_ms[i], S.t_kernel_ms[i]);
+    M.pair_tests += S.pair_tests;
+    M.accepted_pairs += S.accepted_pairs;
+    M.search_pair_tests += S.search_pair_tests;
+    M.gpu_launches += S.gpu_launches;
+    M.search_rounds = std::max(M.search_rounds, S.search_rounds);
+    M.select_rounds = std::max(M.select_rounds, S.select_rounds);
+    M.n_nodes = S.n_nodes;
+    if (S.bad_index >= 0 && (bad < 0 || S.bad_index < bad)) bad = S.bad_index;
+    unconv += S.unconverged;
+  }
+  M.n_todo = std::min(M.iterations, SPH_MAX_TODO);
+  M.bad_index = bad;
+  M.unconverged = unconv;
+  M.known_fallbacks = -1;
+  if (stats) stats[n_ctx] = M;
+  if (bad >= 0) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "particle %lld: %d-th nearest neighbour is at zero distance; >= %d coincident particles",
+             (long long)bad, prm->k, prm->k + 1);
+    return fail(c0, SPH_DEGENERATE, buf);
+  }
+  if (unconv) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%lld of %lld particles still flagged after %d iterations", (long long)unconv,
+             (long long)n, prm->max_iterations);
+    return fail(c0, SPH_NOT_CONVERGED, buf);
+  }
+  // results in the caller's (original) order
+  for (int d = 0; d < n_ctx; ++d) {
+    const Part &P = part[d];
+    char *hb = reinterpret_cast<char *>(h), *rb = reinterpret_cast<char *>(rho), *fb = reinterpret_cast<char *>(flags);
+    for (size_t i = 0; i < P.orig.size(); ++i) {
+      const int64_t o = P.orig[i];
+      *reinterpret_cast<double *>(hb + o * h_stride) = P.h[i];
+      *reinterpret_cast<double *>(rb + o * rho_stride) = P.rho[i];
+      *reinterpret_cast<uint8_t *>(fb + o * flags_stride) = P.fl[i];
+    }
+  }
+  return SPH_OK;
 }
 
 int sph_range_query(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,

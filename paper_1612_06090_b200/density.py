@@ -199,10 +199,36 @@ def _stats_from(st: _lib.SphStats, t_total: float) -> PassStats:
                      skipped_items=0, t_total=t_total, device=d)
 
 
+def _multi_stats(sts, t_total: float) -> PassStats:
+    """PassStats of a multi-device pass: the merged trace, items_per_worker =
+    each device's own todo trace (iterations x devices, density.py:407-409)."""
+    merged = _stats_from(sts[-1], t_total)
+    iters = merged.iteration_count
+    per = np.zeros((len(merged.todo_sizes), len(sts) - 1), dtype=np.int64)
+    for d, st in enumerate(sts[:-1]):
+        t = np.array(st.todo_sizes[:min(st.iterations, _lib.MAX_TODO)], dtype=np.int64)
+        per[:t.size, d] = t
+    merged.items_per_worker = per[:max(iters, 0)] if iters else per[:0]
+    merged.device = dict(merged.device, per_device=[_lib.SphStats.as_dict(s) for s in sts[:-1]])
+    return merged
+
+
+def _run_multi(devices, prm, x, y, z, pos_stride, m, m_stride, h, h_stride, rho, rho_stride, flags, f_stride):
+    import ctypes
+    L = _lib.load()
+    ctxs = _lib.contexts(devices)
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value if hasattr(c, "value") else c for c in ctxs])
+    sts = (_lib.SphStats * (len(ctxs) + 1))()
+    rc = L.sph_density_pass_multi(arr, len(ctxs), prm, x, y, z, pos_stride, m, m_stride, h, h_stride, rho,
+                                  rho_stride, flags, f_stride, sts)
+    return rc, ctxs[0], list(sts)
+
+
 def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_count: int = 1,
                          max_iterations: int = DEFAULT_MAX_ITERATIONS, *, precision: str = "auto",
                          periodic: bool = False, box: float | None = None,
-                         kernel: str = "wendland_c6", device: int = 0) -> tuple[np.ndarray, PassStats]:
+                         kernel: str = "wendland_c6", device: int = 0,
+                         devices=None) -> tuple[np.ndarray, PassStats]:
     """Run the density pass on the GPU over the caller's particle records.
 
     Same contract as the reference (density.py:286-413): reads positions,
@@ -215,7 +241,10 @@ def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_co
     coordinate is fp32-representable, results still bit-exact against the
     fp64 reference), "f64" or "f32"; ``periodic``/``box`` for a periodic
     cube [0, box)^3 (the reference has open boundaries only); ``kernel``
-    "wendland_c6" (the reference) or "m4".
+    "wendland_c6" (the reference) or "m4"; ``devices`` (a list of device
+    ids, repeats allowed) splits the targets over several GPUs
+    (sph_density_pass_multi): PassStats.items_per_worker then has one column
+    per device, as the reference's has one per worker thread.
     """
     n = particles.shape[0]
     if n == 0:
@@ -228,7 +257,8 @@ def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_co
     if periodic and (box is None or not box > 0.0):
         raise ValueError("periodic mode needs box > 0")
     t0 = time.perf_counter()
-    ctx = _lib.context(device)
+    multi = devices is not None and len(devices) > 1
+    ctx = _lib.context(devices[0] if devices else device)
     L = _lib.load()
 
     prm = _lib.SphParams(n=n, k=config.k_neighbors, max_iterations=max_iterations,
@@ -242,9 +272,14 @@ def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_co
         base = particles.ctypes.data
         stride = particles.dtype.itemsize
         vp = ctypes_addr
-        rc = L.sph_density_pass(ctx, prm, vp(base + 8), vp(base + 16), vp(base + 24), stride,
-                                vp(base + 32), stride, vp(base + 40), stride, vp(base + 48), stride,
-                                vp(base + 56), stride, st)
+        if multi:
+            rc, ctx, sts = _run_multi(devices, prm, vp(base + 8), vp(base + 16), vp(base + 24), stride,
+                                      vp(base + 32), stride, vp(base + 40), stride, vp(base + 48), stride,
+                                      vp(base + 56), stride)
+        else:
+            rc = L.sph_density_pass(ctx, prm, vp(base + 8), vp(base + 16), vp(base + 24), stride,
+                                    vp(base + 32), stride, vp(base + 40), stride, vp(base + 48), stride,
+                                    vp(base + 56), stride, st)
     else:
         x = np.ascontiguousarray(particles["x"], dtype=np.float64)
         y = np.ascontiguousarray(particles["y"], dtype=np.float64)
@@ -253,8 +288,12 @@ def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_co
         h = np.array(particles["smoothing_length"], dtype=np.float64)
         rho = np.zeros(n, dtype=np.float64)
         flags = np.zeros(n, dtype=np.uint8)
-        rc = L.sph_density_pass(ctx, prm, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), 8, _lib.ptr(m), 8,
-                                _lib.ptr(h), 8, _lib.ptr(rho), 8, _lib.ptr(flags), 1, st)
+        if multi:
+            rc, ctx, sts = _run_multi(devices, prm, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), 8, _lib.ptr(m), 8,
+                                      _lib.ptr(h), 8, _lib.ptr(rho), 8, _lib.ptr(flags), 1)
+        else:
+            rc = L.sph_density_pass(ctx, prm, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), 8, _lib.ptr(m), 8,
+                                    _lib.ptr(h), 8, _lib.ptr(rho), 8, _lib.ptr(flags), 1, st)
         if rc == _lib.SPH_OK:
             particles["smoothing_length"] = h
             particles["density"] = rho
@@ -262,7 +301,8 @@ def compute_density_pass(particles: np.ndarray, config: VariantConfig, thread_co
     if rc != _lib.SPH_OK:
         particles["needs_recompute"] = 1
     _raise_for(rc, ctx)
-    stats = _stats_from(st, time.perf_counter() - t0)
+    dt = time.perf_counter() - t0
+    stats = _multi_stats(sts, dt) if multi else _stats_from(st, dt)
     return np.array(particles["density"], dtype=np.float64), stats
 
 
@@ -273,7 +313,8 @@ def ctypes_addr(a: int):
 
 def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MAX_ITERATIONS, *,
                      precision: str | None = None, periodic: bool = False, box: float = 0.0,
-                     kernel: str = "wendland_c6", device: int = 0, out=None, n_targets: int | None = None):
+                     kernel: str = "wendland_c6", device: int = 0, out=None, n_targets: int | None = None,
+                     devices=None):
     """SoA form of the pass on host arrays: returns (h, rho, flags, PassStats).
 
     ``precision`` defaults to the dtype of x ("f32" for float32 inputs).
@@ -305,7 +346,10 @@ def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MA
         h = np.array(np.broadcast_to(np.asarray(h0, dtype=np.float64), (nt,)))
         rho = np.zeros(nt, dtype=np.float64)
         flags = np.zeros(nt, dtype=np.uint8)
-    ctx = _lib.context(device)
+    multi = devices is not None and len(devices) > 1
+    if multi and nt != n:
+        raise ValueError("a multi-device pass takes every particle as a target (n_targets = None)")
+    ctx = _lib.context(devices[0] if devices else device)
     L = _lib.load()
     prm = _lib.SphParams(n=n, k=k, max_iterations=max_iterations, precision=_lib.PRECISION[precision],
                          periodic=1 if periodic else 0, box=float(box), kernel=_lib.KERNELS[kernel],
@@ -313,6 +357,11 @@ def density_pass_soa(x, y, z, mass, h0, k: int, max_iterations: int = DEFAULT_MA
     st = _lib.SphStats()
     t0 = time.perf_counter()
     es = x.itemsize
+    if multi:
+        rc, ctx, sts = _run_multi(devices, prm, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), es, _lib.ptr(m), 8,
+                                  _lib.ptr(h), 8, _lib.ptr(rho), 8, _lib.ptr(flags), 1)
+        _raise_for(rc, ctx)
+        return h, rho, flags, _multi_stats(sts, time.perf_counter() - t0)
     rc = L.sph_density_pass(ctx, prm, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), es, _lib.ptr(m), 8,
                             _lib.ptr(h), 8, _lib.ptr(rho), 8, _lib.ptr(flags), 1, st)
     _raise_for(rc, ctx)
