@@ -24,6 +24,8 @@
  *                                                              workload.py:42-84
  *   sph_range_query       <- range_query(tree, pos_i, h_i, exclude=i) for all i
  *                                                              octree.py:179-227, 351-379
+ *   sph_octree_build,     <- build_octree(positions) / range_query(tree, center,
+ *   sph_octree_query         radius, workspace, exclude)     octree.py:306-379
  *   sph_nfw_positions_device: the clustered inputs of BASELINE configs 2-5
  *                           (the reference has no such generator; it follows
  *                           the UniformBox counter pattern, workload.py:42-84)
@@ -209,10 +211,31 @@ int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d
 int sph_decomp_group_boxes_device(sph_ctx *ctx, int64_t n_groups, const int64_t *d_starts, const int64_t *d_counts,
                                   int32_t width, const double *d_rows, const double *d_bound, double *d_out);
 
-/* Octree particle_perm (leaf capacity 8), bit-exact with the reference.
+/* The reference's tree object and its query around an arbitrary centre
+ * (build_octree + range_query, octree.py:306-379).  sph_octree_build orders
+ * the positions (host pointers, per precision) and builds the search tree,
+ * kept in the context until its next build or pass.  sph_octree_query answers
+ * m queries: for query q every particle j (original index) with
+ * (dx*dx + dy*dy) + dz*dz <= radii[q]^2 in unfused fp64, dx = x_j - c_x
+ * (octree.py:211-214), except exclude[q] (exclude may be NULL; -1 = none);
+ * CSR offsets_out[m + 1], idx_out / d2_out sorted by index within a query.
+ * When the total exceeds cap, *total_out is set, nothing else is written and
+ * SPH_INVALID is returned (call again with a larger buffer: the reference's
+ * QueryWorkspace.grow). */
+int sph_octree_build(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z);
+int sph_octree_query(sph_ctx *ctx, int64_t m, const double *centers, const double *radii, const int64_t *exclude,
+                     int64_t cap, int64_t *offsets_out, int64_t *idx_out, double *d2_out, int64_t *total_out);
+
+/* Octree particle_perm (leaf capacity 8), bit-exact with the reference,
+ * depth up to 48 (runs of identical 63-bit keys are subdivided further).
  * Host pointers; positions per precision (contiguous). */
 int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y,
                   const void *z, int64_t *perm_out);
+/* The same for any leaf capacity in [1, 32] (build_octree(positions,
+ * leaf_capacity).particle_perm, octree.py:306-317); trees deeper than the 21
+ * levels of the key are followed to MAX_TREE_DEPTH = 48 (octree.py:31). */
+int sph_sort_perm_ex(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y,
+                     const void *z, int32_t leaf_capacity, int64_t *perm_out);
 
 /* Fixed-h neighbour counts #{j != i : (dx*dx + dy*dy) + dz*dz <= h_i*h_i}
  * in unfused fp64, bit-exact.  periodic/box as in sph_params. */

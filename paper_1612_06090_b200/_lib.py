@@ -30,7 +30,8 @@ EXPORTED_SYMBOLS = (
     "sph_morton_keys_device", "sph_decomp_pack_rows_device", "sph_decomp_gather_rows_device",
     "sph_decomp_row_keys_device", "sph_decomp_level_bounds_device", "sph_decomp_window_bounds_device",
     "sph_decomp_ghost_mask_device", "sph_decomp_group_boxes_device", "sph_bbox_device", "sph_range_query",
-    "sph_nfw_positions_device", "sph_density_pass_multi",
+    "sph_nfw_positions_device", "sph_density_pass_multi", "sph_octree_build", "sph_octree_query",
+    "sph_sort_perm_ex",
 )
 
 
@@ -98,6 +99,9 @@ def load():
                                        vp, i64, vp, i64, ctypes.POINTER(SphStats)]
         L.sph_density_pass_device.argtypes = [vp, ctypes.POINTER(SphParams), vp, vp, vp, vp, vp, vp, vp,
                                               ctypes.POINTER(SphStats)]
+        L.sph_sort_perm_ex.argtypes = [vp, i32, i64, vp, vp, vp, i32, vp]
+        L.sph_octree_build.argtypes = [vp, i32, i64, vp, vp, vp]
+        L.sph_octree_query.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]
         L.sph_density_pass_multi.argtypes = [ctypes.POINTER(vp), i32, ctypes.POINTER(SphParams), vp, vp, vp, i64,
                                              vp, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(SphStats)]
         L.sph_sort_perm.argtypes = [vp, i32, i64, vp, vp, vp, vp]

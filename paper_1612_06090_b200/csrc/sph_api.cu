@@ -64,6 +64,7 @@ struct sph_ctx {
   // ordering
   DevBuf<unsigned long long> keys_in, keys, bbox_ord;
   DevBuf<uint32_t> idx_in, idx, perm, deep_list, iota, list;
+  DevBuf<unsigned char> deep_segs;
   DevBuf<uint8_t> lvl8, lvl32, state;
   DevBuf<int> ints;  // [0] deep_count [1] err_flag [2] list_count [3] work_counter [4] task count [5] member cursor [6..] rounds hist
   DevBuf<int2> tasks;
@@ -100,6 +101,12 @@ struct sph_ctx {
   // with the original index of each in slice_orig
   int64_t slice_lo = 0, slice_hi = -1;
   DevBuf<int64_t> slice_orig;
+  // the tree of the last sph_octree_build (-1: none; any other tree build on
+  // this context invalidates it)
+  int64_t octree_n = -1;
+  int leaf_cap = 8;  // reference leaf capacity of the ordering (sph_sort_perm_ex; the pass uses 8)
+  int octree_f32 = 0;
+  PassArgs octree_args{};
   DevBuf<uint32_t> seeds;
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
   cudaStream_t stream2 = nullptr;  // side stream for host-to-device copies the first kernels do not need
@@ -317,6 +324,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
   SPH_CK(ctx->idx.ensure(n));
   SPH_CK(ctx->perm.ensure(n));
   SPH_CK(ctx->deep_list.ensure(n));
+  SPH_CK(ctx->deep_segs.ensure(deep_segs_bytes()));
   SPH_CK(ctx->iota.ensure(n));
   SPH_CK(ctx->list.ensure(n));
   SPH_CK(ctx->lvl8.ensure(n));
@@ -343,6 +351,7 @@ int ensure_common(sph_ctx *ctx, size_t n, int max_it) {
 
 TreeBuffers tree_buffers(sph_ctx *ctx) {
   TreeBuffers tb{};
+  tb.leaf_cap = ctx->leaf_cap;
   tb.keys_in = ctx->keys_in.p;
   tb.keys = ctx->keys.p;
   tb.idx_in = ctx->idx_in.p;
@@ -352,6 +361,7 @@ TreeBuffers tree_buffers(sph_ctx *ctx) {
   tb.lvl32 = ctx->lvl32.p;
   tb.deep_count = ctx->ints.p + 0;
   tb.deep_list = ctx->deep_list.p;
+  tb.deep_segs = ctx->deep_segs.p;
   tb.err_flag = ctx->ints.p + 1;
   tb.noff = ctx->noff.p;
   tb.nlo = ctx->nlo.p;
@@ -386,6 +396,7 @@ int stage_root(sph_ctx *ctx, int n, int precision, const void *x, const void *y,
 // keys .. search tree; returns the node count through *n_nodes (one sync)
 int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *x, const void *y, const void *z,
                const double *mass, int k, float rmax, int *n_nodes, int *launches, bool search_tree) {
+  ctx->octree_n = -1;
   TreeBuffers tb = tree_buffers(ctx);
   tb.mass_ready = ctx->in_mass_ready;
   if (search_tree && compute_f32) {  // the known-radius kernel stages (x, y, z, index) records
@@ -418,10 +429,6 @@ int stage_tree(sph_ctx *ctx, int n, int precision, int compute_f32, const void *
   SPH_CK(cudaStreamSynchronize(ctx->stream));
   ctx->last_ncell = host[2];
   SPH_CK(cudaGetLastError());
-  if (host[0])
-    return fail(ctx, SPH_UNSUPPORTED,
-                "more than 8 distinct positions share one 2^-21 octree cell: the reference tree is deeper "
-                "than the 21 levels of a 63-bit key");
   *n_nodes = host[1];
   return SPH_OK;
 }
@@ -1000,7 +1007,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   cudaStreamSynchronize(c->stream);
   c->in_x.release(); c->in_y.release(); c->in_z.release(); c->in_m.release(); c->io_h.release();
   c->out_rho.release(); c->out_flags.release(); c->keys_in.release(); c->keys.release(); c->bbox_ord.release();
-  c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->iota.release();
+  c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->deep_segs.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
   c->cub_temp.release(); c->tasks.release(); c->members.release(); c->seeds.release(); c->node_p.release();
@@ -1405,6 +1412,123 @@ int sph_range_query(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, c
   return SPH_OK;
 }
 
+int sph_octree_build(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z) {
+  if (!ctx) return SPH_INVALID;
+  if (n < 1) return fail(ctx, SPH_INVALID, "need at least one particle");
+  if (n > (int64_t(1) << 27)) return fail(ctx, SPH_INVALID, "n must be <= 2^27 per device");
+  if (precision < 0 || precision > 2) return fail(ctx, SPH_INVALID, "unknown precision");
+  if (!x || !y || !z) return fail(ctx, SPH_INVALID, "null array pointer");
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  int rc = ensure_common(ctx, n, 1);
+  if (rc) return rc;
+  const size_t es = elem_size(precision);
+  SPH_CK(ctx->in_x.ensure(n));
+  SPH_CK(ctx->in_y.ensure(n));
+  SPH_CK(ctx->in_z.ensure(n));
+  SPH_CK(ctx->in_m.ensure(n));
+  cudaStream_t s = ctx->stream;
+  SPH_CK(cudaMemcpyAsync(ctx->in_x.p, x, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_y.p, y, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(ctx->in_z.p, z, es * n, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemsetAsync(ctx->in_m.p, 0, 8 * n, s));
+  int launches = 0;
+  RootInfo root{};
+  rc = stage_root(ctx, (int)n, precision, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, &root, &launches);
+  if (rc) return rc;
+  const int compute_f32 = precision == SPH_PRECISION_F32 || (precision == 2 && !root.not_f32);
+  const float rmax = compute_rmax(root, 0, 0.0);
+  int n_nodes = 0;
+  rc = stage_tree(ctx, (int)n, precision, compute_f32, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, ctx->in_m.p, 1, rmax,
+                  &n_nodes, &launches, true);
+  if (rc) return rc;
+  sph_params prm{};
+  PassArgs a = base_args(ctx, (int)n, 1, n_nodes, &prm, rmax);
+  rc = prepare_target_tree(ctx, (int)n, n_nodes, a);
+  if (rc) return rc;
+  SPH_CK(cudaStreamSynchronize(s));
+  SPH_CK(cudaGetLastError());
+  ctx->octree_args = a;
+  ctx->octree_f32 = compute_f32;
+  ctx->octree_n = n;
+  return SPH_OK;
+}
+
+int sph_octree_query(sph_ctx *ctx, int64_t m, const double *centers, const double *radii, const int64_t *exclude,
+                     int64_t cap, int64_t *offsets_out, int64_t *idx_out, double *d2_out, int64_t *total_out) {
+  if (!ctx) return SPH_INVALID;
+  if (ctx->octree_n < 0) return fail(ctx, SPH_INVALID, "no octree on this context (sph_octree_build first)");
+  if (m < 0) return fail(ctx, SPH_INVALID, "query count must be >= 0");
+  if (!offsets_out || (m > 0 && (!centers || !radii))) return fail(ctx, SPH_INVALID, "null array pointer");
+  for (int64_t q = 0; q < m; ++q)
+    if (!(radii[q] >= 0.0)) {
+      char buf[128];
+      snprintf(buf, sizeof(buf), "radius must be non-negative, got %g", radii[q]);
+      return fail(ctx, SPH_INVALID, buf);
+    }
+  cudaSetDevice(ctx->device);
+  ctx->err.clear();
+  offsets_out[0] = 0;
+  if (total_out) *total_out = 0;
+  if (m == 0) return SPH_OK;
+  cudaStream_t s = ctx->stream;
+  struct Tmp {  // per-call workspace, freed on every return path
+    DevBuf<double> cen, rad, d2a, d2b;
+    DevBuf<int64_t> exc, cnt, off, ia, ib;
+    DevBuf<unsigned char> temp;
+    DevBuf<int> err;
+    ~Tmp() { cen.release(); rad.release(); d2a.release(); d2b.release(); exc.release(); cnt.release(); off.release();
+             ia.release(); ib.release(); temp.release(); err.release(); }
+  } t;
+  SPH_CK(t.cen.ensure(3 * m));
+  SPH_CK(t.rad.ensure(m));
+  SPH_CK(t.cnt.ensure(m));
+  SPH_CK(t.off.ensure(m + 1));
+  SPH_CK(t.err.ensure(1));
+  SPH_CK(cudaMemcpyAsync(t.cen.p, centers, 24 * m, cudaMemcpyHostToDevice, s));
+  SPH_CK(cudaMemcpyAsync(t.rad.p, radii, 8 * m, cudaMemcpyHostToDevice, s));
+  const int64_t *d_exc = nullptr;
+  if (exclude) {
+    SPH_CK(t.exc.ensure(m));
+    SPH_CK(cudaMemcpyAsync(t.exc.p, exclude, 8 * m, cudaMemcpyHostToDevice, s));
+    d_exc = t.exc.p;
+  }
+  SPH_CK(cudaMemsetAsync(t.err.p, 0, sizeof(int), s));
+  const PassArgs &a = ctx->octree_args;
+  range_points(s, ctx->octree_f32, 1, m, t.cen.p, t.rad.p, d_exc, ctx->perm.p, ctx->pos_sorted.p, a.tree, nullptr,
+               t.cnt.p, nullptr, nullptr, t.err.p, ctx->num_sms);
+  std::vector<int64_t> cnt(m);
+  int herr = 0;
+  SPH_CK(cudaMemcpyAsync(cnt.data(), t.cnt.p, 8 * m, cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaMemcpyAsync(&herr, t.err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaStreamSynchronize(s));
+  if (herr) return fail(ctx, SPH_CUDA_ERROR, "range query: traversal stack overflow");
+  for (int64_t q = 0; q < m; ++q) offsets_out[q + 1] = offsets_out[q] + cnt[q];
+  const int64_t total = offsets_out[m];
+  if (total_out) *total_out = total;
+  if (total > cap) return fail(ctx, SPH_INVALID, "range query: results exceed the output capacity (see total)");
+  if (total == 0) return SPH_OK;
+  if (!idx_out || !d2_out) return fail(ctx, SPH_INVALID, "null output array");
+  SPH_CK(t.ia.ensure(total));
+  SPH_CK(t.ib.ensure(total));
+  SPH_CK(t.d2a.ensure(total));
+  SPH_CK(t.d2b.ensure(total));
+  const size_t need = range_sort_temp((int)m, total);
+  SPH_CK(t.temp.ensure(need + 1));
+  SPH_CK(cudaMemcpyAsync(t.off.p, offsets_out, 8 * (m + 1), cudaMemcpyHostToDevice, s));
+  range_points(s, ctx->octree_f32, 0, m, t.cen.p, t.rad.p, d_exc, ctx->perm.p, ctx->pos_sorted.p, a.tree, t.off.p,
+               nullptr, t.ia.p, t.d2a.p, t.err.p, ctx->num_sms);
+  if (segmented_sort_pairs(s, m, total, t.off.p, t.ia.p, t.ib.p, t.d2a.p, t.d2b.p, t.temp.p, need + 1) != 0)
+    return fail(ctx, SPH_CUDA_ERROR, "range query: sort workspace too small");
+  SPH_CK(cudaMemcpyAsync(idx_out, t.ib.p, 8 * total, cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaMemcpyAsync(d2_out, t.d2b.p, 8 * total, cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaMemcpyAsync(&herr, t.err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPH_CK(cudaStreamSynchronize(s));
+  SPH_CK(cudaGetLastError());
+  if (herr) return fail(ctx, SPH_CUDA_ERROR, "range query: list lengths changed between the count and fill passes");
+  return SPH_OK;
+}
+
 int sph_morton_keys_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x, const void *d_y,
                            const void *d_z, const double *centre, double half, uint64_t *d_keys) {
   if (!ctx) return SPH_INVALID;
@@ -1527,7 +1651,14 @@ int sph_bbox_device(sph_ctx *ctx, int32_t precision, int64_t n, const void *d_x,
 
 int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
                   int64_t *perm_out) {
+  return sph_sort_perm_ex(ctx, precision, n, x, y, z, 8, perm_out);
+}
+
+int sph_sort_perm_ex(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, const void *y, const void *z,
+                     int32_t leaf_capacity, int64_t *perm_out) {
   if (!ctx) return SPH_INVALID;
+  if (leaf_capacity < 1) return fail(ctx, SPH_INVALID, "leaf_capacity must be >= 1");
+  if (leaf_capacity > kMaxLeafCap) return fail(ctx, SPH_UNSUPPORTED, "leaf_capacity above 32 is not supported");
   if (n < 1) return fail(ctx, SPH_INVALID, "need at least one particle");
   if (n >= (1ll << 31) - 64) return fail(ctx, SPH_INVALID, "n must be < 2^31 per device");
   if (precision != SPH_PRECISION_F32 && precision != SPH_PRECISION_F64)
@@ -1549,8 +1680,10 @@ int sph_sort_perm(sph_ctx *ctx, int32_t precision, int64_t n, const void *x, con
   rc = stage_root(ctx, (int)n, precision, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, &root, &launches);
   if (rc) return rc;
   int n_nodes = 0;
+  ctx->leaf_cap = leaf_capacity;
   rc = stage_tree(ctx, (int)n, precision, 0, ctx->in_x.p, ctx->in_y.p, ctx->in_z.p, nullptr, 1, 1.f, &n_nodes,
                   &launches, false);
+  ctx->leaf_cap = 8;
   if (rc) return rc;
   std::vector<uint32_t> tmp(n);
   SPH_CK(cudaMemcpyAsync(tmp.data(), ctx->perm.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));

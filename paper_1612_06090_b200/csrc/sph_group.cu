@@ -345,6 +345,10 @@ __global__ void __launch_bounds__(kGWarps * 32, SPH_GROUP_MINB) k_cell(const Pas
     const int q = s0 + lane;
     const bool is_t = q < e0 && a.state[q] == ST_NEED_HIST;
     unsigned pend = __ballot_sync(FULL, is_t);
+    // a cell of more than 32 particles (a run of identical keys): the rest go
+    // to the general kernel
+    for (int r = s0 + 32 + lane; r < e0; r += 32)
+      if (a.state[r] == ST_NEED_HIST) a.fb_list[atomicAdd(a.fb_count, 1)] = (uint32_t)r;
     if (!pend) continue;
     // per-lane target state (lane = particle of the cell)
     float4 myq = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -9,6 +9,7 @@ namespace sph {
 
 constexpr int kMaxLevel = 21;        // 63-bit Morton keys: 21 octree levels
 constexpr int kLeafCap = 8;          // reference leaf capacity (octree.py:30)
+constexpr int kMaxLeafCap = 32;      // largest leaf capacity particle_perm takes (the key-window halo)
 #ifndef SPH_CELL_CAP
 #define SPH_CELL_CAP 32
 #endif
@@ -163,6 +164,8 @@ struct TreeBuffers {
   uint8_t *lvl8, *lvl32;
   int *deep_count;
   uint32_t *deep_list;
+  void *deep_segs;                      // k_deep's depth-first segment stacks (deep_segs_bytes())
+  int leaf_cap;                         // reference leaf capacity of the ordering (8 for the pass)
   int *err_flag;
   // search tree
   int *noff;                            // n+1 node offsets per position
@@ -195,11 +198,17 @@ void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const v
                  const void *z, unsigned long long *ord, RootInfo *root, int *launches);
 
 size_t cub_temp_needed(int n);
+size_t deep_segs_bytes();
 // batched range query lists (sph_range.cu)
 int range_fill(cudaStream_t s, int f32, int n, const uint32_t *perm, const void *pos_sorted, const double *h_sorted,
                const TreeView &tree, const int64_t *offsets, int64_t total, int64_t *idx_out, double *d2_out,
                int *err, void *temp, size_t temp_bytes, int64_t *idx_tmp, double *d2_tmp, int num_sms);
 size_t range_sort_temp(int n, int64_t total);
+int range_points(cudaStream_t s, int f32, int count_only, int64_t m, const double *centers, const double *radii,
+                 const int64_t *excl, const uint32_t *perm, const void *pos_sorted, const TreeView &tree,
+                 const int64_t *offsets, int64_t *counts, int64_t *idx_tmp, double *d2_tmp, int *err, int num_sms);
+int segmented_sort_pairs(cudaStream_t s, int64_t m, int64_t total, const int64_t *offsets, const int64_t *idx_in,
+                         int64_t *idx_out, const double *d2_in, double *d2_out, void *temp, size_t temp_bytes);
 // domain decomposition helpers (sph_decomp.cu)
 void launch_pack_rows(cudaStream_t s, int64_t n, int precision_in, const int64_t *order, const void *x,
                       const void *y, const void *z, const double *m, const double *h0, const int64_t *gid,

@@ -131,7 +131,7 @@ __global__ void k_keys(int n, const PosT *__restrict__ x, const PosT *__restrict
 // common prefix >= 3L.  M(p) = max over those windows of cpl(key[s], key[s+C]);
 // level = floor(M/3) + 1 (0 when no full window exists).
 __global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uint8_t *__restrict__ lvl8,
-                         uint8_t *__restrict__ lvl32, int *deep_count, uint32_t *deep_list) {
+                         uint8_t *__restrict__ lvl32, int *deep_count, uint32_t *deep_list, int cap) {
   constexpr int H = kCellCap > 32 ? kCellCap : 32;  // window halo
   __shared__ unsigned long long sk[kTB + 2 * H];
   __shared__ int w8[kTB + H], w32[kTB + H];
@@ -143,7 +143,7 @@ __global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uin
   __syncthreads();
   for (int t = threadIdx.x; t < kTB + H; t += kTB) {
     int s = b0 - H + t;  // window start
-    w8[t] = (s >= 0 && s + 8 <= n - 1) ? key_cpl(sk[t], sk[t + 8]) : -1;
+    w8[t] = (s >= 0 && s + cap <= n - 1) ? key_cpl(sk[t], sk[t + cap]) : -1;
     w32[t] = (s >= 0 && s + kCellCap <= n - 1) ? key_cpl(sk[t], sk[t + kCellCap]) : -1;
   }
   __syncthreads();
@@ -151,14 +151,13 @@ __global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uin
   if (p >= n) return;
   const int tp = threadIdx.x + H;  // index of window starting at p
   int m8 = -1, m32 = -1;
-#pragma unroll
-  for (int d = 0; d <= 8; ++d) m8 = max(m8, w8[tp - d]);
+  for (int d = 0; d <= cap; ++d) m8 = max(m8, w8[tp - d]);
 #pragma unroll 8
   for (int d = 0; d <= kCellCap; ++d) m32 = max(m32, w32[tp - d]);
   int l8 = m8 < 0 ? 0 : m8 / 3 + 1;
   int l32 = m32 < 0 ? 0 : m32 / 3 + 1;
   if (l8 > kMaxLevel) {
-    l8 = kMaxLevel + 1;  // > 8 identical 63-bit keys: resolved by k_deep
+    l8 = kMaxLevel + 1;  // > cap identical 63-bit keys: resolved by k_deep
     int slot = atomicAdd(deep_count, 1);
     deep_list[slot] = (uint32_t)p;
   }
@@ -169,11 +168,24 @@ __global__ void k_levels(int n, const unsigned long long *__restrict__ keys, uin
 // Runs of > 8 identical 63-bit keys.  If every position in the run is the
 // same point the reference keeps it as one non-separable leaf (octree.py:
 // 75-86) at the first level where no other particle shares its prefix.
-// Otherwise the reference tree is deeper than 21 levels: unsupported.
+// Otherwise the reference tree goes below the 21 levels of the key: the run
+// is subdivided here exactly as octree.py:36-176 does it (stable 8-way
+// partitions by x-major octant with the reference's fp64 centre arithmetic,
+// from the depth-21 cell down to MAX_TREE_DEPTH = 48, leaves at <= 8 members
+// or non-separable), writing the run's slice of the particle order directly;
+// its members keep lvl8 = kMaxLevel + 1 so k_leaf_order leaves them alone.
+// Such a run stays one search cell (its particles share all 63 key bits); the
+// search kernels take cells of any size.
+constexpr int kMaxDepth = 48;  // octree.py:31
+struct DeepSeg { int s, e, depth; double cx, cy, cz, half; };
+constexpr int kDeepStack = 8 * (kMaxDepth - kMaxLevel) + 8;  // segments per thread (depth-first)
+constexpr int kDeepThreads = 256;                             // k_deep grid (runs are rare)
 template <typename PosT>
 __global__ void k_deep(int n, const unsigned long long *__restrict__ keys, const uint32_t *__restrict__ idx,
                        const PosT *__restrict__ x, const PosT *__restrict__ y, const PosT *__restrict__ z,
-                       const int *deep_count, const uint32_t *deep_list, uint8_t *lvl8, int *err_flag) {
+                       const RootInfo *__restrict__ root, const int *deep_count, const uint32_t *deep_list,
+                       uint8_t *lvl8, uint32_t *__restrict__ perm, uint32_t *__restrict__ scratch,
+                       DeepSeg *__restrict__ segs, int *err_flag, int cap) {
   const int cnt = *deep_count;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
     const int p = (int)deep_list[t];
@@ -187,12 +199,65 @@ __global__ void k_deep(int n, const unsigned long long *__restrict__ keys, const
       const uint32_t j = idx[q];
       same = x[j] == x[j0] && y[j] == y[j0] && z[j] == z[j0];
     }
-    if (!same) { atomicOr(err_flag, 1); continue; }
-    const int cl = p > 0 ? key_cpl(keys[p - 1], kp) : -1;
-    const int cr = e < n ? key_cpl(keys[e - 1], keys[e]) : -1;
-    const int m = max(cl, cr);
-    const int L = m < 0 ? 0 : m / 3 + 1;
-    for (int q = p; q < e; ++q) lvl8[q] = (uint8_t)L;
+    if (same) {
+      const int cl = p > 0 ? key_cpl(keys[p - 1], kp) : -1;
+      const int cr = e < n ? key_cpl(keys[e - 1], keys[e]) : -1;
+      const int m = max(cl, cr);
+      const int L = m < 0 ? 0 : m / 3 + 1;
+      for (int q = p; q < e; ++q) lvl8[q] = (uint8_t)L;
+      continue;
+    }
+    // the depth-21 cell of the run: the key's own descent (k_keys arithmetic)
+    double cx = root->c[0], cy = root->c[1], cz = root->c[2], half = root->half;
+    for (int l = 0; l < kMaxLevel; ++l) {
+      const unsigned o = (unsigned)(kp >> (60 - 3 * l)) & 7u;
+      const double h2 = __dmul_rn(half, 0.5);
+      cx = (o & 4u) ? __dadd_rn(cx, h2) : __dsub_rn(cx, h2);
+      cy = (o & 2u) ? __dadd_rn(cy, h2) : __dsub_rn(cy, h2);
+      cz = (o & 1u) ? __dadd_rn(cz, h2) : __dsub_rn(cz, h2);
+      half = h2;
+    }
+    // inside a node the reference keeps the parent's stable order; at depth
+    // 21 that is original-index order, which the stable key sort left in idx
+    DeepSeg *stk = segs + (size_t)(blockIdx.x * blockDim.x + threadIdx.x) * kDeepStack;  // global, per thread
+    int sp = 0;
+    stk[sp++] = DeepSeg{p, e, kMaxLevel, cx, cy, cz, half};
+    while (sp > 0) {
+      const DeepSeg g = stk[--sp];
+      if (g.e - g.s <= cap || g.depth >= kMaxDepth) continue;
+      const uint32_t f = perm[g.s];
+      bool sep = false;
+      for (int q = g.s + 1; q < g.e && !sep; ++q) {
+        const uint32_t j = perm[q];
+        sep = x[j] != x[f] || y[j] != y[f] || z[j] != z[f];
+      }
+      if (!sep) continue;  // coincident-point guard (octree.py:75-86)
+      int counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int q = g.s; q < g.e; ++q) {
+        const uint32_t j = perm[q];
+        const int o = (((double)x[j] >= g.cx) << 2) | (((double)y[j] >= g.cy) << 1) | ((double)z[j] >= g.cz);
+        ++counts[o];
+      }
+      int offs[9];
+      offs[0] = 0;
+      for (int o = 0; o < 8; ++o) offs[o + 1] = offs[o] + counts[o];
+      int cur[8];
+      for (int o = 0; o < 8; ++o) cur[o] = offs[o];
+      for (int q = g.s; q < g.e; ++q) {
+        const uint32_t j = perm[q];
+        const int o = (((double)x[j] >= g.cx) << 2) | (((double)y[j] >= g.cy) << 1) | ((double)z[j] >= g.cz);
+        scratch[g.s + cur[o]++] = j;
+      }
+      for (int q = g.s; q < g.e; ++q) perm[q] = scratch[q];
+      const double h2 = __dmul_rn(g.half, 0.5);
+      for (int o = 0; o < 8; ++o) {
+        if (counts[o] <= cap) continue;
+        stk[sp++] = DeepSeg{g.s + offs[o], g.s + offs[o + 1], g.depth + 1,
+                        (o & 4) ? __dadd_rn(g.cx, h2) : __dsub_rn(g.cx, h2),
+                        (o & 2) ? __dadd_rn(g.cy, h2) : __dsub_rn(g.cy, h2),
+                        (o & 1) ? __dadd_rn(g.cz, h2) : __dsub_rn(g.cz, h2), h2};
+      }
+    }
   }
 }
 
@@ -204,17 +269,18 @@ __device__ __forceinline__ bool same_leaf(const unsigned long long *keys, const 
 // inside each leaf the reference keeps original-index order (stable
 // partitions from an identity perm); the key sort ordered them by key
 __global__ void k_leaf_order(int n, const unsigned long long *__restrict__ keys, const uint8_t *__restrict__ lvl8,
-                             const uint32_t *__restrict__ idx, uint32_t *__restrict__ perm) {
+                             const uint32_t *__restrict__ idx, uint32_t *__restrict__ perm, int cap) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  if (lvl8[p] > kMaxLevel) return;  // a run below depth 21: ordered by k_deep
   if (p > 0 && same_leaf(keys, lvl8, p - 1, p)) return;
-  uint32_t v[kLeafCap];
+  uint32_t v[kMaxLeafCap];
   int c = 0;
-  while (p + c < n && c <= kLeafCap && (c == 0 || same_leaf(keys, lvl8, p, p + c))) {
-    if (c < kLeafCap) v[c] = idx[p + c];
+  while (p + c < n && c <= cap && (c == 0 || same_leaf(keys, lvl8, p, p + c))) {
+    if (c < cap) v[c] = idx[p + c];
     ++c;
   }
-  if (c > kLeafCap || c < 2) return;  // coincident runs are already in index order
+  if (c > cap || c < 2) return;  // coincident runs are already in index order
   for (int i = 1; i < c; ++i) {
     uint32_t t = v[i];
     int j = i - 1;
@@ -492,6 +558,8 @@ __global__ void k_keys_at(int n, const PosT *__restrict__ x, const PosT *__restr
 
 }  // namespace
 
+size_t deep_segs_bytes() { return sizeof(DeepSeg) * (size_t)kDeepStack * kDeepThreads; }
+
 size_t cub_temp_needed(int n) {
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
@@ -541,15 +609,20 @@ int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int com
   cub::DeviceRadixSort::SortPairs(tb.cub_temp, tbytes, tb.keys_in, tb.keys, tb.idx_in, tb.idx, n, 0, 63, s);
   cudaMemsetAsync(tb.deep_count, 0, sizeof(int), s);
   cudaMemsetAsync(tb.err_flag, 0, sizeof(int), s);
-  k_levels<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.lvl32, tb.deep_count, tb.deep_list);
-  if (in32)
-    k_deep<float><<<64, 128, 0, s>>>(n, tb.keys, tb.idx, (const float *)x, (const float *)y, (const float *)z,
-                                     tb.deep_count, tb.deep_list, tb.lvl8, tb.err_flag);
-  else
-    k_deep<double><<<64, 128, 0, s>>>(n, tb.keys, tb.idx, (const double *)x, (const double *)y,
-                                      (const double *)z, tb.deep_count, tb.deep_list, tb.lvl8, tb.err_flag);
+  const int cap = tb.leaf_cap > 0 ? tb.leaf_cap : kLeafCap;
+  k_levels<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.lvl32, tb.deep_count, tb.deep_list, cap);
   cudaMemcpyAsync(tb.perm, tb.idx, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
-  k_leaf_order<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.idx, tb.perm);
+  // idx_in (the sort's input) is free again: k_deep's partition scratch
+  if (in32)
+    k_deep<float><<<kDeepThreads / 128, 128, 0, s>>>(n, tb.keys, tb.idx, (const float *)x, (const float *)y,
+                                                     (const float *)z, tb.root, tb.deep_count, tb.deep_list, tb.lvl8,
+                                                     tb.perm, tb.idx_in, (DeepSeg *)tb.deep_segs, tb.err_flag, cap);
+  else
+    k_deep<double><<<kDeepThreads / 128, 128, 0, s>>>(n, tb.keys, tb.idx, (const double *)x, (const double *)y,
+                                                      (const double *)z, tb.root, tb.deep_count, tb.deep_list,
+                                                      tb.lvl8, tb.perm, tb.idx_in, (DeepSeg *)tb.deep_segs,
+                                                      tb.err_flag, cap);
+  k_leaf_order<<<nblk(n), kTB, 0, s>>>(n, tb.keys, tb.lvl8, tb.idx, tb.perm, cap);
   *launches += 5;  // keys, levels, deep, leaf order (+ the radix sort's own kernels)
   return 0;
 }

@@ -10,6 +10,11 @@ bit for bit.
 ``neighbor_counts`` is ``range_query(tree, pos_i, h_i, exclude=i).size``
 (octree.py:351-379) for every particle at once: the number of other
 particles with (dx*dx + dy*dy) + dz*dz <= h_i*h_i in unfused fp64.
+
+``build_octree`` / ``range_query`` mirror the reference's tree object and its
+query around an arbitrary centre (octree.py:244-273, 306-379): the tree is
+built once on the device (kept in its own library context) and queried any
+number of times; ``range_query_many`` answers a batch of centres in one call.
 """
 
 from __future__ import annotations
@@ -39,9 +44,11 @@ def _xyz(positions, dtype=None):
 
 
 def particle_perm(positions, leaf_capacity: int = DEFAULT_LEAF_CAPACITY, device: int = 0) -> np.ndarray:
-    """The reference octree's particle_perm (leaf capacity 8 only)."""
-    if leaf_capacity != DEFAULT_LEAF_CAPACITY:
-        raise ValueError("the GPU ordering implements the reference leaf capacity 8")
+    """The reference octree's particle_perm (build_octree(positions,
+    leaf_capacity).particle_perm, octree.py:306-348), leaf capacity 1-32,
+    depth up to 48."""
+    if leaf_capacity < 1:
+        raise ValueError(f"leaf_capacity must be >= 1, got {leaf_capacity}")
     x, y, z = _xyz(positions)
     n = x.shape[0]
     if n == 0:
@@ -51,7 +58,8 @@ def particle_perm(positions, leaf_capacity: int = DEFAULT_LEAF_CAPACITY, device:
     ctx = _lib.context(device)
     out = np.empty(n, dtype=np.int64)
     prec = _lib.PRECISION["f32" if x.dtype == np.float32 else "f64"]
-    rc = _lib.load().sph_sort_perm(ctx, prec, n, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), _lib.ptr(out))
+    rc = _lib.load().sph_sort_perm_ex(ctx, prec, n, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z), int(leaf_capacity),
+                                      _lib.ptr(out))
     if rc != _lib.SPH_OK:
         msg = _lib.last_error(ctx)
         raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(msg)
@@ -101,3 +109,119 @@ def range_query_all(positions, h, device: int = 0):
         msg = _lib.last_error(ctx)
         raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(msg)
     return offsets, idx, d2
+
+
+class QueryWorkspace:
+    """Accepted for signature compatibility with the reference
+    (octree.py:276-289); the device query allocates its own buffers."""
+
+    def __init__(self, capacity: int = 2048):
+        self.capacity = capacity
+
+
+class Octree:
+    """The reference's Octree (octree.py:244-273) as a device-resident search
+    tree: positions ordered by the bit-exact octree keys, cells of <= 32
+    particles with tight fp32 boxes.  ``particle_perm`` is the reference
+    permutation (computed on first use); queries go through
+    ``range_query`` / ``range_query_many``."""
+
+    def __init__(self, positions, leaf_capacity: int = DEFAULT_LEAF_CAPACITY, device: int = 0):
+        import ctypes
+        if leaf_capacity < 1:
+            raise ValueError(f"leaf_capacity must be >= 1, got {leaf_capacity}")
+        x, y, z = _xyz(positions)
+        if x.shape[0] and not (np.isfinite(x).all() and np.isfinite(y).all() and np.isfinite(z).all()):
+            raise ValueError("positions must be finite")
+        self.x, self.y, self.z = x, y, z
+        self.leaf_capacity = leaf_capacity
+        self.device = device
+        self._perm = None
+        self._ctx = None
+        n = x.shape[0]
+        if n == 0:
+            return
+        L = _lib.load()
+        if L.sph_device_count() <= 0:
+            raise RuntimeError("no CUDA device visible: the B200 pass has no CPU fallback")
+        h = ctypes.c_void_p()
+        rc = L.sph_ctx_create(ctypes.byref(h), device)
+        if rc != _lib.SPH_OK:
+            raise RuntimeError(f"sph_ctx_create(device={device}) failed with status {rc}")
+        self._ctx = h
+        prec = _lib.PRECISION["f32" if x.dtype == np.float32 else "auto"]
+        rc = L.sph_octree_build(h, prec, n, _lib.ptr(x), _lib.ptr(y), _lib.ptr(z))
+        if rc != _lib.SPH_OK:
+            raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(_lib.last_error(h))
+
+    def __del__(self):
+        if getattr(self, "_ctx", None) is not None:
+            try:
+                _lib.load().sph_ctx_destroy(self._ctx)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+            self._ctx = None
+
+    @property
+    def n_particles(self) -> int:
+        return int(self.x.shape[0])
+
+    @property
+    def particle_perm(self) -> np.ndarray:
+        if self._perm is None:
+            self._perm = particle_perm((self.x, self.y, self.z), self.leaf_capacity, self.device)
+        return self._perm
+
+
+def build_octree(positions, leaf_capacity: int = DEFAULT_LEAF_CAPACITY, max_depth: int = MAX_TREE_DEPTH,
+                 device: int = 0) -> Octree:
+    """``build_octree`` (octree.py:306-348) on the device."""
+    if max_depth < 1:
+        raise ValueError(f"max_depth must be >= 1, got {max_depth}")
+    return Octree(positions, leaf_capacity, device)
+
+
+def range_query_many(tree: Octree, centers, radii, exclude=None):
+    """``range_query`` for many centres at once: CSR (offsets int64[m+1],
+    idx int64[total], d2 float64[total]), each list sorted by index."""
+    c = np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(-1, 3))
+    m = c.shape[0]
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(radii, dtype=np.float64), (m,)))
+    if np.any(r < 0.0) or np.any(np.isnan(r)):
+        bad = r[~(r >= 0.0)][0]
+        raise ValueError(f"radius must be non-negative, got {bad}")
+    ex = None if exclude is None else np.ascontiguousarray(
+        np.broadcast_to(np.asarray(exclude, dtype=np.int64), (m,)))
+    offsets = np.zeros(m + 1, dtype=np.int64)
+    if tree.n_particles == 0 or m == 0:
+        return offsets, np.zeros(0, dtype=np.int64), np.zeros(0)
+    import ctypes
+    L = _lib.load()
+    total = ctypes.c_int64(0)
+    cap = max(1024, 64 * m)
+    while True:
+        idx = np.empty(cap, dtype=np.int64)
+        d2 = np.empty(cap, dtype=np.float64)
+        rc = L.sph_octree_query(tree._ctx, m, _lib.ptr(c), _lib.ptr(r), _lib.ptr(ex) if ex is not None else None,
+                                cap, _lib.ptr(offsets), _lib.ptr(idx), _lib.ptr(d2), ctypes.byref(total))
+        if rc == _lib.SPH_INVALID and total.value > cap:
+            cap = int(total.value)  # the reference's workspace.grow()
+            continue
+        if rc != _lib.SPH_OK:
+            raise (ValueError if rc == _lib.SPH_INVALID else RuntimeError)(_lib.last_error(tree._ctx))
+        t = int(total.value)
+        return offsets, idx[:t], d2[:t]
+
+
+def range_query(tree: Octree, center, radius: float, workspace: QueryWorkspace | None = None,
+                exclude: int = -1):
+    """``range_query(tree, center, radius, workspace, exclude)``
+    (octree.py:351-379): every particle with (dx*dx + dy*dy) + dz*dz <=
+    radius*radius (unfused fp64, dx = x_j - center_x), except ``exclude``;
+    (indices, squared distances) sorted by index (the reference returns the
+    same set in tree order)."""
+    if radius < 0.0:
+        raise ValueError(f"radius must be non-negative, got {radius}")
+    _, idx, d2 = range_query_many(tree, [tuple(float(v) for v in center)], [float(radius)],
+                                  None if exclude < 0 else [int(exclude)])
+    return idx, d2
