@@ -159,6 +159,15 @@ def context(device: int = 0):
         return c
 
 
+def drop_context(device: int = 0) -> None:
+    """Destroy the cached per-device context (frees its device buffers; the
+    next call on the device creates a fresh one)."""
+    with _lock:
+        c = _ctx.pop(device, None)
+    if c is not None:
+        load().sph_ctx_destroy(c)
+
+
 def new_context(device: int = 0):
     """A private context (its own stream and buffers), e.g. one per in-process
     rank of an emulated decomposition; never destroyed before exit."""

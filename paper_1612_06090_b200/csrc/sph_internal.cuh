@@ -198,6 +198,10 @@ void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const v
                  const void *z, unsigned long long *ord, RootInfo *root, int *launches);
 
 size_t cub_temp_needed(int n);
+// stable radix sort of the 63-bit keys with their indices (sph_sort.cu): a -> b
+size_t radix_sort_temp_bytes(int n);
+void radix_sort_pairs(cudaStream_t s, int n, unsigned long long *keys_a, uint32_t *vals_a, unsigned long long *keys_b,
+                      uint32_t *vals_b, void *temp);
 size_t deep_segs_bytes();
 // batched range query lists (sph_range.cu)
 int range_fill(cudaStream_t s, int f32, int n, const uint32_t *perm, const void *pos_sorted, const double *h_sorted,

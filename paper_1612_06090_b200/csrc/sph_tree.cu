@@ -561,10 +561,9 @@ __global__ void k_keys_at(int n, const PosT *__restrict__ x, const PosT *__restr
 size_t deep_segs_bytes() { return sizeof(DeepSeg) * (size_t)kDeepStack * kDeepThreads; }
 
 size_t cub_temp_needed(int n) {
-  size_t a = 0, b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                  (uint32_t *)nullptr, (uint32_t *)nullptr, n, 0, 63);
+  size_t b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, n + 1);
+  const size_t a = radix_sort_temp_bytes(n);
   return a > b ? a : b;
 }
 
@@ -606,7 +605,9 @@ int tree_build(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, int com
     k_keys<double><<<nblk(n), kTB, 0, s>>>(n, (const double *)x, (const double *)y, (const double *)z, tb.root,
                                            tb.keys_in, tb.idx_in);
   size_t tbytes = tb.cub_temp_bytes;
-  cub::DeviceRadixSort::SortPairs(tb.cub_temp, tbytes, tb.keys_in, tb.keys, tb.idx_in, tb.idx, n, 0, 63, s);
+  // stable LSD radix sort of (key, original index), hand-written onesweep (sph_sort.cu)
+  radix_sort_pairs(s, n, tb.keys_in, tb.idx_in, tb.keys, tb.idx, tb.cub_temp);
+  (void)tbytes;
   cudaMemsetAsync(tb.deep_count, 0, sizeof(int), s);
   cudaMemsetAsync(tb.err_flag, 0, sizeof(int), s);
   const int cap = tb.leaf_cap > 0 ? tb.leaf_cap : kLeafCap;

@@ -43,6 +43,10 @@ def main():
     h_ref, rho_ref, _, st = density_pass_soa(pos32[:, 0], pos32[:, 1], pos32[:, 2], w["mass"], w["h0"], k,
                                              periodic=True, box=box)
     t_single = st.device["t_stage_ms"]["total"]
+    # the whole-set context is large (C4: ~40 GB): free it before the ranks build theirs
+    from paper_1612_06090_b200 import _lib
+    _lib.drop_context(0)
+    torch.cuda.empty_cache()
 
     W = D.ThreadWorld(world)
     out, comps, errs = [None] * world, [None] * world, []
