@@ -200,6 +200,11 @@ void launch_bbox(cudaStream_t s, int n, int precision_in, const void *x, const v
 size_t cub_temp_needed(int n);
 // stable radix sort of the 63-bit keys with their indices (sph_sort.cu): a -> b
 size_t radix_sort_temp_bytes(int n);
+// single-pass exclusive scan / order-preserving select by state (sph_scan.cu)
+size_t scan_temp_bytes(int n);
+void scan_exclusive_i32(cudaStream_t s, const int *in, int *out, int n, void *temp);
+void select_state(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
+                  uint32_t *list_out, int *count_out, void *temp);
 void radix_sort_pairs(cudaStream_t s, int n, unsigned long long *keys_a, uint32_t *vals_a, unsigned long long *keys_b,
                       uint32_t *vals_b, void *temp);
 size_t deep_segs_bytes();

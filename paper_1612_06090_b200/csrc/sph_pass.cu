@@ -25,7 +25,6 @@
 // d^2 are exactly the reference's fp64 results.
 #include "sph_internal.cuh"
 
-#include <cub/cub.cuh>
 
 #include <algorithm>
 
@@ -843,12 +842,6 @@ void launch_one(cudaStream_t s, const PassArgs &a, int num_sms) {
   k_pass<MODE, F32><<<num_sms * blocks_per_sm, kWarps * 32, smem, s>>>(a);
 }
 
-struct StateIs {
-  const uint8_t *state;
-  uint8_t want;
-  __device__ __forceinline__ bool operator()(const uint32_t &p) const { return state[p] == want; }
-};
-
 }  // namespace
 
 template <int MODE, bool F32>
@@ -883,18 +876,13 @@ void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count
 #undef SPH_PASS_CASE
 }
 
-size_t select_temp_needed(int n) {
-  size_t b = 0;
-  StateIs op{nullptr, 0};
-  cub::DeviceSelect::If(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int *)nullptr, n, op);
-  return b;
-}
+size_t select_temp_needed(int n) { return scan_temp_bytes(n); }
 
-// list_out = [p in list_in : state[p] == want], order preserved
+// list_out = [p in list_in : state[p] == want], order preserved (sph_scan.cu)
 void launch_select(cudaStream_t s, const uint32_t *list_in, int n_in, const uint8_t *state, uint8_t want,
                    uint32_t *list_out, int *count_out, void *temp, size_t temp_bytes) {
-  StateIs op{state, want};
-  cub::DeviceSelect::If(temp, temp_bytes, list_in, list_out, count_out, n_in, op, s);
+  (void)temp_bytes;
+  select_state(s, list_in, n_in, state, want, list_out, count_out, temp);
 }
 
 }  // namespace sph

@@ -15,7 +15,6 @@
 //     padded octree cubes
 #include "sph_internal.cuh"
 
-#include <cub/cub.cuh>
 
 namespace sph {
 
@@ -560,10 +559,8 @@ __global__ void k_keys_at(int n, const PosT *__restrict__ x, const PosT *__restr
 
 size_t deep_segs_bytes() { return sizeof(DeepSeg) * (size_t)kDeepStack * kDeepThreads; }
 
-size_t cub_temp_needed(int n) {
-  size_t b = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, n + 1);
-  const size_t a = radix_sort_temp_bytes(n);
+size_t cub_temp_needed(int n) {  // the sort's and the scan's workspace (no library kernels)
+  const size_t a = radix_sort_temp_bytes(n), b = scan_temp_bytes(n + 1);
   return a > b ? a : b;
 }
 
@@ -651,8 +648,7 @@ int tree_build_search(cudaStream_t s, TreeBuffers &tb, int n, int precision_in, 
                                                    (const double *)z, mass, (D4 *)tb.pos_sorted);
   }
   k_node_count<<<nblk(n + 1), kTB, 0, s>>>(n, tb.keys, tb.lvl32, tb.noff);
-  size_t tbytes = tb.cub_temp_bytes;
-  cub::DeviceScan::ExclusiveSum(tb.cub_temp, tbytes, tb.noff, tb.noff, n + 1, s);
+  scan_exclusive_i32(s, tb.noff, tb.noff, n + 1, tb.cub_temp);  // node offsets (sph_scan.cu)
   if (!tb.emit_r0 && tb.node_p) {
     k_node_owner<<<nblk(n), kTB, 0, s>>>(n, tb.noff, tb.node_p);
     const int max_nodes = 2 * n + 64;
