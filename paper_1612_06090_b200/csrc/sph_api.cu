@@ -467,6 +467,7 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.stats = ctx->stats.p;
   a.periodic = prm ? prm->periodic : 0;
   a.box = prm ? prm->box : 0.0;
+  a.box_lo = (float)(a.box - (double)(float)a.box);  // second word of the fp32 image arithmetic
   a.rmax = rmax;
   a.dbg = nullptr;
   a.sub_d = 2.0f;  // walking fallback passes: task extent in units of the leader's radius

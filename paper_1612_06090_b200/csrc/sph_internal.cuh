@@ -124,6 +124,7 @@ struct PassArgs {
   unsigned long long *stats;  // [0] pair tests, [1] accepted pairs
   int periodic;
   double box;
+  float box_lo;             // box - (float)box: the fp32 image arithmetic's second word
   float rmax;               // largest meaningful search radius
   unsigned long long *dbg;  // optional per-bundle diagnostics (4 words per bundle) or nullptr
   float sub_d;              // task grouping: Chebyshev radius in units of the leader's radius

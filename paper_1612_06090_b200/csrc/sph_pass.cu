@@ -281,11 +281,15 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
           qlz = __double2float_rd((double)bz0 - sz * bxs); qhz = __double2float_ru((double)bz1 - sz * bxs);
           if (box_gap2(nlo[0], nhi[0], qlx, qly, qlz, qhx, qhy, qhz) > R2b) continue;
         }
-        // fp32 image arithmetic: x_j - box is exact when it matters (Sterbenz);
-        // for a +box shift the target moves instead: x_i - box
         const float boxf = (float)a.box;
-        const float csx = sx < 0 ? -boxf : 0.f, csy = sy < 0 ? -boxf : 0.f, csz = sz < 0 ? -boxf : 0.f;
-        const float tfx = sx > 0 ? fx - boxf : fx, tfy = sy > 0 ? fy - boxf : fy, tfz = sz > 0 ? fz - boxf : fz;
+        // image offsets with the box side in two fp32 words, box = hi + lo (see
+        // k_target): -1 shift: candidate - hi (exact), target + lo; +1 shift:
+        // the target moves, (x_i - hi) - lo
+        const float bxh = boxf, bxl = (float)(a.box - (double)boxf);
+        const float csx = sx < 0 ? -bxh : 0.f, csy = sy < 0 ? -bxh : 0.f, csz = sz < 0 ? -bxh : 0.f;
+        const float tfx = sx < 0 ? fx + bxl : sx > 0 ? (fx - bxh) - bxl : fx,
+                    tfy = sy < 0 ? fy + bxl : sy > 0 ? (fy - bxh) - bxl : fy,
+                    tfz = sz < 0 ? fz + bxl : sz > 0 ? (fz - bxh) - bxl : fz;
         const double dsx = sx * a.box, dsy = sy * a.box, dsz = sz * a.box;
         // this lane's target in the tree frame of the shift (x_i - s*box), plus slack
         const float pqx = shifted ? (float)(tx - dsx) : fx, pqy = shifted ? (float)(ty - dsy) : fy,
@@ -507,6 +511,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                 if constexpr (F32) {
                   float dx, dy, dz;
                   if (shifted) {
+                    // box side in two fp32 words (see k_target): within the guard band
                     dx = (c.x + csx) - tfx; dy = (c.y + csy) - tfy; dz = (c.z + csz) - tfz;
                   } else {
                     dx = c.x - fx; dy = c.y - fy; dz = c.z - fz;

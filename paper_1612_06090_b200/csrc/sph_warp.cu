@@ -294,13 +294,21 @@ __global__ void __launch_bounds__(kWarps * 32, SPH_TARGET_MINB) k_target(const P
         const float pqx = sx ? (float)(tx - dsx) : fx, pqy = sy ? (float)(ty - dsy) : fy,
                     pqz = sz ? (float)(tz - dsz) : fz;
         const float pslack = shifted ? boxf * 4.8e-7f : slack0;
-        // fp32 image arithmetic: x_j - box exact when it matters (Sterbenz); for a
-        // +box shift the target moves instead (x_i - box)
-        // kept in shared memory: the candidate loop reads them instead of
-        // re-deriving them from the shift under register pressure
         if (lane == 0) {
+          // fp32 image arithmetic with the box side in two words, box = hi + lo
+          // (C3's side is no fp32 value): for a -1 shift the candidate moves by
+          // -hi (exact: Sterbenz, the hit candidates sit within R of the face)
+          // and the target takes the lo word, x_i + lo; for a +1 shift the
+          // target moves, (x_i - hi) - lo; unshifted, x_i - 0.  Each adds one
+          // rounding at the scale of the target's distance to the face (< R),
+          // so the fp32 d2 stays within 2 (R / d) 2^-24 of the exact
+          // image-augmented value: inside the 2^-20 guard band of the exact
+          // recheck.  (Written branch-free: the hot loop's register allocation
+          // is sensitive to this block.)
+          const float bl = a.box_lo;
           simg[0] = make_float4(sx < 0 ? -boxf : 0.f, sy < 0 ? -boxf : 0.f, sz < 0 ? -boxf : 0.f, 0.f);
-          simg[1] = make_float4(sx > 0 ? fx - boxf : fx, sy > 0 ? fy - boxf : fy, sz > 0 ? fz - boxf : fz, 0.f);
+          simg[1] = make_float4((sx > 0 ? fx - boxf : fx) - (float)sx * bl, (sy > 0 ? fy - boxf : fy) - (float)sy * bl,
+                                (sz > 0 ? fz - boxf : fz) - (float)sz * bl, 0.f);
         }
         __syncwarp();
 

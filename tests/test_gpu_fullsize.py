@@ -52,9 +52,10 @@ def _todo_from_h(h, h0, max_it=100):
     return todo
 
 
-def _sampled(w, p32, h, rho, n_sample, seed):
+def _sampled(w, p32, h, rho, n_sample, seed, targets=None):
     n, k, box = p32.shape[0], int(w["k"]), float(w["box"])
-    tg = np.sort(np.random.default_rng(seed).choice(n, size=n_sample, replace=False))
+    tg = (np.sort(np.random.default_rng(seed).choice(n, size=n_sample, replace=False)) if targets is None
+          else np.sort(targets))
     margin = 1.05 * float(h[tg].max()) + 1e-9
     xs, ys, zs = (p32[:, a] for a in range(3))
     sel = oracle.periodic_crop(xs, ys, zs, box, tg, margin)
@@ -145,3 +146,22 @@ def test_device_generator_matches_host_restatement():
     assert np.all((diff <= 4 * ulp) | wrapped)
     assert float(np.mean(diff == 0)) > 0.99
     assert int(wrapped.sum()) <= 2
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_periodic_boundary_targets_full_size(cfg):
+    """Targets whose search sphere crosses a face of the periodic box (their
+    candidates include images; C3's box side, 100 * 16^(1/3), is not an fp32
+    value, so the image offsets must be applied in fp64 to keep the fp32
+    guard band)."""
+    w = workload.config_device(cfg)
+    p32 = _host32(w)
+    n, k, box = p32.shape[0], int(w["k"]), float(w["box"])
+    h, rho, flags, st = sph.density_pass_soa(p32[:, 0], p32[:, 1], p32[:, 2], w["mass"], w["h0"], k,
+                                             periodic=True, box=box)
+    p64 = p32.astype(np.float64)
+    gap = np.minimum(p64, box - p64).min(axis=1)
+    near = np.nonzero(gap < h)[0]
+    assert near.size > 1000
+    tg = np.random.default_rng(cfg).choice(near, size=min(near.size, 3000), replace=False)
+    _sampled(w, p32, h, rho, 0, 0, targets=tg)
