@@ -13,6 +13,8 @@
 #include "sph_internal.cuh"
 #include "../../include/sph_b200.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: host ranges around the pass stages (nsys / ncu --nvtx)
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -305,6 +307,24 @@ __global__ void __launch_bounds__(256) k_ffma_probe(float *out, int iters) {
   for (int j = 0; j < 16; ++j) s += x[j];
   if (s == 1234.5f) out[0] = s;
 }
+
+// scoped NVTX range (no-op unless a tool is attached)
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx &) = delete;
+  Nvtx &operator=(const Nvtx &) = delete;
+};
+// an NVTX range that may end before its scope does
+struct NvtxSpan {
+  bool on = true;
+  explicit NvtxSpan(const char *name) { nvtxRangePushA(name); }
+  void end() {
+    if (on) nvtxRangePop();
+    on = false;
+  }
+  ~NvtxSpan() { end(); }
+};
 
 struct Timer {
   sph_ctx *c;
@@ -618,6 +638,7 @@ void use_target_tree(const sph_ctx *ctx, int n_nodes, PassArgs &a) {
 int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const void *y, const void *z,
                      const double *mass, const double *h0, double *h_out, double *rho_out, uint8_t *flags_out,
                      sph_stats *st, Timer &tm) {
+  Nvtx range_pass("sph.pass");
   const int n = (int)prm->n;
   const int n_targets = prm->n_targets > 0 ? (int)prm->n_targets : n;
   const int k = prm->k;
@@ -657,11 +678,15 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   const int compute_f32 = prm->precision == SPH_PRECISION_F32 || (prm->precision == 2 && !root.not_f32);
   const float rmax = compute_rmax(root, prm->periodic, prm->box);
   int n_nodes = 0;
-  rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
+  {
+    Nvtx r("sph.tree");
+    rc = stage_tree(ctx, n, prm->precision, compute_f32, x, y, z, mass, k, rmax, &n_nodes, &launches, true);
+  }
   if (rc) return rc;
   tm.mark(2);
   int hist_rounds = 1, band_rounds = 0;
   // ---- search, exact select and density (per-target kernels) ----
+  NvtxSpan range_search("sph.search");
   const bool sliced = ctx->slice_hi >= 0;
   const int slo = sliced ? (int)ctx->slice_lo : 0, shi = sliced ? (int)ctx->slice_hi : n;
   k_init_state<<<nblk(n), kTB, 0, ctx->stream>>>(n, n_targets, ctx->perm.p, ctx->state.p, slo, shi);
@@ -820,7 +845,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   PassArgs warp_args = a;
   tm.mark(4);
   tm.mark(5);
+  range_search.end();
   // ---- finalize ----
+  Nvtx range_fin("sph.finalize");
   int *rounds_hist = ctx->ints.p + kIntsFixed;
   std::vector<int> hist(max_it + 2);
   unsigned long long stat_all[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1227,6 +1254,7 @@ int sph_density_pass_multi(sph_ctx *const *ctxs, int32_t n_ctx, const sph_params
   };
   std::vector<Part> part(n_ctx);
   auto work = [&](int d) {
+    Nvtx range_dev("sph.multi.device");
     sph_ctx *ctx = ctxs[d];
     Part &P = part[d];
     const int64_t lo = n * d / n_ctx, hi = n * (d + 1) / n_ctx, m = hi - lo;
