@@ -642,13 +642,20 @@ def run_decomposed(args, world, rank, local):
     if not args.no_e2e:
         pin = [torch.from_numpy(a).pin_memory() for a in (*hp, hm, hh0, sel.astype(np.int64))]
         e2e_ms = []
+        outs = None  # pinned result buffers (the owned count is fixed for a fixed input)
         for i in range(args.warmup + args.steps):
             torch.cuda.synchronize(device)
             tdist.barrier()
             t0 = time.perf_counter()
             d = [t.to(device, non_blocking=True) for t in pin]
             rr = step(*d)
-            out = (rr.gid.cpu(), rr.h.cpu(), rr.rho.cpu())
+            src = (rr.gid, rr.h, rr.rho)
+            if outs is None or outs[0].numel() != src[0].numel():
+                outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in src]
+            for o, t in zip(outs, src):
+                o.copy_(t, non_blocking=True)
+            torch.cuda.synchronize(device)
+            out = outs
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 e2e_ms.append(dt * 1e3)
