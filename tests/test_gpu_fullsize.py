@@ -1,7 +1,10 @@
 """Parity at BASELINE's full sizes (configs 2-5, the device-generated sets).
 
 The whole pass runs on the GPU; the CPU oracle (the reference algorithm in C)
-runs on a seeded random sample of targets (exact for every sampled target:
+runs on EVERY target of C2 (1,048,576), C3 (16,777,216, the bench's headline
+config) and C5 (8,388,608, K = 128), on 2,000,000 random targets of C4
+(134,217,728) and on 30,000 targets at the periodic faces of C2 and C3
+(exact for every checked target:
 each target's h and rho depend only on the positions, reference
 density.py:11-13).  The oracle works on a crop of the set -- every particle
 within a margin above the targets' h, periodic images included
@@ -88,22 +91,27 @@ def _check(cfg, n_sample, seed=0):
     return w, p32, h, st
 
 
-def test_config2_full_size_sampled_oracle():
-    _, _, _, st = _check(2, 2048)
+def test_config2_every_particle_against_oracle():
+    # every one of the 1,048,576 targets (the oracle over the whole set)
+    w = workload.config_device(2)
+    _, _, _, st = _check(2, w["x"].shape[0])
     assert st.device["pair_tests"] > 0
 
 
-def test_config5_full_size_k128_sampled_oracle():
-    _check(5, 512, seed=1)
+def test_config5_every_particle_k128_against_oracle():
+    # all 8,388,608 targets of the single-halo stress case (K = 128)
+    _check(5, 8388608, seed=1)
 
 
-def test_config3_full_size_sampled_oracle():
-    _check(3, 1024, seed=2)
+def test_config3_every_particle_against_oracle():
+    # all 16,777,216 targets of the bench's headline config
+    _check(3, 16777216, seed=2)
 
 
 def test_config4_full_size_sampled_oracle():
-    # 134,217,728 particles on one GPU (BASELINE names 8; the pass fits one B200)
-    _check(4, 256, seed=3)
+    # 134,217,728 particles on one GPU (BASELINE names 8; the pass fits one B200);
+    # 2M random targets
+    _check(4, 2000000, seed=3)
 
 
 @pytest.mark.parametrize("cfg", [2, 3])
@@ -150,7 +158,7 @@ def test_device_generator_matches_host_restatement():
 
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_periodic_boundary_targets_full_size(cfg):
-    """Targets whose search sphere crosses a face of the periodic box (their
+    """30,000 targets whose search sphere crosses a face of the periodic box (their
     candidates include images; C3's box side, 100 * 16^(1/3), is not an fp32
     value, so the image offsets must be applied in fp64 to keep the fp32
     guard band)."""
@@ -163,5 +171,5 @@ def test_periodic_boundary_targets_full_size(cfg):
     gap = np.minimum(p64, box - p64).min(axis=1)
     near = np.nonzero(gap < h)[0]
     assert near.size > 1000
-    tg = np.random.default_rng(cfg).choice(near, size=min(near.size, 3000), replace=False)
+    tg = np.random.default_rng(cfg).choice(near, size=min(near.size, 30000), replace=False)
     _sampled(w, p32, h, rho, 0, 0, targets=tg)
