@@ -133,15 +133,9 @@ struct PassArgs {
   int *task_count;          // device task counter
   int *member_cursor;       // device member allocation cursor
   int shortcut;             // bit per mode: count whole cells from their box when possible
-  // neighbour lists recorded by the histogram pass (nullptr = off): per target
-  // ncap entries {idx | shift << 27, fp32 d2 bits} or {cell start | shift << 27, tag | count}
-  uint2 *nlists;
-  int *ncount;              // entries recorded (> ncap: overflowed, list unusable)
-  int ncap;
-  int lshrink;              // shrink after every candidate chunk (not only per flush)
-  int lcompact;             // compact the list at a shrink once it holds more entries than this
+  int *ncount;              // per target: collect-instance marker (0x7fffffff: list overflowed in the main kernel)
   int tshrink;              // per-target kernel: shrink after every K >> tshrink new candidates
-  int static_sched;         // per-target kernel: strided static assignment instead of the atomic counter
+  int static_sched;         // per-target kernel: strided static assignment (0: the atomic counter; always 0)
   int tchunk;               // per-target kernel: consecutive targets per work grab (identity target order)
   const unsigned *clist;    // per-target kernel: neighbour-cell lists per cell (child-record indices into tree.crec), clcap each
   const int *clen;          // list length per cell (-1: none)

@@ -141,7 +141,6 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
     float hR2 = 0.f;  // HIST: histogram range R_b^2 of this lane's sub-bundle
     float h_fin = 0.f;  // HIST: final (shrunk) acceptance radius^2: the recorded list is complete below it
     int ne = 0;         // HIST: neighbour-list entries recorded for this lane's target
-    uint2 *const nl = (MODE == MODE_HIST && a.nlists && active) ? a.nlists + (size_t)p * a.ncap : nullptr;
     // BAND
     double lo = 0.0, hi = -1.0, scale = 0.0, emin = INFINITY, emax = -INFINITY;
     float lo_f = -1.f, hi_f = -2.f;
@@ -249,14 +248,6 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
           if (edge < hr2) {
             hr2 = edge;
             h_fin = edge;
-            if (nl && ne > a.lcompact && ne <= a.ncap) {
-              int w2 = 0;
-              for (int i = 0; i < ne; ++i) {
-                const uint2 e = nl[i];
-                if (e.y >= kCellTag || __uint_as_float(e.y) <= edge) nl[w2++] = e;
-              }
-              ne = w2;
-            }
           }
         }
       };
@@ -426,10 +417,6 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                       if (sc >= 0) {
                         hist[sc * 32 + lane] += (unsigned)ncell;
                         seen += ncell;
-                        if (nl) {  // whole cell recorded as one entry
-                          if (ne < a.ncap) nl[ne] = make_uint2((unsigned)s0 | ((unsigned)sidx << 27), kCellTag | (unsigned)ncell);
-                          ++ne;
-                        }
                       }
                     } else if constexpr (MODE == MODE_BAND) {
                       if (sc > 0) c_below += sc;
@@ -535,10 +522,6 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                     const int bin = min(max((__float_as_int(x) >> 21) - kHistBase + 1, 0), NB_HIST - 1);
                     atomicAdd(&hist[bin * 32 + lane], 1u);  // no return value: no LDS->STS chain
                     ++seen;
-                    if (nl) {
-                      if (ne < a.ncap) nl[ne] = make_uint2((unsigned)cidx | ((unsigned)sidx << 27), __float_as_uint(F32 ? af : (float)ad));
-                      ++ne;
-                    }
                   }
                 } else if constexpr (MODE == MODE_BAND) {
                   if (!is_self) {
@@ -612,15 +595,7 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
                 }
                }
               }
-              if constexpr (MODE == MODE_HIST) {
-                // list recording: shrink as soon as K/2 more were counted, so
-                // that the list stays near K entries
-                if (nl && a.lshrink && member && seen > K && seen - seen_shrunk >= (K >> 1)) {
-                  shrink(seen, h_r2);
-                  seen_shrunk = seen;
-                }
-                h_r2d = (double)h_r2;
-              }
+              if constexpr (MODE == MODE_HIST) h_r2d = (double)h_r2;
             }
             __syncwarp();
           }
@@ -682,13 +657,6 @@ __device__ __forceinline__ void run_task(const PassArgs &a, const int2 task, con
           } else {
             tl = (double)__int_as_float((kHistBase + bb - 1) << 21) * R2d * (1.0 - 8.0 * kEpsD);
             th = (double)__int_as_float((kHistBase + bb) << 21) * R2d * (1.0 + 8.0 * kEpsD);
-          }
-          if (a.nlists) {
-            // the recorded list holds every candidate with d2 <= h_fin (fp32
-            // prefilter, 2^-20 guard): clip the bracket to that
-            th = fmin(th, (double)h_fin * (1.0 - 4.0 * kEpsD));
-            if (th < tl) th = tl;
-            a.ncount[p] = ne;
           }
           a.t_lo[p] = tl;
           a.t_hi[p] = th;
