@@ -59,6 +59,10 @@ def lib():
         L.sph_oracle_counts.argtypes = [i64, p, p, p, p, p, ctypes.c_int]
         L.sph_oracle_density_pass.argtypes = [i64, p, p, p, p, p, p, p, i64, i64,
                                               ctypes.c_int, p, i64, p, i64, p]
+        L.sph_oracle_tree_new.argtypes = [i64, p, p, p, ctypes.POINTER(ctypes.c_int)]
+        L.sph_oracle_tree_new.restype = p
+        L.sph_oracle_tree_free.argtypes = [p]
+        L.sph_oracle_density_pass_tree.argtypes = [p, p, p, p, p, i64, i64, ctypes.c_int, p, i64, p, i64, p]
         L.sph_oracle_w.argtypes = [ctypes.c_double, ctypes.c_double]
         L.sph_oracle_w.restype = ctypes.c_double
         L.sph_oracle_nthreads.restype = ctypes.c_int
@@ -145,6 +149,50 @@ def density_pass(x, y, z, mass, h0, k: int, max_iterations: int = 100,
         raise ValueError(f"oracle density pass failed with status {st}")
     it = int(info[0])
     return OracleResult(h, rho, flags, todo[:it].copy(), it, int(info[3]))
+
+
+class Prepared:
+    """The oracle's octree over a fixed particle set, built once and reused by
+    passes over target subsets (the CPU baseline's sampled timing: the tree
+    build is the fixed part of a pass, timed once).  Periodic boxes: the
+    originals plus their images within ``margin`` (``periodic_images``);
+    targets index the originals."""
+
+    def __init__(self, x, y, z, box: float | None = None, margin: float | None = None):
+        x, y, z = _f8(x), _f8(y), _f8(z)
+        self.n = x.shape[0]
+        if box:
+            ax, ay, az, src = periodic_images(x, y, z, box, margin if margin is not None else 0.5 * box)
+        else:
+            ax, ay, az, src = x, y, z, np.arange(self.n)
+        self._x, self._y, self._z, self.src = _f8(ax), _f8(ay), _f8(az), src  # must outlive the handle
+        st = ctypes.c_int(0)
+        self._h = lib().sph_oracle_tree_new(self._x.shape[0], _ptr(self._x), _ptr(self._y), _ptr(self._z),
+                                            ctypes.byref(st))
+        if not self._h:
+            raise ValueError(f"oracle tree build failed with status {st.value}")
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sph_oracle_tree_free(self._h)
+            self._h = None
+
+    def density_pass(self, mass, h0, k: int, targets, max_iterations: int = 100, threads: int = 0) -> OracleResult:
+        m = _f8(mass)[self.src]
+        h = _f8(h0)[self.src].copy()
+        na = h.shape[0]
+        rho = np.zeros(na, dtype=np.float64)
+        flags = np.zeros(na, dtype=np.uint8)
+        todo = np.zeros(max(max_iterations, 1) + 1, dtype=np.int64)
+        info = np.zeros(4, dtype=np.int64)
+        tg = np.ascontiguousarray(targets, dtype=np.int64)
+        st = lib().sph_oracle_density_pass_tree(self._h, _ptr(m), _ptr(h), _ptr(rho), _ptr(flags), k,
+                                                max_iterations, threads, _ptr(tg), tg.shape[0], _ptr(todo),
+                                                todo.shape[0], _ptr(info))
+        if st:
+            raise ValueError(f"oracle density pass failed with status {st}")
+        it = int(info[0])
+        return OracleResult(h[:self.n], rho[:self.n], flags[:self.n], todo[:it].copy(), it, int(info[3]))
 
 
 def kernel_w(r, h):

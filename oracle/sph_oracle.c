@@ -374,20 +374,18 @@ int sph_oracle_counts(int64_t n, const double *x, const double *y, const double 
  *   info[2] = still-flagged count on ConvergenceError, info[3] = total
  *   candidates seen (pair tests accepted by the leaf test, all rounds)
  */
-int sph_oracle_density_pass(int64_t n, const double *x, const double *y, const double *z,
-                            const double *mass, double *h_inout, double *rho_out,
-                            uint8_t *flags_out, int64_t k, int64_t max_iterations,
-                            int nthreads, const int64_t *targets, int64_t n_targets,
-                            int64_t *todo_out, int64_t todo_cap, int64_t *info) {
-    if (n <= 0 || k < 1) return ST_INVALID;
+/* the todo loop of density.py:286-413 over a built tree (not freed here) */
+static int pass_on_tree(otree *tp, int64_t n, const double *x, const double *y, const double *z,
+                        const double *mass, double *h_inout, double *rho_out,
+                        uint8_t *flags_out, int64_t k, int64_t max_iterations,
+                        int nthreads, const int64_t *targets, int64_t n_targets,
+                        int64_t *todo_out, int64_t todo_cap, int64_t *info) {
     const double growth = 1.2599210498948732; /* 2.0 ** (1.0 / 3.0), density.py:53 */
-    otree t;
-    int st = otree_build(&t, n, x, y, z, 8, 48);
-    if (st) return st;
+    otree t = *tp;
     int64_t nt = targets ? n_targets : n;
     int64_t *todo = malloc(sizeof(int64_t) * (nt ? nt : 1));
     int64_t *next = malloc(sizeof(int64_t) * (nt ? nt : 1));
-    if (!todo || !next) { free(todo); free(next); otree_free(&t); return ST_NOMEM; }
+    if (!todo || !next) { free(todo); free(next); return ST_NOMEM; }
     for (int64_t q = 0; q < nt; ++q) {
         int64_t i = targets ? targets[q] : q;
         todo[q] = i;
@@ -403,7 +401,7 @@ int sph_oracle_density_pass(int64_t n, const double *x, const double *y, const d
         ++iteration;
         if (iteration > max_iterations) {
             info[0] = iteration - 1; info[2] = ntodo; info[3] = cand_total;
-            free(todo); free(next); otree_free(&t);
+            free(todo); free(next);
             return ST_NOT_CONVERGED;
         }
         if (iteration - 1 < todo_cap) todo_out[iteration - 1] = ntodo;
@@ -459,10 +457,10 @@ int sph_oracle_density_pass(int64_t n, const double *x, const double *y, const d
             }
             qs_free(&w);
         }
-        if (err) { free(todo); free(next); otree_free(&t); return err; }
+        if (err) { free(todo); free(next); return err; }
         if (bad >= 0) {
             info[0] = iteration; info[1] = bad; info[3] = cand_total;
-            free(todo); free(next); otree_free(&t);
+            free(todo); free(next);
             return ST_DEGENERATE;
         }
         int64_t m = 0;
@@ -470,8 +468,49 @@ int sph_oracle_density_pass(int64_t n, const double *x, const double *y, const d
         int64_t *tmp = todo; todo = next; next = tmp; ntodo = m;
     }
     info[0] = iteration; info[3] = cand_total;
-    free(todo); free(next); otree_free(&t);
+    free(todo); free(next);
     return ST_OK;
+}
+
+int sph_oracle_density_pass(int64_t n, const double *x, const double *y, const double *z,
+                            const double *mass, double *h_inout, double *rho_out,
+                            uint8_t *flags_out, int64_t k, int64_t max_iterations,
+                            int nthreads, const int64_t *targets, int64_t n_targets,
+                            int64_t *todo_out, int64_t todo_cap, int64_t *info) {
+    if (n <= 0 || k < 1) return ST_INVALID;
+    otree t;
+    int st = otree_build(&t, n, x, y, z, 8, 48);
+    if (st) return st;
+    st = pass_on_tree(&t, n, x, y, z, mass, h_inout, rho_out, flags_out, k, max_iterations, nthreads, targets,
+                      n_targets, todo_out, todo_cap, info);
+    otree_free(&t);
+    return st;
+}
+
+/* A built tree kept across calls (the CPU baseline times its sampled passes
+ * without rebuilding the tree; the positions must outlive the handle). */
+void *sph_oracle_tree_new(int64_t n, const double *x, const double *y, const double *z, int *status) {
+    otree *t = malloc(sizeof(otree));
+    if (!t) { *status = ST_NOMEM; return NULL; }
+    *status = n > 0 ? otree_build(t, n, x, y, z, 8, 48) : ST_INVALID;
+    if (*status) { free(t); return NULL; }
+    return t;
+}
+
+void sph_oracle_tree_free(void *h) {
+    if (!h) return;
+    otree_free((otree *)h);
+    free(h);
+}
+
+int sph_oracle_density_pass_tree(void *h, const double *mass, double *h_inout, double *rho_out,
+                                 uint8_t *flags_out, int64_t k, int64_t max_iterations, int nthreads,
+                                 const int64_t *targets, int64_t n_targets, int64_t *todo_out, int64_t todo_cap,
+                                 int64_t *info) {
+    otree *t = (otree *)h;
+    if (!t || k < 1) return ST_INVALID;
+    return pass_on_tree(t, t->n, t->x, t->y, t->z, mass, h_inout, rho_out, flags_out, k, max_iterations, nthreads,
+                        targets, n_targets, todo_out, todo_cap, info);
 }
 
 /* Wendland C6 at separation r for smoothing length h (kernel.py:39-45) */
