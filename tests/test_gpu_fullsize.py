@@ -173,3 +173,38 @@ def test_periodic_boundary_targets_full_size(cfg):
     assert near.size > 1000
     tg = np.random.default_rng(cfg).choice(near, size=min(near.size, 30000), replace=False)
     _sampled(w, p32, h, rho, 0, 0, targets=tg)
+
+
+def test_fp64_uniform_million_every_particle():
+    # the fp64 path at scale: 1,048,576 uniform fp64 positions (the reference's
+    # UniformBox stream), periodic, K = 64, every particle against the oracle
+    n, k = 1 << 20, 64
+    pos = workload.uniform_box(n, 13)
+    m = np.full(n, 1.0 / n)
+    h0 = np.full(n, 2.0 * n ** (-1.0 / 3.0))
+    h, rho, flags, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], m, h0, k, periodic=True, box=1.0)
+    want = oracle.density_pass_periodic(pos[:, 0], pos[:, 1], pos[:, 2], m, h0, k, 1.0)
+    assert np.array_equal(h, want.h)
+    np.testing.assert_allclose(rho, want.rho, rtol=1e-12, atol=0)
+    assert list(st.todo_sizes) == list(want.todo_sizes)
+
+
+def test_auto_precision_c2_every_particle():
+    # fp64 records holding fp32 values (precision "auto"): fp32 search, densities
+    # summed term for term in fp64 -- every C2 particle against the oracle
+    w = workload.config_device(2)
+    p64 = _host32(w).astype(np.float64)
+    n, k, box = p64.shape[0], int(w["k"]), float(w["box"])
+    h, rho, flags, st = sph.density_pass_soa(p64[:, 0], p64[:, 1], p64[:, 2], w["mass"], w["h0"], k,
+                                             precision="auto", periodic=True, box=box)
+    h32, _, _, _ = sph.density_pass_soa(p64[:, 0].astype(np.float32), p64[:, 1].astype(np.float32),
+                                         p64[:, 2].astype(np.float32), w["mass"], w["h0"], k, periodic=True, box=box)
+    assert np.array_equal(h, h32)
+    tg = np.arange(n)
+    margin = 1.05 * float(h.max())
+    h0 = np.array(w["h0"], dtype=np.float64, copy=True)
+    h0[:] = h * 1.01
+    want = oracle.density_pass_periodic(p64[:, 0], p64[:, 1], p64[:, 2], w["mass"], h0, k, box, margin=margin,
+                                        targets=tg)
+    assert np.array_equal(h, want.h)
+    np.testing.assert_allclose(rho, want.rho, rtol=1e-12, atol=0)
