@@ -1,4 +1,4 @@
-# r02o: bench lines for every config on one B200 (C4: 134M particles on one GPU)
+# bench lines for every config on one B200 (C4: 134M particles on one GPU)
 cd $GRAFT_REPO_ROOT
 for c in 1 2 5 4; do
   st=10; [ $c = 4 ] && st=5

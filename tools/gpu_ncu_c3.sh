@@ -1,4 +1,4 @@
-# r02n: full ncu captures of the two k_target launches on C3 (the bench config): seed and main
+# full ncu captures of the two k_target launches on C3 (the bench config): seed and main
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"^k_target$" --launch-count 1 \
