@@ -446,6 +446,7 @@ def run_ours(args):
     tests = accepted = search_tests = launches = 0
     stage_tot = {}
     last = None
+    known_ms = 0.0
     for i in range(args.steps):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -468,6 +469,7 @@ def run_ours(args):
         accepted += d["accepted_pairs"]
         search_tests += d["search_pair_tests"]
         launches += d["gpu_launches"]
+        known_ms += d.get("t_known_ms", 0.0)
         last = d
     torch.cuda.synchronize(device)
     clk = clocks.stop()
@@ -520,6 +522,8 @@ def run_ours(args):
             "search_efficiency": n * k / (search_tests / args.steps) if search_tests else None,
             "pair_tests_per_step": tests / args.steps,
             "kernel_ms_per_step": {kk: v / args.steps for kk, v in kern.items()},
+            "known_ms_per_step": known_ms / args.steps,
+            "known_fallbacks": last.get("known_fallbacks") if last else None,
             "stage_ms_per_step": {kk: v / args.steps for kk, v in stage_tot.items()},
             "todo_sizes": last["todo_sizes"] if last else None,
             "search_rounds": last["search_rounds"] if last else None,

@@ -86,6 +86,8 @@ struct sph_ctx {
   int seed_stride = 12;   // SPH_SEED: seed stride of the per-target pass (12 beat 6/8/16 on C1-C5, r01l; 0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
   int known = 0;          // SPH_KNOWN: 0 seeds + per-target kernel (measured fastest), 2 per-cell group kernel from R0, 3 seeds + group kernel
+  float lane_margin = 1.25f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
+  float lane_exc = 1.5f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   int group_g = 8;        // SPH_GROUP_G: targets per group
   int group_lcap = 0;     // SPH_GROUP_LCAP: list entries per target (0: group_list_cap(k))
   float group_r0f = 1.35f;  // SPH_GROUP_R0F: first radius = this x the tree estimate R0
@@ -765,7 +767,23 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     // neighbour-cell lists for the radii the seeds imply
     const int cap = ctx->cell_lists;
     const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
-    if (compute_f32 && ctx->known == 3 && ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
+    if (compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k) && ctx->kn_list.ensure(n) == cudaSuccess) {
+      // one lane per target over bundles of 32 sorted neighbours (sph_lane.cu);
+      // what it leaves, the per-target kernel takes
+      cudaEventRecord(ctx->kev_known[0], ctx->stream);
+      PassArgs ka = a;
+      ka.posj = ctx->posj.p;
+      ka.fb_list = ctx->kn_list.p;
+      ka.fb_count = ctx->qints.p + 21;
+      ka.kn_counters = ctx->qints.p + 10;
+      launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->num_sms);
+      cudaEventRecord(ctx->kev_known[1], ctx->stream);
+      SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
+      a.list = ctx->kn_list.p;
+      a.list_count = ctx->qints.p + 21;
+      launches += 2;
+      known_run = true;
+    } else if (compute_f32 && ctx->known == 3 && ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
       // the per-cell group kernel from the seeds' radii
       cudaEventRecord(ctx->kev_known[0], ctx->stream);
       PassArgs ka = a;
@@ -807,7 +825,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     int fbk[32];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(fbk, ctx->qints.p, sizeof(fbk), cudaMemcpyDeviceToHost);
-    if (ctx->known >= 2)
+    if (ctx->known == 5)
+      fprintf(stderr, "[sph lane] %d targets to the per-target kernel: bundles bailed %d; lanes: few within R %d, "
+              "list full %d, bracket %d, left out %d\n", fbk[21], fbk[10], fbk[11], fbk[12], fbk[13], fbk[23]);
+    else if (ctx->known >= 2)
       fprintf(stderr, "[sph group] %d targets to the general kernel: walk overflow (groups) %d, retries %d, "
               "retries exhausted %d, select %d; first tries from R0: few %d full %d edge %d; from the cell's h: "
               "few %d full %d edge %d; (target, chunk) pairs %u, chunks %u, groups %u\n", fbk[21], fbk[10], fbk[11],
@@ -1014,6 +1035,8 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_SEED")) c->seed_stride = atoi(v);
   if (const char *v = getenv("SPH_SEEDM")) c->seed_margin = (float)atof(v);
   if (const char *v = getenv("SPH_KNOWN")) c->known = atoi(v);
+  if (const char *v = getenv("SPH_LANEM")) c->lane_margin = (float)atof(v);
+  if (const char *v = getenv("SPH_LANEX")) c->lane_exc = (float)atof(v);
   if (const char *v = getenv("SPH_GROUP_G")) c->group_g = atoi(v);
   if (const char *v = getenv("SPH_GROUP_LCAP")) c->group_lcap = atoi(v);
   if (const char *v = getenv("SPH_GROUP_R0F")) c->group_r0f = (float)atof(v);
