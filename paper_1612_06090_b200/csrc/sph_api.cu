@@ -87,6 +87,7 @@ struct sph_ctx {
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
   int known = 0;          // SPH_KNOWN: 0 seeds + per-target kernel (measured fastest), 2 per-cell group kernel from R0, 3 seeds + group kernel
   float lane_margin = 1.25f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
+  int lane_stream = 3072;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
   float lane_exc = 1.5f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   int group_g = 8;        // SPH_GROUP_G: targets per group
   int group_lcap = 0;     // SPH_GROUP_LCAP: list entries per target (0: group_list_cap(k))
@@ -767,6 +768,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     // neighbour-cell lists for the radii the seeds imply
     const int cap = ctx->cell_lists;
     const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
+    bool lane_ran = false;
     if (compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k) && ctx->kn_list.ensure(n) == cudaSuccess) {
       // one lane per target over bundles of 32 sorted neighbours (sph_lane.cu);
       // what it leaves, the per-target kernel takes
@@ -776,13 +778,15 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ka.fb_list = ctx->kn_list.p;
       ka.fb_count = ctx->qints.p + 21;
       ka.kn_counters = ctx->qints.p + 10;
-      launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->num_sms);
+      launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->lane_stream,
+                  ctx->num_sms);
       cudaEventRecord(ctx->kev_known[1], ctx->stream);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       a.list = ctx->kn_list.p;
       a.list_count = ctx->qints.p + 21;
       launches += 2;
       known_run = true;
+      lane_ran = true;
     } else if (compute_f32 && ctx->known == 3 && ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
       // the per-cell group kernel from the seeds' radii
       cudaEventRecord(ctx->kev_known[0], ctx->stream);
@@ -800,7 +804,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       a.list_count = ctx->qints.p + 21;
       launches += 2;
       known_run = true;
-    } else if (cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
+    }
+    // neighbour-cell lists for the cells that still hold targets (all of them, or what the lane kernel left)
+    if ((!known_run || lane_ran) && cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
         ctx->clen.ensure(ncell) == cudaSuccess && ctx->crad2.ensure(ncell) == cudaSuccess &&
         ctx->cnear.ensure(ncell) == cudaSuccess) {
       launch_cell_lists(ctx->stream, a, ctx->cellnode.p, ctx->ncell_dev.p, cap, ctx->clist.p, ctx->clen.p,
@@ -1037,6 +1043,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_KNOWN")) c->known = atoi(v);
   if (const char *v = getenv("SPH_LANEM")) c->lane_margin = (float)atof(v);
   if (const char *v = getenv("SPH_LANEX")) c->lane_exc = (float)atof(v);
+  if (const char *v = getenv("SPH_LANE_STREAM")) c->lane_stream = atoi(v);
   if (const char *v = getenv("SPH_GROUP_G")) c->group_g = atoi(v);
   if (const char *v = getenv("SPH_GROUP_LCAP")) c->group_lcap = atoi(v);
   if (const char *v = getenv("SPH_GROUP_R0F")) c->group_r0f = (float)atof(v);

@@ -34,6 +34,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 namespace sph {
 namespace {
@@ -42,19 +43,20 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int kLWarps = 2;
 constexpr int kTile = 128;    // candidates per staged tile (>= the largest search cell)
 constexpr int kCells = 384;   // cells per bundle
-constexpr int kMaxStream = 3072;  // candidates per bundle: longer streams (ragged bundles) go to the per-target kernel
 constexpr int kBins = 64;     // histogram bins over [0, R^2)
-constexpr int kLStack = 128;  // traversal stack (internal node ids)
+constexpr int kLStack = 96;   // traversal stack (internal node ids)
 constexpr int kInb = 16;      // in-bracket entries per lane (doubles; alias the tile buffers)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_warp.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
 static_assert(kInb * 32 * 8 <= 2 * kTile * 16, "in-bracket buffer aliases the tile buffers");
 
 // per warp: mbarriers | tile buffers (the walk's cell boxes and, after pass 2, the in-bracket doubles live there
-// too) | cell table | stack | lists (the histogram lives there until pass 2 starts)
+// too) | run starts | stack | lists (16-bit run codes; the 16-bit histogram lives there until pass 2 starts) |
+// run codes of the staged tile | run offsets (16-bit)
 __host__ __device__ constexpr int lane_smem_bytes(int lcap) {
-  return 16 + 2 * kTile * 16 + 2 * kTile * 4 + kCells * 4 + (kCells + 4) * 4 + kLStack * 4 + lcap * 128;
+  return (16 + 2 * kTile * 16 + kCells * 4 + kLStack * 4 + lcap * 64 + 2 * kTile * 2 + (kCells + 8) * 2 + 15) & ~15;
 }
+static_assert(kCells <= 512 && kTile <= 128, "a list entry is (run << 7 | offset) in 16 bits");
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
@@ -96,7 +98,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // counters (a.kn_counters): [0] bundles bailed (table / stack / cell size), [1] lanes with fewer than K within R,
 // [2] lanes whose list would overflow, [3] lanes whose bracket could not be ranked, [13] lanes left out of their
 // bundle (far from its bulk / periodic face)
-__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc) {
+__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -105,12 +107,12 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
   float4 *tile = reinterpret_cast<float4 *>(wb + 16);
   float4 *sbox = tile;
   double *inb = reinterpret_cast<double *>(tile);
-  unsigned *tidx = reinterpret_cast<unsigned *>(tile + 2 * kTile);  // sorted index of each staged candidate
-  int *cstart = reinterpret_cast<int *>(tidx + 2 * kTile);
-  int *coff = cstart + kCells;
-  int *stk = coff + kCells + 4;
-  unsigned *list = reinterpret_cast<unsigned *>(stk + kLStack);
-  unsigned *hist = list;
+  int *cstart = reinterpret_cast<int *>(tile + 2 * kTile);
+  int *stk = cstart + kCells;
+  unsigned short *list = reinterpret_cast<unsigned short *>(stk + kLStack);
+  unsigned short *hist = list;
+  unsigned short *tcode = list + lcap * 32;  // run code of each staged candidate (pass 2)
+  unsigned short *coff = tcode + 2 * kTile;
 
   const float4 *__restrict__ pos = reinterpret_cast<const float4 *>(a.pos);
   const float4 *__restrict__ posj = a.posj;
@@ -267,20 +269,20 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
                 if (nt >= kCells || cnt > kTile) { bail = true; break; }
                 if (lane == 0) {
                   cstart[nt] = s0;
-                  coff[nt] = total;
+                  coff[nt] = (unsigned short)total;
                 }
                 ++nt;
                 run_cnt = cnt;
               }
               run_end = s0 + cnt;
               total += cnt;
-              if (total > kMaxStream) { bail = true; break; }
+              if (total > max_stream) { bail = true; break; }  // ragged bundle: the per-target kernel is cheaper
             }
           }
         }
         __syncwarp();
       }
-      if (lane == 0) coff[nt] = total;
+      if (lane == 0) coff[nt] = (unsigned short)total;
       __syncwarp();
       if (bail || nt == 0) {
         ++c_bail;
@@ -289,17 +291,18 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
         auto issue = [&](int c0, int buf, int &nc, int &cnt) {
           const int base = coff[c0];
           const int ci = c0 + lane;
-          const int e = ci < nt ? coff[ci + 1] - base : INT_MAX;
+          const int e = ci < nt ? (int)coff[ci + 1] - base : INT_MAX;
           nc = __popc(__ballot_sync(FULL, e <= kTile));
           cnt = __shfl_sync(FULL, e, nc - 1);
           if (lane == 0) mbar_arrive_expect_tx(&bars[buf], (unsigned)cnt * 16u);
           __syncwarp();
           if (lane < nc) {
-            const int o = coff[ci] - base;
+            const int o = (int)coff[ci] - base;
             bulk_g2s(tile + buf * kTile + o, posj + cstart[ci], (unsigned)(e - o) * 16u, &bars[buf]);
           }
         };
-        auto stream = [&](auto body4, auto body1) {
+        auto stream = [&](auto codes, auto body4, auto body1) {
+          constexpr bool kCodes = decltype(codes)::value;
           int c0 = 0, buf = 0, nc_cur = 0, cnt_cur = 0;
           issue(0, 0, nc_cur, cnt_cur);
           for (;;) {
@@ -309,24 +312,38 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             while (!mbar_try_wait(&bars[buf], (phase >> buf) & 1u)) {}
             phase ^= 1u << buf;
             float4 *tb = tile + buf * kTile;
-            unsigned *ti = tidx + buf * kTile;
-            // staged (x, y, z, index) -> the bundle's frame: (x', y', z', |c'|^2), indices aside
+            unsigned short *tc = tcode + buf * kTile;
+            // staged (x, y, z, index) -> the bundle's frame: (x', y', z', |c'|^2); pass 2 also needs each
+            // candidate's run code (run << 7 | offset in the run): the run by bisection of the tile's offsets
+            const int sp0 = coff[c0];
             for (int q = lane; q < cnt_cur; q += 32) {
               const float4 c = tb[q];
               const float x = c.x - ox, y = c.y - oy, z = c.z - oz;
               tb[q] = make_float4(x, y, z, fmaf(x, x, fmaf(y, y, z * z)));
-              ti[q] = __float_as_uint(c.w);
+              if constexpr (kCodes) {
+                const int sp = sp0 + q;
+                int lo = c0, hi = c1;
+                while (hi - lo > 1) {
+                  const int mid = (lo + hi) >> 1;
+                  if ((int)coff[mid] <= sp) lo = mid; else hi = mid;
+                }
+                tc[q] = (unsigned short)((lo << 7) | (sp - (int)coff[lo]));
+              }
             }
             __syncwarp();
-            // four candidates (and their indices) loaded ahead of their tests: the tests write shared
+            // four candidates (and their codes) loaded ahead of their tests: the tests write shared
             // memory, so the compiler would not hoist the loads itself
             const float4 *tq = tb;
-            const uint4 *iq = reinterpret_cast<const uint4 *>(ti);
+            const uint2 *iq = reinterpret_cast<const uint2 *>(tc);
             int left = cnt_cur;
 #pragma unroll 2
-            for (; left >= 4; left -= 4, tq += 4, ++iq) body4(tq[0], tq[1], tq[2], tq[3], iq[0]);
-            const unsigned *i1 = reinterpret_cast<const unsigned *>(iq);
-            for (int s = 0; s < left; ++s) body1(tq[s], i1[s]);
+            for (; left >= 4; left -= 4, tq += 4, ++iq) {
+              uint2 cd = make_uint2(0u, 0u);
+              if constexpr (kCodes) cd = iq[0];
+              body4(tq[0], tq[1], tq[2], tq[3], cd);
+            }
+            const unsigned short *i1 = reinterpret_cast<const unsigned short *>(iq);
+            for (int s = 0; s < left; ++s) body1(tq[s], kCodes ? (unsigned)i1[s] : 0u);
             __syncwarp();
             if (c1 >= nt) break;
             c0 = c1;
@@ -338,7 +355,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
 
         // ---- pass 1: per-lane histogram of d2 over [0, R^2) ----
 #pragma unroll
-        for (int bb = 0; bb <= kBins; ++bb) hist[bb * 32 + lane] = 0u;
+        for (int bb = 0; bb <= kBins; ++bb) hist[bb * 32 + lane] = 0;
         __syncwarp();
         // d2 = |c' - t'|^2 = (|c'|^2 - 2 t'.c') + |t'|^2 in the bundle's frame: three FFMAs per candidate.  The
         // value is within E = 2^-18 reach^2 of the exact d2 wherever it matters (|c'| <= reach), which only
@@ -347,7 +364,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
         const float tpx = t.x - ox, tpy = t.y - oy, tpz = t.z - oz;
         const float m2x = act ? -2.0f * tpx : 0.f, m2y = act ? -2.0f * tpy : 0.f, m2z = act ? -2.0f * tpz : 0.f;
         const float t2s = act ? fmaf(tpx, tpx, fmaf(tpy, tpy, tpz * tpz)) * scale : 0.f;
-        unsigned *hcol = hist + lane;
+        unsigned short *hcol = hist + lane;  // 16-bit counters: two lanes per bank word, at most 2-way conflicts
         // own column, plain read-modify-write (shared atomics cost 2 cycles per lane); four candidates at a
         // time: the four counters are read first, repeated bins are accounted for in registers, so one
         // shared-memory latency is paid per four candidates
@@ -356,19 +373,20 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
           return __float2uint_rz(fminf(fmaf(sv, scale, t2s), (float)kBins)) << 5;  // bin kBins: beyond R
         };
         stream(
-            [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint4) {
+            std::false_type{},
+            [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint2) {
               const unsigned b0 = bin_of(q0), b1 = bin_of(q1), b2 = bin_of(q2), b3 = bin_of(q3);
               const unsigned v0 = hcol[b0];
               unsigned v1 = hcol[b1], v2 = hcol[b2], v3 = hcol[b3];
               v1 += b1 == b0;
               v2 += (b2 == b0) + (b2 == b1);
               v3 += (b3 == b0) + (b3 == b1) + (b3 == b2);
-              hcol[b0] = v0 + 1u;
-              hcol[b1] = v1 + 1u;
-              hcol[b2] = v2 + 1u;
-              hcol[b3] = v3 + 1u;
+              hcol[b0] = (unsigned short)(v0 + 1u);
+              hcol[b1] = (unsigned short)(v1 + 1u);
+              hcol[b2] = (unsigned short)(v2 + 1u);
+              hcol[b3] = (unsigned short)(v3 + 1u);
             },
-            [&](const float4 c, const unsigned) { hcol[bin_of(c)] += 1u; });
+            [&](const float4 c, const unsigned) { hcol[bin_of(c)] += 1; });
         tests += (unsigned long long)total * (unsigned)__popc(am);
         // the bin holding the K-th other (self counted at d2 = 0): cumulative count >= K + 1
         int cum = 0, bsel = -1, csel = 0;
@@ -409,23 +427,24 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
           }
           const unsigned lp0 = smem_u32(list + lane);
           unsigned lp = lp0;
-          auto keep = [&](const float4 c, const unsigned j) {
+          auto keep = [&](const float4 c, const unsigned code) {
             const float sv = fmaf(m2x, c.x, fmaf(m2y, c.y, fmaf(m2z, c.z, c.w)));
             if (sv <= thr_s) {
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lp), "r"(j) : "memory");
-              lp += 128u;
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(lp), "h"((unsigned short)code) : "memory");
+              lp += 64u;
             }
           };
           stream(
-              [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint4 i4) {
-                keep(q0, i4.x);
-                keep(q1, i4.y);
-                keep(q2, i4.z);
-                keep(q3, i4.w);
+              std::true_type{},
+              [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint2 cd) {
+                keep(q0, cd.x & 0xffffu);
+                keep(q1, cd.x >> 16);
+                keep(q2, cd.y & 0xffffu);
+                keep(q3, cd.y >> 16);
               },
               keep);
           tests += (unsigned long long)total * (unsigned)__popc(okm);
-          const int cnt = (int)((lp - lp0) >> 7);
+          const int cnt = (int)((lp - lp0) >> 6);
           int maxcnt = cnt;
           for (int o = 16; o; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(FULL, maxcnt, o));
 
@@ -436,6 +455,11 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
           const double th = ok ? fmax((double)(bsel + 1) / sc_d * (1.0 - 4.0 * kEpsD) - E, tl) : 0.0;
           const float lo_f = __double2float_rd(tl * (1.0 - kEpsD)) - 1e-37f;
           const float hi_f = __double2float_ru(th * (1.0 + kEpsD)) + 1e-37f;
+          // a list entry is a run code: sorted index = the run's start + the offset
+          auto entry = [&](int slot) {
+            const unsigned code = list[slot];
+            return cstart[code >> 7] + (int)(code & 127u);
+          };
           int below = 0, n_in = 0;
           auto classify = [&](const int j, const float4 c) {
             const float dx = c.x - t.x, dy = c.y - t.y, dz = c.z - t.z;
@@ -457,7 +481,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             int j[4];
             float4 c[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j[u] = e + u < cnt ? (int)list[(e + u) * 32 + lane] : p;
+            for (int u = 0; u < 4; ++u) j[u] = e + u < cnt ? entry((e + u) * 32 + lane) : p;
 #pragma unroll
             for (int u = 0; u < 4; ++u) c[u] = pos[j[u]];
 #pragma unroll
@@ -506,11 +530,11 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             for (; e + 4 <= cnt; e += 4) {
               float4 c[4];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) c[u] = pos[list[(e + u) * 32 + lane]];
+              for (int u = 0; u < 4; ++u) c[u] = pos[entry((e + u) * 32 + lane)];
 #pragma unroll
               for (int u = 0; u < 4; ++u) term(c[u]);
             }
-            for (; e < cnt; ++e) term(pos[list[e * 32 + lane]]);
+            for (; e < cnt; ++e) term(pos[entry(e * 32 + lane)]);
             rho = __dmul_rn(norm_h3, (double)accf);
           }
           if (ok) {
@@ -562,12 +586,12 @@ int lane_list_cap(int k) {
 
 bool lane_supported(int k) { return lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int num_sms) {
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms) {
   const int smem = kLWarps * lane_smem_bytes(lcap);
   int bps = 0;
   cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lane, kLWarps * 32, smem);
-  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc);
+  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, std::min(max_stream, 60000));
 }
 
 }  // namespace sph
