@@ -85,10 +85,10 @@ struct sph_ctx {
   bool debug = false;     // SPH_DEBUG=1: fallback counters on stderr
   int seed_stride = 12;   // SPH_SEED: seed stride of the per-target pass (12 beat 6/8/16 on C1-C5, r01l; 0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
-  int known = 0;          // SPH_KNOWN: 0 seeds + per-target kernel (measured fastest), 2 per-cell group kernel from R0, 3 seeds + group kernel
-  float lane_margin = 1.25f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
-  int lane_stream = 3072;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
-  float lane_exc = 1.5f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
+  int known = 5;          // SPH_KNOWN: 5 seeds + lane kernel + per-target kernel for what it leaves (default), 0 seeds + per-target kernel, 2 per-cell group kernel from R0, 3 seeds + group kernel
+  float lane_margin = 1.15f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
+  int lane_stream = 2400;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
+  float lane_exc = 2.0f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   int group_g = 8;        // SPH_GROUP_G: targets per group
   int group_lcap = 0;     // SPH_GROUP_LCAP: list entries per target (0: group_list_cap(k))
   float group_r0f = 1.35f;  // SPH_GROUP_R0F: first radius = this x the tree estimate R0

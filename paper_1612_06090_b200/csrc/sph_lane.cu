@@ -98,6 +98,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // counters (a.kn_counters): [0] bundles bailed (table / stack / cell size), [1] lanes with fewer than K within R,
 // [2] lanes whose list would overflow, [3] lanes whose bracket could not be ranked, [13] lanes left out of their
 // bundle (far from its bulk / periodic face)
+template <bool BATCH>
 __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -245,6 +246,8 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
         if (hit && !is_cell) stk[top + __popc(pm & lt_mask)] = __float_as_int(l4.w);
         top += __popc(pm);
         const unsigned cm = __ballot_sync(FULL, hit && is_cell);
+        // room for the step's cells; a ragged bundle (long stream) is cheaper in the per-target kernel
+        if (nt + __popc(cm) > kCells || total > max_stream) { bail = true; break; }
         if (cm) {
           if (hit && is_cell) {
             const int kk = __popc(cm & lt_mask);
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
                 // next to the last kept cell in memory: one copy serves both
                 run_cnt += cnt;
               } else {
-                if (nt >= kCells || cnt > kTile) { bail = true; break; }
+                if (cnt > kTile) { bail = true; break; }
                 if (lane == 0) {
                   cstart[nt] = s0;
                   coff[nt] = (unsigned short)total;
@@ -276,7 +279,6 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
               }
               run_end = s0 + cnt;
               total += cnt;
-              if (total > max_stream) { bail = true; break; }  // ragged bundle: the per-target kernel is cheaper
             }
           }
         }
@@ -376,6 +378,13 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             std::false_type{},
             [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint2) {
               const unsigned b0 = bin_of(q0), b1 = bin_of(q1), b2 = bin_of(q2), b3 = bin_of(q3);
+              if constexpr (!BATCH) {
+                hcol[b0] += 1;
+                hcol[b1] += 1;
+                hcol[b2] += 1;
+                hcol[b3] += 1;
+                return;
+              }
               const unsigned v0 = hcol[b0];
               unsigned v1 = hcol[b1], v2 = hcol[b2], v3 = hcol[b3];
               v1 += b1 == b0;
@@ -587,11 +596,16 @@ int lane_list_cap(int k) {
 bool lane_supported(int k) { return lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
 void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms) {
+  static const bool batch = getenv("SPH_LANE_BATCH") ? atoi(getenv("SPH_LANE_BATCH")) != 0 : false;
   const int smem = kLWarps * lane_smem_bytes(lcap);
-  int bps = 0;
-  cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lane, kLWarps * 32, smem);
-  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, std::min(max_stream, 60000));
+  const int ms = std::min(max_stream, 60000 - kCells * 0 - 4096);  // 16-bit run offsets (a step adds < 1024)
+  auto go = [&](auto kern) {
+    int bps = 0;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kLWarps * 32, smem);
+    kern<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms);
+  };
+  if (batch) go(k_lane<true>); else go(k_lane<false>);
 }
 
 }  // namespace sph

@@ -1,8 +1,10 @@
 """Every pipeline of the library against the CPU oracle.
 
 The default pass: seeds (every 12th sorted target) through the general
-per-target kernel, then neighbour-cell lists sized by the seeds' radii and
-the per-target kernel for every other target.  The alternative pipelines are
+per-target kernel, then the lane kernel (sph_lane.cu: bundles of 32 sorted
+neighbours, one lane per target) and, for what it leaves, neighbour-cell
+lists and the per-target kernel (SPH_KNOWN=0: the per-target kernel for every
+non-seed target).  The alternative pipelines are
 the per-cell group kernel (sph_group.cu) started from the tree estimate
 (SPH_KNOWN=2) or from the seeds (SPH_KNOWN=3), whose leftovers go back to the
 general kernel.  The fallbacks (the collect instance for overflowed neighbour
@@ -25,6 +27,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 CONFIGS = {
     "default": {},
+    "per_target_only": {"SPH_KNOWN": "0"},
+    "lane_tight_margin": {"SPH_LANEM": "1.0"},                      # many lanes with < K within R: per-target kernel
+    "lane_wide_margin_short_lists": {"SPH_LANEM": "1.8", "SPH_LANE_LEXTRA": "8"},   # full lists, crowded brackets
+    "lane_short_streams": {"SPH_LANE_STREAM": "600"},              # most bundles bail to the per-target kernel
+    "lane_no_exclusion_batched": {"SPH_LANEX": "0", "SPH_LANE_BATCH": "1"},
     "group_from_tree_estimate": {"SPH_KNOWN": "2"},
     "group_from_seeds": {"SPH_KNOWN": "3"},
     "group_g8_short_lists": {"SPH_KNOWN": "2", "SPH_GROUP_G": "8", "SPH_GROUP_LCAP": "96"},  # retries, full lists
