@@ -484,11 +484,10 @@ def run_ours(args):
     total_particles = float(n_total.item())
     value = total_particles * k / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (k_target: per-target search + select + density) ----
+    # ---- roofline of the search launches (k_target seeds + k_lane + k_target leftovers: 92 % of the pass) ----
     peak_ffma = float(L.sph_fp32_peak(ctx))
     t_k = kern["search"] + kern["select"] + kern["density"]
     ops = 6.0 * tests + 10.0 * accepted
-    dom = "k_target"
     achieved = ops / (t_k * 1e-3) / 1e12 if t_k > 0 else 0.0
     peak = peak_ffma / 1e12
     traffic = None
@@ -499,8 +498,8 @@ def run_ours(args):
             pj = json.load(open(prof))
             # measured on one config only: attached to that config's line
             if int(pj.get("config_index", 2)) == int(args.config):
-                traffic = pj.get(f"{dom}_bytes_per_launch")
-            issue = {"issue_slots_busy": pj.get("issue_slots_busy"), "note": pj.get("issue_note")}
+                traffic = pj.get("search_bytes_per_launch")
+            issue = {"issue_slots_busy": pj.get("issue_slots_busy"), "warp_instructions": pj.get("warp_instructions")}
         except Exception:
             traffic = None
 
@@ -511,13 +510,15 @@ def run_ours(args):
             "converged_particles_per_s": total_particles / (ms_max * 1e-3),
             "gpu_launches": launches // args.steps,
             "clocks": clk,
-            "roofline": {"bound": "fp32", "kernel": "k_target (per-target search + exact select + density; + fallbacks)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "fp32", "kernel": "search launches: k_lane (one lane per target over bundles of 32 sorted neighbours) + k_target (seeds and what k_lane leaves)", "achieved": achieved, "peak": peak,
                          "unit": "Tops/s (fp32-pipe ops)", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
                          "peak_source": "measured FFMA issue rate on this B200 (sph_fp32_peak); MEASURED_PEAKS.json "
                                         "has no FP32 vector figure",
-                         "ops_model": "6 per pair test, +10 per accepted pair (density)",
-                         "traffic_unit": "DRAM bytes (read + write) of the k_target launches of one pass, ncu",
+                         "ops_model": "6 per executed pair test, +10 per accepted pair (density); useful_frac counts only N*K pair "
+                                      "tests and N*(K+1) kernel terms",
+                         "useful_frac": ((6.0 * n * k + 10.0 * n * (k + 1)) * args.steps / (t_k * 1e-3) / 1e12 / peak) if (t_k > 0 and peak) else None,
+                         "traffic_unit": "DRAM bytes (read + write) of the search launches of one pass, ncu",
                          "issue_bound": issue},
             "search_efficiency": n * k / (search_tests / args.steps) if search_tests else None,
             "pair_tests_per_step": tests / args.steps,

@@ -1,9 +1,15 @@
-# full ncu captures of the two k_target launches on C3 (the bench config): seed and main
+# full ncu captures of the search launches on C3 (the bench config): k_target seeds, k_lane, k_target leftovers
+# usage: bash tools/gpu_ncu_c3.sh TAG
 cd $GRAFT_REPO_ROOT
+TAG=${1:-rXX}
 mkdir -p gpurun_out
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"^k_target$" --launch-count 1 \
-  -o gpurun_out/r02n_k_target_c3 python bench.py --config 3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02n_ncu_seed.log 2>&1; echo seed_rc=$?
-timeout 1500 ncu --set full --import-source on --clock-control none -k regex:"^k_target$" --launch-skip 1 --launch-count 1 \
-  -o gpurun_out/r02n_k_target_main_c3 python bench.py --config 3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r02n_ncu_main.log 2>&1; echo main_rc=$?
-for t in r02n_k_target_c3 r02n_k_target_main_c3; do ncu -i gpurun_out/$t.ncu-rep --page details > gpurun_out/${t}_details.txt 2>&1; done
-python tools/traffic_json.py r02n 3
+cap() {  # name regex skip
+  timeout 1500 ncu --set full --import-source on --clock-control none -k regex:"$2" --launch-skip $3 --launch-count 1 \
+    -o gpurun_out/${TAG}_$1_c3 python bench.py --config 3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_$1.log 2>&1
+  echo "$1 rc=$?"
+  ncu -i gpurun_out/${TAG}_$1_c3.ncu-rep --page details > gpurun_out/${TAG}_$1_c3_details.txt 2>&1
+}
+cap k_target_seed "^k_target$" 0
+cap k_lane "^k_lane$" 0
+cap k_target_rest "^k_target$" 1
+python tools/traffic_json.py $TAG 3
