@@ -87,6 +87,7 @@ struct sph_ctx {
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
   int known = 5;          // SPH_KNOWN: 5 seeds + lane kernel + per-target kernel for what it leaves (default), 0 seeds + per-target kernel, 2 per-cell group kernel from R0, 3 seeds + group kernel
   float lane_margin = 1.15f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
+  int lane_interp = 0;        // SPH_LANE_INTERP: lane kernel radius from the two seeds' h interpolated along the sorted order (instead of the larger)
   int lane_stream = 2400;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
   float lane_exc = 2.0f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   int group_g = 8;        // SPH_GROUP_G: targets per group
@@ -778,8 +779,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ka.fb_list = ctx->kn_list.p;
       ka.fb_count = ctx->qints.p + 21;
       ka.kn_counters = ctx->qints.p + 10;
+      // identity seeding only: with ghosts / slices the seeds follow the compacted target order
+      const bool interp = ctx->lane_interp && !(n_targets < n || sliced);
       launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->lane_stream,
-                  ctx->num_sms);
+                  ctx->num_sms, interp ? ctx->seed_stride : 0, ctx->lane_margin);
       cudaEventRecord(ctx->kev_known[1], ctx->stream);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       a.list = ctx->kn_list.p;
@@ -1044,6 +1047,7 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LANEM")) c->lane_margin = (float)atof(v);
   if (const char *v = getenv("SPH_LANEX")) c->lane_exc = (float)atof(v);
   if (const char *v = getenv("SPH_LANE_STREAM")) c->lane_stream = atoi(v);
+  if (const char *v = getenv("SPH_LANE_INTERP")) c->lane_interp = atoi(v);
   if (const char *v = getenv("SPH_GROUP_G")) c->group_g = atoi(v);
   if (const char *v = getenv("SPH_GROUP_LCAP")) c->group_lcap = atoi(v);
   if (const char *v = getenv("SPH_GROUP_R0F")) c->group_r0f = (float)atof(v);

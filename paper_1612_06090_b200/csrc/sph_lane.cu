@@ -15,16 +15,19 @@
 //   radius  R_i = margin x the larger converged h of the two seeds around the
 //           target (k_seed_radius); lanes far from the bundle's bulk or whose
 //           sphere crosses a periodic face are left to the per-target kernel;
-//   walk    the search tree once with the bundle box grown by max R; each hit
-//           cell is kept if it meets at least one lane's own sphere;
-//   pass 1  stream the cells: per lane a 64-bin histogram of d2 over
-//           [0, R_i^2) (one shared-memory column per lane: no conflicts) ->
-//           the bin holding the K-th neighbour;
+//   walk    the search tree once with the bundle box grown by max R (and the
+//           bundle's bounding sphere); each hit cell is kept if it meets at
+//           least one lane's own sphere; memory-adjacent cells merge into runs;
+//   pass 1  stream the runs; each landed tile is rewritten in the bundle's
+//           frame, (x', y', z', |c'|^2), so a pair test is three FFMAs; per
+//           lane a 64-bin histogram of d2 over [0, R_i^2) (one column of
+//           16-bit counters per lane) -> the bin holding the K-th neighbour;
 //   pass 2  stream again: per lane the list of every candidate up to that
-//           bin's upper edge (K + a few entries, sorted indices);
-//   select  per lane over its list: exact unfused fp64 d2 (octree.py:211-214)
-//           for entries in the guard band of the bin, count below + rank
-//           inside -> d2_K (h = sqrt(d2_K), density.py:226-245);
+//           bin's upper edge (K + a few entries, 16-bit run codes);
+//   select  per lane over its list, from the raw positions: exact unfused
+//           fp64 d2 (octree.py:211-214) for entries in the guard band of the
+//           bin, count below + rank inside -> d2_K (h = sqrt(d2_K),
+//           density.py:226-245);
 //   sum     rho = sum over list entries within h of m_j W(r/h), self included
 //           (density.py:160-171, 249-261; kernel.py:30-45).
 // Lanes the bundle cannot finish (fewer than K within R_i, list or bracket too
@@ -41,11 +44,17 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kLWarps = 2;
-constexpr int kTile = 128;    // candidates per staged tile (>= the largest search cell)
-constexpr int kCells = 384;   // cells per bundle
+#ifndef SPH_LANE_TILE
+#define SPH_LANE_TILE 128
+#endif
+#ifndef SPH_LANE_CELLS
+#define SPH_LANE_CELLS 384
+#endif
+constexpr int kTile = SPH_LANE_TILE;    // candidates per staged tile (>= the largest search cell)
+constexpr int kCells = SPH_LANE_CELLS;   // runs of cells per bundle
 constexpr int kBins = 64;     // histogram bins over [0, R^2)
 constexpr int kLStack = 96;   // traversal stack (internal node ids)
-constexpr int kInb = 16;      // in-bracket entries per lane (doubles; alias the tile buffers)
+constexpr int kInb = kTile / 8;  // in-bracket entries per lane (doubles; alias the tile buffers)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_warp.cu)
 constexpr double kEpsD = 9.5367431640625e-07;
 static_assert(kInb * 32 * 8 <= 2 * kTile * 16, "in-bracket buffer aliases the tile buffers");
@@ -99,7 +108,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 // [2] lanes whose list would overflow, [3] lanes whose bracket could not be ranked, [13] lanes left out of their
 // bundle (far from its bulk / periodic face)
 template <bool BATCH>
-__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream) {
+__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream, int seed_stride,
+                                                      float margin) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -148,7 +158,19 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
     float R = 0.f;
     if (want) {
       t = pos[p];
-      R = fminf(a.radius[p] * rscale, a.rmax);
+      R = a.radius[p] * rscale;
+      if (seed_stride > 0) {
+        // the two seeds around the target (every seed_stride-th sorted position, finished before this
+        // launch): their converged h interpolated geometrically along the sorted order
+        const int s0 = p - p % seed_stride, s1 = s0 + seed_stride;
+        const double ha = a.state[s0] == ST_FINAL ? a.d2k[s0] : 0.0;
+        const double hb = (s1 < n && a.state[s1] == ST_FINAL) ? a.d2k[s1] : 0.0;
+        if (ha > 0.0 && hb > 0.0 && ha < 1e30 && hb < 1e30) {
+          const float f = (float)(p - s0) / (float)seed_stride;
+          R = margin * exp2f(0.5f * ((1.0f - f) * log2f((float)ha) + f * log2f((float)hb)));
+        }
+      }
+      R = fminf(R, a.rmax);
       if (!(R > 0.f)) act = false;
       // spheres crossing a periodic face are searched with image shifts: the per-target kernel
       if (a.periodic) {
@@ -595,7 +617,8 @@ int lane_list_cap(int k) {
 
 bool lane_supported(int k) { return lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms) {
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
+                 int seed_stride, float margin) {
   static const bool batch = getenv("SPH_LANE_BATCH") ? atoi(getenv("SPH_LANE_BATCH")) != 0 : false;
   const int smem = kLWarps * lane_smem_bytes(lcap);
   const int ms = std::min(max_stream, 60000 - kCells * 0 - 4096);  // 16-bit run offsets (a step adds < 1024)
@@ -603,7 +626,7 @@ void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, floa
     int bps = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kLWarps * 32, smem);
-    kern<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms);
+    kern<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms, seed_stride, margin);
   };
   if (batch) go(k_lane<true>); else go(k_lane<false>);
 }

@@ -26,6 +26,12 @@ def metric(rep, name):
     return float(v[h.index(name)]) if name in h else None
 
 
+def duration_ms(rep):
+    h, u, v = raw(rep)
+    i = h.index("gpu__time_duration.sum")
+    return float(v[i]) * {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}.get(u[i], 1.0)
+
+
 if __name__ == "__main__":
     tag = sys.argv[1]
     cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 3
@@ -33,7 +39,7 @@ if __name__ == "__main__":
     b = {k: dram(r) for k, r in reps.items()}
     busy = {k: metric(r, "sm__inst_issued.avg.pct_of_peak_sustained_active") for k, r in reps.items()}
     inst = {k: metric(r, "smsp__inst_executed.sum") for k, r in reps.items()}
-    ms = {k: (metric(r, "gpu__time_duration.sum") or 0.0) / 1e6 for k, r in reps.items()}
+    ms = {k: duration_ms(r) for k, r in reps.items()}
     json.dump({"config_index": cfg, "search_bytes_per_launch": sum(b.values()), "launch_bytes": b,
                "unit": "bytes of DRAM traffic (read + write) of the search launches of one pass "
                        "(k_target seeds + k_lane + k_target leftovers)",
