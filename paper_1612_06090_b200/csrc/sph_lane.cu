@@ -45,10 +45,10 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kLWarps = 2;
 #ifndef SPH_LANE_TILE
-#define SPH_LANE_TILE 128
+#define SPH_LANE_TILE 96
 #endif
 #ifndef SPH_LANE_CELLS
-#define SPH_LANE_CELLS 384
+#define SPH_LANE_CELLS 256
 #endif
 constexpr int kTile = SPH_LANE_TILE;    // candidates per staged tile (>= the largest search cell)
 constexpr int kCells = SPH_LANE_CELLS;   // runs of cells per bundle
