@@ -1675,7 +1675,7 @@ int sph_decomp_ghost_mask_device(sph_ctx *ctx, int64_t n_groups, const double *d
   if (n_groups < 0 || n_foreign < 0 || width < 3) return fail(ctx, SPH_INVALID, "bad ghost-mask arguments");
   cudaSetDevice(ctx->device);
   ctx->err.clear();
-  SPH_CK(ctx->dscratch.ensure(7 * ((n_foreign + 31) / 32) + 7));
+  SPH_CK(ctx->dscratch.ensure(7 * ((n_foreign + 31) / 32) + 7 * ((n_foreign + 1023) / 1024) + 14));
   launch_ghost_mask(ctx->stream, n_groups, d_gdesc, d_gstart, d_gcount, width, d_rows, n_foreign, d_fdesc, d_frank,
                     periodic, box, d_mask, ctx->dscratch.p);
   SPH_CK(cudaGetLastError());

@@ -181,8 +181,8 @@ __device__ __forceinline__ double box_gap2(const double *a, const double *b, int
 // ghost marking: a particle of my group g is sent to rank q when it lies
 // within the margin of some group f of q (margin = the largest bound on h of
 // f's particles, so every neighbour of f's targets is covered).  One warp per
-// my group: the lanes scan super boxes of 32 consecutive foreign groups (box
-// vs box), then the members of the hit ones, and for each hit member the warp
+// my group: the lanes scan top boxes of 1024 consecutive foreign groups, then
+// the 32-group super boxes of the hit ones (box vs box), then their members, and for each hit member the warp
 // tests the group's particles (point vs box) and ORs the rank bit.
 __device__ __forceinline__ bool desc_hit(const double *gb, const double *__restrict__ d, int periodic, double box) {
   double fb[6];
@@ -195,7 +195,8 @@ __device__ __forceinline__ bool desc_hit(const double *gb, const double *__restr
 __global__ void k_ghost_mask(int64_t ng, const double *__restrict__ gdesc, const int64_t *__restrict__ gstart,
                              const int64_t *__restrict__ gcount, int width, const double *__restrict__ rows,
                              int64_t nf, const double *__restrict__ fdesc, const int32_t *__restrict__ frank,
-                             int64_t nsup, const double *__restrict__ sdesc, int periodic, double box,
+                             int64_t nsup, const double *__restrict__ sdesc, int64_t ntop,
+                             const double *__restrict__ tdesc, int periodic, double box,
                              uint32_t *__restrict__ mask) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -204,26 +205,34 @@ __global__ void k_ghost_mask(int64_t ng, const double *__restrict__ gdesc, const
 #pragma unroll
   for (int i = 0; i < 6; ++i) gb[i] = gdesc[7 * g + i];
   const int64_t s = gstart[g], c = gcount[g];
-  for (int64_t s0 = 0; s0 < nsup; s0 += 32) {
-    const int64_t sv = s0 + lane;
-    unsigned sh = __ballot_sync(0xffffffffu, sv < nsup && desc_hit(gb, sdesc + 7 * sv, periodic, box));
-    while (sh) {
-      const int64_t S = s0 + __ffs(sh) - 1;
-      sh &= sh - 1u;
-      const int64_t f = S * 32 + lane;
-      unsigned fm = __ballot_sync(0xffffffffu, f < nf && desc_hit(gb, fdesc + 7 * f, periodic, box));
-      while (fm) {
-        const int64_t fh = S * 32 + __ffs(fm) - 1;
-        fm &= fm - 1u;
-        double hb[6];
+  // two levels of super boxes over the foreign descriptors (key order, so they are spatially tight): 1024
+  // descriptors per top box, 32 per super box
+  for (int64_t t0 = 0; t0 < ntop; t0 += 32) {
+    const int64_t tv = t0 + lane;
+    unsigned th = __ballot_sync(0xffffffffu, tv < ntop && desc_hit(gb, tdesc + 7 * tv, periodic, box));
+    while (th) {
+      const int64_t T = t0 + __ffs(th) - 1;
+      th &= th - 1u;
+      const int64_t sv = T * 32 + lane;
+      unsigned sh = __ballot_sync(0xffffffffu, sv < nsup && desc_hit(gb, sdesc + 7 * sv, periodic, box));
+      while (sh) {
+        const int64_t S = T * 32 + __ffs(sh) - 1;
+        sh &= sh - 1u;
+        const int64_t f = S * 32 + lane;
+        unsigned fm = __ballot_sync(0xffffffffu, f < nf && desc_hit(gb, fdesc + 7 * f, periodic, box));
+        while (fm) {
+          const int64_t fh = S * 32 + __ffs(fm) - 1;
+          fm &= fm - 1u;
+          double hb[6];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) hb[i] = fdesc[7 * fh + i];
-        const double m = fdesc[7 * fh + 6] * (1.0 + 1e-9);
-        const uint32_t bit = 1u << frank[fh];
-        for (int64_t i = lane; i < c; i += 32) {
-          const double *r = rows + (s + i) * width;
-          const double pb[6] = {r[0], r[1], r[2], r[0], r[1], r[2]};
-          if (box_gap2(pb, hb, periodic, box) <= m * m) atomicOr(mask + s + i, bit);
+          for (int i = 0; i < 6; ++i) hb[i] = fdesc[7 * fh + i];
+          const double m = fdesc[7 * fh + 6] * (1.0 + 1e-9);
+          const uint32_t bit = 1u << frank[fh];
+          for (int64_t i = lane; i < c; i += 32) {
+            const double *r = rows + (s + i) * width;
+            const double pb[6] = {r[0], r[1], r[2], r[0], r[1], r[2]};
+            if (box_gap2(pb, hb, periodic, box) <= m * m) atomicOr(mask + s + i, bit);
+          }
         }
       }
     }
@@ -289,10 +298,12 @@ void launch_ghost_mask(cudaStream_t s, int64_t ng, const double *gdesc, const in
                        int width, const double *rows, int64_t nf, const double *fdesc, const int32_t *frank,
                        int periodic, double box, uint32_t *mask, double *scratch) {
   if (ng <= 0 || nf <= 0) return;
-  const int64_t nsup = (nf + 31) / 32;
+  const int64_t nsup = (nf + 31) / 32, ntop = (nsup + 31) / 32;
+  double *top = scratch + 7 * nsup;  // scratch holds 7 * (nsup + ntop) doubles
   k_super_desc<<<nb(nsup), kDT, 0, s>>>(nf, fdesc, nsup, scratch);
-  k_ghost_mask<<<nb(ng * 32), kDT, 0, s>>>(ng, gdesc, gstart, gcount, width, rows, nf, fdesc, frank, nsup, scratch,
-                                           periodic, box, mask);
+  k_super_desc<<<nb(ntop), kDT, 0, s>>>(nsup, scratch, ntop, top);
+  k_ghost_mask<<<nb(ng * 32), kDT, 0, s>>>(ng, gdesc, gstart, gcount, width, rows, nf, fdesc, frank, nsup, scratch, ntop,
+                                           top, periodic, box, mask);
 }
 
 void launch_group_boxes(cudaStream_t s, int64_t ng, const int64_t *starts, const int64_t *counts, int width,
