@@ -615,7 +615,9 @@ int lane_list_cap(int k) {
   return std::max(k + 1 + std::max(extra, 8), kBins + 1);  // the histogram rows alias the lists
 }
 
-bool lane_supported(int k) { return lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
+// K up to 160 (measured at 64 and 128): beyond it the K-th's histogram bin holds more candidates than the
+// in-bracket buffer and most lanes would fall back anyway
+bool lane_supported(int k) { return k <= 160 && lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
 void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
                  int seed_stride, float margin) {
