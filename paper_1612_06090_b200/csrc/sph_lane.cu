@@ -433,8 +433,14 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
         if (ok && bsel < 0) {
           ok = false;
           ++c_few;
-          a.radius[p] = fminf(R * 1.3f, a.rmax);  // the per-target kernel starts wider
+          // the per-target kernel starts from the radius the count within R suggests (its own growth rule)
+          const int others = cum - 1;
+          const float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.15f : 2.f;
+          a.radius[p] = fminf(R * fminf(fmaxf(f, 1.1f), 2.5f), a.rmax);
         }
+        // a lane that does not finish below still knows the K-th lies in bin bsel: a tight radius for the
+        // per-target kernel (overwritten when the lane finishes)
+        if (ok) a.radius[p] = fminf(R * sqrtf((float)(bsel + 1) / (float)kBins) * 1.002f, a.rmax);
         if (ok && csel > lcap) {
           ok = false;
           ++c_full;
