@@ -85,15 +85,10 @@ struct sph_ctx {
   bool debug = false;     // SPH_DEBUG=1: fallback counters on stderr
   int seed_stride = 12;   // SPH_SEED: seed stride of the per-target pass (12 beat 6/8/16 on C1-C5, r01l; 0/1 = off)
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
-  int known = 5;          // SPH_KNOWN: 5 seeds + lane kernel + per-target kernel for what it leaves (default), 0 seeds + per-target kernel, 2 per-cell group kernel from R0, 3 seeds + group kernel
+  int known = 5;          // SPH_KNOWN: 5 seeds + lane kernel + per-target kernel for what it leaves (default), 0 seeds + per-target kernel for every other target
   float lane_margin = 1.15f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
-  int lane_interp = 0;        // SPH_LANE_INTERP: lane kernel radius from the two seeds' h interpolated along the sorted order (instead of the larger)
   int lane_stream = 2400;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
   float lane_exc = 2.0f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
-  int group_g = 8;        // SPH_GROUP_G: targets per group
-  int group_lcap = 0;     // SPH_GROUP_LCAP: list entries per target (0: group_list_cap(k))
-  float group_r0f = 1.35f;  // SPH_GROUP_R0F: first radius = this x the tree estimate R0
-  int group_first = 2;    // SPH_GROUP_FIRST: targets in a cell's first group (longer lists)      // SPH_KNOWN=0: no known-radius kernel (the general kernel takes every non-seed target)
   bool known_ran = false;
   cudaEvent_t kev_known[2];
   DevBuf<uint32_t> kn_list;   // targets the known-radius kernel leaves to the general kernel
@@ -714,25 +709,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   }
   bool known_run = false;
   const bool seeded = ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride;
-  if (compute_f32 && ctx->known == 2 && ctx->last_ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
-    // the per-cell group kernel (sph_group.cu) takes every target from the
-    // tree's radius estimate; what it leaves, the general kernel takes
-    cudaEventRecord(ctx->kev_known[0], ctx->stream);
-    PassArgs ka = a;
-    ka.posj = ctx->posj.p;
-    ka.fb_list = ctx->kn_list.p;
-    ka.fb_count = ctx->qints.p + 21;
-    ka.kn_counters = ctx->qints.p + 10;
-    launch_group(ctx->stream, ka, ctx->cellnode.p, ctx->ncell_dev.p,
-                 ctx->group_lcap > 0 ? ctx->group_lcap : group_list_cap(k), ctx->seed_margin, ctx->group_r0f,
-                 ctx->group_first, ctx->num_sms, ctx->group_g);
-    cudaEventRecord(ctx->kev_known[1], ctx->stream);
-    SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-    a.list = ctx->kn_list.p;
-    a.list_count = ctx->qints.p + 21;
-    launches += 2;
-    known_run = true;
-  } else if (seeded) {
+  if (seeded) {
     // seeds first (every seed_stride-th sorted position, the general kernel
     // from the tree's radius estimate), then every other target starts from
     // its neighbouring seeds' converged h (sorted neighbours are spatial
@@ -779,10 +756,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ka.fb_list = ctx->kn_list.p;
       ka.fb_count = ctx->qints.p + 21;
       ka.kn_counters = ctx->qints.p + 10;
-      // identity seeding only: with ghosts / slices the seeds follow the compacted target order
-      const bool interp = ctx->lane_interp && !(n_targets < n || sliced);
       launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->lane_stream,
-                  ctx->num_sms, interp ? ctx->seed_stride : 0, ctx->lane_margin);
+                  ctx->num_sms);
       cudaEventRecord(ctx->kev_known[1], ctx->stream);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       a.list = ctx->kn_list.p;
@@ -790,23 +765,6 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       launches += 2;
       known_run = true;
       lane_ran = true;
-    } else if (compute_f32 && ctx->known == 3 && ncell >= 0 && ctx->kn_list.ensure(n) == cudaSuccess) {
-      // the per-cell group kernel from the seeds' radii
-      cudaEventRecord(ctx->kev_known[0], ctx->stream);
-      PassArgs ka = a;
-      ka.posj = ctx->posj.p;
-      ka.fb_list = ctx->kn_list.p;
-      ka.fb_count = ctx->qints.p + 21;
-      ka.kn_counters = ctx->qints.p + 10;
-      launch_group(ctx->stream, ka, ctx->cellnode.p, ctx->ncell_dev.p,
-                   ctx->group_lcap > 0 ? ctx->group_lcap : group_list_cap(k), ctx->seed_margin, 1.0f, ctx->group_g,
-                   ctx->num_sms, ctx->group_g);
-      cudaEventRecord(ctx->kev_known[1], ctx->stream);
-      SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
-      a.list = ctx->kn_list.p;
-      a.list_count = ctx->qints.p + 21;
-      launches += 2;
-      known_run = true;
     }
     // neighbour-cell lists for the cells that still hold targets (all of them, or what the lane kernel left)
     if ((!known_run || lane_ran) && cap > 0 && ncell >= 0 && ctx->clist.ensure((size_t)ncell * cap) == cudaSuccess &&
@@ -837,12 +795,6 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     if (ctx->known == 5)
       fprintf(stderr, "[sph lane] %d targets to the per-target kernel: bundles bailed %d; lanes: few within R %d, "
               "list full %d, bracket %d, left out %d\n", fbk[21], fbk[10], fbk[11], fbk[12], fbk[13], fbk[23]);
-    else if (ctx->known >= 2)
-      fprintf(stderr, "[sph group] %d targets to the general kernel: walk overflow (groups) %d, retries %d, "
-              "retries exhausted %d, select %d; first tries from R0: few %d full %d edge %d; from the cell's h: "
-              "few %d full %d edge %d; (target, chunk) pairs %u, chunks %u, groups %u\n", fbk[21], fbk[10], fbk[11],
-              fbk[12], fbk[13], fbk[23], fbk[24], fbk[25], fbk[26], fbk[27], fbk[28], (unsigned)fbk[29],
-              (unsigned)fbk[30], (unsigned)fbk[31]);
     else
       fprintf(stderr, "[sph seeds] %d seeds to the general kernel\n", fbk[14]);
     fprintf(stderr, "[sph warp] fall back to the walking select: %d overflowed lists, %d bracket misses; %d walks\n",
@@ -1047,11 +999,6 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LANEM")) c->lane_margin = (float)atof(v);
   if (const char *v = getenv("SPH_LANEX")) c->lane_exc = (float)atof(v);
   if (const char *v = getenv("SPH_LANE_STREAM")) c->lane_stream = atoi(v);
-  if (const char *v = getenv("SPH_LANE_INTERP")) c->lane_interp = atoi(v);
-  if (const char *v = getenv("SPH_GROUP_G")) c->group_g = atoi(v);
-  if (const char *v = getenv("SPH_GROUP_LCAP")) c->group_lcap = atoi(v);
-  if (const char *v = getenv("SPH_GROUP_R0F")) c->group_r0f = (float)atof(v);
-  if (const char *v = getenv("SPH_GROUP_FIRST")) c->group_first = atoi(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);

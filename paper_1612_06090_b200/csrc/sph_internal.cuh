@@ -146,8 +146,8 @@ struct PassArgs {
   int clcap;
   uint32_t *fb_list;        // per-target kernel: targets left for the collect instance (+ counter)
   int *fb_count;
-  const float4 *posj;       // sorted (x, y, z, sorted index bits) per position (fp32 path; k_known stages it)
-  int *kn_counters;         // k_known fallback reasons (image, list full, < K within R, select) or nullptr
+  const float4 *posj;       // sorted (x, y, z, sorted index bits) per position (fp32 path; k_lane stages it)
+  int *kn_counters;         // k_lane hand-over reasons (see sph_lane.cu) or nullptr
 };
 
 // ---- launchers (sph_tree.cu) ----
@@ -234,15 +234,10 @@ void launch_keys_at(cudaStream_t s, int n, int precision_in, const void *x, cons
 // ---- launchers (sph_pass.cu) ----
 enum PassMode { MODE_HIST = 0, MODE_BAND = 1, MODE_DENS = 2, MODE_COUNT = 3 };
 void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count, uint8_t want, int num_sms);
-// known-radius pass, one warp per cell and its targets in groups (sph_group.cu)
-int group_list_cap(int k);
-void launch_group(cudaStream_t s, const PassArgs &a, const int *cellnode, const int *ncells, int lcap, float margin,
-                  float r0f, int first_g, int num_sms, int g);
 // one lane per target over bundles of 32 consecutive sorted targets (sph_lane.cu)
 int lane_list_cap(int k);
 bool lane_supported(int k);
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
-                 int seed_stride, float margin);
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms);
 // fused per-target search + select + density (sph_warp.cu)
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,

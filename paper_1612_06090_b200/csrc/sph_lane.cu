@@ -107,9 +107,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // counters (a.kn_counters): [0] bundles bailed (table / stack / cell size), [1] lanes with fewer than K within R,
 // [2] lanes whose list would overflow, [3] lanes whose bracket could not be ranked, [13] lanes left out of their
 // bundle (far from its bulk / periodic face)
-template <bool BATCH>
-__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream, int seed_stride,
-                                                      float margin) {
+__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -159,17 +157,6 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
     if (want) {
       t = pos[p];
       R = a.radius[p] * rscale;
-      if (seed_stride > 0) {
-        // the two seeds around the target (every seed_stride-th sorted position, finished before this
-        // launch): their converged h interpolated geometrically along the sorted order
-        const int s0 = p - p % seed_stride, s1 = s0 + seed_stride;
-        const double ha = a.state[s0] == ST_FINAL ? a.d2k[s0] : 0.0;
-        const double hb = (s1 < n && a.state[s1] == ST_FINAL) ? a.d2k[s1] : 0.0;
-        if (ha > 0.0 && hb > 0.0 && ha < 1e30 && hb < 1e30) {
-          const float f = (float)(p - s0) / (float)seed_stride;
-          R = margin * exp2f(0.5f * ((1.0f - f) * log2f((float)ha) + f * log2f((float)hb)));
-        }
-      }
       R = fminf(R, a.rmax);
       if (!(R > 0.f)) act = false;
       // spheres crossing a periodic face are searched with image shifts: the per-target kernel
@@ -389,9 +376,8 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
         const float m2x = act ? -2.0f * tpx : 0.f, m2y = act ? -2.0f * tpy : 0.f, m2z = act ? -2.0f * tpz : 0.f;
         const float t2s = act ? fmaf(tpx, tpx, fmaf(tpy, tpy, tpz * tpz)) * scale : 0.f;
         unsigned short *hcol = hist + lane;  // 16-bit counters: two lanes per bank word, at most 2-way conflicts
-        // own column, plain read-modify-write (shared atomics cost 2 cycles per lane); four candidates at a
-        // time: the four counters are read first, repeated bins are accounted for in registers, so one
-        // shared-memory latency is paid per four candidates
+        // own column, plain read-modify-write (shared atomics cost 2 cycles per lane; reading four counters
+        // ahead and fixing repeated bins in registers measured the same at 20 warps per SM)
         auto bin_of = [&](const float4 c) {
           const float sv = fmaf(m2x, c.x, fmaf(m2y, c.y, fmaf(m2z, c.z, c.w)));
           return __float2uint_rz(fminf(fmaf(sv, scale, t2s), (float)kBins)) << 5;  // bin kBins: beyond R
@@ -400,22 +386,10 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             std::false_type{},
             [&](const float4 q0, const float4 q1, const float4 q2, const float4 q3, const uint2) {
               const unsigned b0 = bin_of(q0), b1 = bin_of(q1), b2 = bin_of(q2), b3 = bin_of(q3);
-              if constexpr (!BATCH) {
-                hcol[b0] += 1;
-                hcol[b1] += 1;
-                hcol[b2] += 1;
-                hcol[b3] += 1;
-                return;
-              }
-              const unsigned v0 = hcol[b0];
-              unsigned v1 = hcol[b1], v2 = hcol[b2], v3 = hcol[b3];
-              v1 += b1 == b0;
-              v2 += (b2 == b0) + (b2 == b1);
-              v3 += (b3 == b0) + (b3 == b1) + (b3 == b2);
-              hcol[b0] = (unsigned short)(v0 + 1u);
-              hcol[b1] = (unsigned short)(v1 + 1u);
-              hcol[b2] = (unsigned short)(v2 + 1u);
-              hcol[b3] = (unsigned short)(v3 + 1u);
+              hcol[b0] += 1;
+              hcol[b1] += 1;
+              hcol[b2] += 1;
+              hcol[b3] += 1;
             },
             [&](const float4 c, const unsigned) { hcol[bin_of(c)] += 1; });
         tests += (unsigned long long)total * (unsigned)__popc(am);
@@ -625,18 +599,13 @@ int lane_list_cap(int k) {
 // in-bracket buffer and most lanes would fall back anyway
 bool lane_supported(int k) { return k <= 160 && lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
-                 int seed_stride, float margin) {
-  static const bool batch = getenv("SPH_LANE_BATCH") ? atoi(getenv("SPH_LANE_BATCH")) != 0 : false;
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms) {
   const int smem = kLWarps * lane_smem_bytes(lcap);
-  const int ms = std::min(max_stream, 60000 - kCells * 0 - 4096);  // 16-bit run offsets (a step adds < 1024)
-  auto go = [&](auto kern) {
-    int bps = 0;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kLWarps * 32, smem);
-    kern<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms, seed_stride, margin);
-  };
-  if (batch) go(k_lane<true>); else go(k_lane<false>);
+  const int ms = std::min(max_stream, 60000 - 4096);  // 16-bit run offsets (a step adds < 1024)
+  int bps = 0;
+  cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lane, kLWarps * 32, smem);
+  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms);
 }
 
 }  // namespace sph

@@ -4,12 +4,9 @@ The default pass: seeds (every 12th sorted target) through the general
 per-target kernel, then the lane kernel (sph_lane.cu: bundles of 32 sorted
 neighbours, one lane per target) and, for what it leaves, neighbour-cell
 lists and the per-target kernel (SPH_KNOWN=0: the per-target kernel for every
-non-seed target).  The alternative pipelines are
-the per-cell group kernel (sph_group.cu) started from the tree estimate
-(SPH_KNOWN=2) or from the seeds (SPH_KNOWN=3), whose leftovers go back to the
-general kernel.  The fallbacks (the collect instance for overflowed neighbour
-lists, the walking select/density kernels, the general kernel for targets the
-group kernel cannot finish) only run on a few targets of large inputs, so
+non-seed target).  The fallbacks (the per-target kernel for what the lane
+kernel leaves, the collect instance for overflowed neighbour lists, the
+walking select/density kernels) only run on a few targets of large inputs, so
 they are forced here with margins and list capacities.  Each configuration
 runs in a fresh process because the switches are read when the library
 context is created.
@@ -31,16 +28,14 @@ CONFIGS = {
     "lane_tight_margin": {"SPH_LANEM": "1.0"},                      # many lanes with < K within R: per-target kernel
     "lane_wide_margin_short_lists": {"SPH_LANEM": "1.8", "SPH_LANE_LEXTRA": "8"},   # full lists, crowded brackets
     "lane_short_streams": {"SPH_LANE_STREAM": "600"},              # most bundles bail to the per-target kernel
-    "lane_no_exclusion_batched": {"SPH_LANEX": "0", "SPH_LANE_BATCH": "1"},
-    "group_from_tree_estimate": {"SPH_KNOWN": "2"},
-    "group_from_seeds": {"SPH_KNOWN": "3"},
-    "group_g8_short_lists": {"SPH_KNOWN": "2", "SPH_GROUP_G": "8", "SPH_GROUP_LCAP": "96"},  # retries, full lists
-    "group_tight_margin": {"SPH_KNOWN": "3", "SPH_SEEDM": "1.0"},   # many targets with < K within R: retries
-    "group_wide_margin": {"SPH_KNOWN": "3", "SPH_SEEDM": "1.7"},    # many full lists: retries / general kernel
-    "cell_lists_far_records": {"SPH_NEARF": "0.3"},
-    "per_target_small_lists": {"SPH_TLISTCAP": "1"},
-    "per_target_seed_stride_8": {"SPH_SEED": "8"},
-    "per_target_crowded_brackets": {"SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
+    "lane_no_exclusion": {"SPH_LANEX": "0"},
+    "cell_lists_far_records": {"SPH_KNOWN": "0", "SPH_NEARF": "0.3"},
+    "lane_then_cell_lists_far_records": {"SPH_NEARF": "0.3"},
+    "per_target_small_lists": {"SPH_KNOWN": "0", "SPH_TLISTCAP": "1"},
+    "lane_then_small_lists": {"SPH_TLISTCAP": "1", "SPH_LANE_STREAM": "900"},
+    "per_target_seed_stride_8": {"SPH_KNOWN": "0", "SPH_SEED": "8"},
+    "lane_seed_stride_8": {"SPH_SEED": "8"},
+    "per_target_crowded_brackets": {"SPH_KNOWN": "0", "SPH_TLISTCAP": "1", "SPH_CCAP": "48"},
     "per_target_unseeded_no_cell_lists": {"SPH_SEED": "0", "SPH_CLIST": "0"},
 }
 
