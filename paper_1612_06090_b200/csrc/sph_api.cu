@@ -87,6 +87,9 @@ struct sph_ctx {
   float seed_margin = 1.1f;  // SPH_SEEDM: non-seed radius = margin x the neighbouring seeds' h
   int known = 5;          // SPH_KNOWN: 5 seeds + lane kernel + per-target kernel for what it leaves (default), 0 seeds + per-target kernel for every other target
   float lane_margin = 1.15f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
+  float lane_noseed = 1.0f;   // SPH_LANE_NOSEED: > 0: no dense seeds, lane radius = this x the calibrated tree estimate (0: seeds every seed_stride-th target)
+  int lane_cal_stride = 256;  // SPH_LANE_CAL: calibration sample = every this-th sorted target
+  float lane_cal_q = 0.88f;   // SPH_LANE_CALQ: quantile of h / R0 over the sample that scales the tree estimate
   int lane_stream = 2400;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
   float lane_exc = 2.0f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   bool known_ran = false;
@@ -109,6 +112,7 @@ struct sph_ctx {
   int octree_f32 = 0;
   PassArgs octree_args{};
   DevBuf<uint32_t> seeds;
+  DevBuf<float> calbuf;   // 64 histogram words of log(h / R0), then the sampled targets' R0
   int collect_cap = 1024;  // SPH_CCAP: list capacity of the collect instance
   cudaStream_t stream2 = nullptr;  // side stream for host-to-device copies the first kernels do not need
   cudaEvent_t ev_side_start = nullptr, ev_mass = nullptr, ev_h = nullptr;
@@ -172,6 +176,28 @@ __global__ void k_append_sgs(const int2 *tasks, const int *count, int4 *sgs, int
 __global__ void k_state_map(int n, uint8_t *state, uint8_t from, uint8_t to) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && state[i] == from) state[i] = to;
+}
+
+// calibration sample of the tree's radius estimate (the lane kernel without dense seeds): R0 of every
+// stride-th target saved before the per-target kernel overwrites it, then a 64-bin histogram of
+// log(h / R0) over [-1.5, 1.5) in the first 64 words
+__global__ void k_cal_save(int ns, int stride, const float *__restrict__ r0, float *__restrict__ cal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 64) reinterpret_cast<int *>(cal)[i] = 0;
+  if (i < ns) cal[64 + i] = r0[(size_t)i * stride];
+}
+__global__ void k_cal_reduce(int ns, int stride, const uint8_t *__restrict__ state, const double *__restrict__ d2k,
+                             float *__restrict__ cal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const size_t p = (size_t)i * stride;
+  const double d = d2k[p];
+  const float r = cal[64 + i];
+  if (state[p] == ST_FINAL && d > 0.0 && d < 1e300 && r > 0.f) {
+    const float v = 0.5f * logf((float)d) - logf(r);
+    const int b = min(max((int)((v + 1.5f) * (64.0f / 3.0f)), 0), 63);
+    atomicAdd(reinterpret_cast<int *>(cal) + b, 1);
+  }
 }
 
 // seed targets for the per-target pass: every stride-th sorted position
@@ -715,6 +741,11 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     // its neighbouring seeds' converged h (sorted neighbours are spatial
     // neighbours): the known-radius kernel takes them
     const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
+    const float noseed_m = ctx->lane_noseed;
+    const int cal_stride = ctx->lane_cal_stride;
+    const float cal_q = ctx->lane_cal_q;
+    const bool noseed = noseed_m > 0.f && compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k) &&
+                        !(n_targets < n || sliced);
     SPH_CK(ctx->seeds.ensure(ns));
     PassArgs sa = a;
     sa.list = ctx->seeds.p;
@@ -735,6 +766,16 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       launches += 5;
       a.list = ctx->tlist.p;  // walk the compacted targets, not every position
       a.list_count = ctx->qints.p + 28;
+    } else if (noseed) {
+      // no dense seeds: the lane kernel starts every target from the tree's radius estimate, scaled by the
+      // geometric mean of h / R0 over a sparse sample (every cal_stride-th target through the per-target kernel)
+      const int ncal = (n + cal_stride - 1) / cal_stride;
+      SPH_CK(ctx->calbuf.ensure(ncal + 64 + (n < 64 ? 64 : 0)));
+      k_seed_list<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->seeds.p, ctx->qints.p + 14);
+      k_cal_save<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->r0.p, ctx->calbuf.p);
+      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+      k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
+      launches += 4;
     } else {
       k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
       launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
@@ -756,8 +797,8 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       ka.fb_list = ctx->kn_list.p;
       ka.fb_count = ctx->qints.p + 21;
       ka.kn_counters = ctx->qints.p + 10;
-      launch_lane(ctx->stream, ka, lane_list_cap(k), ctx->lane_margin / ctx->seed_margin, ctx->lane_exc, ctx->lane_stream,
-                  ctx->num_sms);
+      launch_lane(ctx->stream, ka, lane_list_cap(k), noseed ? noseed_m : ctx->lane_margin / ctx->seed_margin, ctx->lane_exc,
+                  ctx->lane_stream, ctx->num_sms, noseed ? ctx->calbuf.p : nullptr, cal_q);
       cudaEventRecord(ctx->kev_known[1], ctx->stream);
       SPH_CK(cudaMemsetAsync(a.work_counter, 0, sizeof(int), ctx->stream));
       a.list = ctx->kn_list.p;
@@ -999,6 +1040,9 @@ int sph_ctx_create(sph_ctx **out, int device) {
   if (const char *v = getenv("SPH_LANEM")) c->lane_margin = (float)atof(v);
   if (const char *v = getenv("SPH_LANEX")) c->lane_exc = (float)atof(v);
   if (const char *v = getenv("SPH_LANE_STREAM")) c->lane_stream = atoi(v);
+  if (const char *v = getenv("SPH_LANE_NOSEED")) c->lane_noseed = (float)atof(v);
+  if (const char *v = getenv("SPH_LANE_CAL")) c->lane_cal_stride = std::max(16, atoi(v));
+  if (const char *v = getenv("SPH_LANE_CALQ")) c->lane_cal_q = (float)atof(v);
   if (const char *v = getenv("SPH_CLIST")) c->cell_lists = atoi(v);
   if (const char *v = getenv("SPH_CCAP")) c->collect_cap = std::max(32, std::min(1024, atoi(v)));
   if (const char *v = getenv("SPH_TSHRINK")) c->tshrink = atoi(v);
@@ -1019,7 +1063,7 @@ void sph_ctx_destroy(sph_ctx *c) {
   c->idx_in.release(); c->idx.release(); c->perm.release(); c->deep_list.release(); c->deep_segs.release(); c->iota.release();
   c->list.release(); c->lvl8.release(); c->lvl32.release(); c->state.release(); c->ints.release();
   c->noff.release(); c->nlo.release(); c->nhi.release(); c->nsize.release(); c->r0.release(); c->pos_sorted.release();
-  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->seeds.release(); c->node_p.release();
+  c->cub_temp.release(); c->tasks.release(); c->members.release(); c->seeds.release(); c->calbuf.release(); c->node_p.release();
   c->dscratch.release(); c->ncell_dev.release(); c->tlist.release(); c->clist.release(); c->clen.release();
   c->cellidx.release(); c->cellnode.release(); c->crad2.release(); c->cnear.release(); c->ncount.release();
   c->crec.release(); c->anc4.release(); c->parent.release(); c->cellof.release(); c->qints.release();

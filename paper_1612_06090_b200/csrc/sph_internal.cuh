@@ -237,7 +237,8 @@ void launch_pass(cudaStream_t s, int mode, int f32, const PassArgs &a, int count
 // one lane per target over bundles of 32 consecutive sorted targets (sph_lane.cu)
 int lane_list_cap(int k);
 bool lane_supported(int k);
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms);
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
+                 const float *cal = nullptr, float calq = 0.85f);
 // fused per-target search + select + density (sph_warp.cu)
 int target_list_cap(int k);
 void launch_target(cudaStream_t s, int f32, const PassArgs &a, int cap, int *fallbacks, int num_sms,

@@ -107,7 +107,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // counters (a.kn_counters): [0] bundles bailed (table / stack / cell size), [1] lanes with fewer than K within R,
 // [2] lanes whose list would overflow, [3] lanes whose bracket could not be ranked, [13] lanes left out of their
 // bundle (far from its bulk / periodic face)
-__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream) {
+__global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lcap, float rscale, float exc, int max_stream, const float *cal, float calq) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -142,6 +142,31 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
 
   unsigned long long tests = 0, accepted = 0;
   int c_bail = 0, c_few = 0, c_full = 0, c_rank = 0, c_out = 0;
+  // calibration of the tree's radius estimate: the calq quantile of log(h / R0) over a sparse sample of
+  // converged targets (64 bins over [-1.5, 1.5))
+  if (cal) {
+    const int *cb = reinterpret_cast<const int *>(cal);
+    const int c0 = cb[2 * lane], c1 = cb[2 * lane + 1];
+    int incl = c0 + c1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    if (total > 0) {
+      const float want = calq * (float)total;
+      const int excl = incl - c0 - c1;
+      const bool here = (float)incl >= want && (float)excl < want;
+      float lg = 0.f;
+      if (here) {
+        const float pos = (float)excl + (float)c0 >= want ? (float)(2 * lane) + (want - (float)excl) / fmaxf((float)c0, 1.f)
+                                                           : (float)(2 * lane + 1) + (want - (float)(excl + c0)) / fmaxf((float)c1, 1.f);
+        lg = -1.5f + pos * (3.0f / 64.0f);
+      }
+      const unsigned hm = __ballot_sync(FULL, here);
+      if (hm) rscale *= expf(__shfl_sync(FULL, lg, __ffs(hm) - 1));
+    }
+  }
 
   const int nb = (n + 31) >> 5;
   for (;;) {
@@ -561,7 +586,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
     }
     // ---- what is left goes to the per-target kernel ----
     const unsigned fm = __ballot_sync(FULL, want && !done);
-    if (fm) {
+    if (fm && a.fb_list) {
       int base = 0;
       if (lane == 0) base = atomicAdd(a.fb_count, __popc(fm));
       base = __shfl_sync(FULL, base, 0);
@@ -599,13 +624,14 @@ int lane_list_cap(int k) {
 // in-bracket buffer and most lanes would fall back anyway
 bool lane_supported(int k) { return k <= 160 && lane_smem_bytes(lane_list_cap(k)) * kLWarps <= 220 * 1024; }
 
-void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms) {
+void launch_lane(cudaStream_t s, const PassArgs &a, int lcap, float rscale, float exc, int max_stream, int num_sms,
+                 const float *cal, float calq) {
   const int smem = kLWarps * lane_smem_bytes(lcap);
   const int ms = std::min(max_stream, 60000 - 4096);  // 16-bit run offsets (a step adds < 1024)
   int bps = 0;
   cudaFuncSetAttribute(k_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lane, kLWarps * 32, smem);
-  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms);
+  k_lane<<<num_sms * std::max(bps, 1), kLWarps * 32, smem, s>>>(a, lcap, rscale, exc, ms, cal, calq);
 }
 
 }  // namespace sph

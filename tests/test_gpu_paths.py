@@ -29,6 +29,9 @@ CONFIGS = {
     "lane_wide_margin_short_lists": {"SPH_LANEM": "1.8", "SPH_LANE_LEXTRA": "8"},   # full lists, crowded brackets
     "lane_short_streams": {"SPH_LANE_STREAM": "600"},              # most bundles bail to the per-target kernel
     "lane_no_exclusion": {"SPH_LANEX": "0"},
+    "lane_from_dense_seeds": {"SPH_LANE_NOSEED": "0"},
+    "lane_low_quantile": {"SPH_LANE_CALQ": "0.3"},                  # most lanes with < K within R
+    "lane_high_quantile_sparse_sample": {"SPH_LANE_CALQ": "0.99", "SPH_LANE_CAL": "2048"},
     "cell_lists_far_records": {"SPH_KNOWN": "0", "SPH_NEARF": "0.3"},
     "lane_then_cell_lists_far_records": {"SPH_NEARF": "0.3"},
     "per_target_small_lists": {"SPH_KNOWN": "0", "SPH_TLISTCAP": "1"},
