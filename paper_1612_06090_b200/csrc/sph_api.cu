@@ -181,16 +181,17 @@ __global__ void k_state_map(int n, uint8_t *state, uint8_t from, uint8_t to) {
 // calibration sample of the tree's radius estimate (the lane kernel without dense seeds): R0 of every
 // stride-th target saved before the per-target kernel overwrites it, then a 64-bin histogram of
 // log(h / R0) over [-1.5, 1.5) in the first 64 words
-__global__ void k_cal_save(int ns, int stride, const float *__restrict__ r0, float *__restrict__ cal) {
+__global__ void k_cal_save(int ns, const uint32_t *__restrict__ sample, const float *__restrict__ r0,
+                           float *__restrict__ cal) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 64) reinterpret_cast<int *>(cal)[i] = 0;
-  if (i < ns) cal[64 + i] = r0[(size_t)i * stride];
+  if (i < ns) cal[64 + i] = r0[sample[i]];
 }
-__global__ void k_cal_reduce(int ns, int stride, const uint8_t *__restrict__ state, const double *__restrict__ d2k,
-                             float *__restrict__ cal) {
+__global__ void k_cal_reduce(int ns, const uint32_t *__restrict__ sample, const uint8_t *__restrict__ state,
+                             const double *__restrict__ d2k, float *__restrict__ cal) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ns) return;
-  const size_t p = (size_t)i * stride;
+  const size_t p = sample[i];
   const double d = d2k[p];
   const float r = cal[64 + i];
   if (state[p] == ST_FINAL && d > 0.0 && d < 1e300 && r > 0.f) {
@@ -744,8 +745,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     const float noseed_m = ctx->lane_noseed;
     const int cal_stride = ctx->lane_cal_stride;
     const float cal_q = ctx->lane_cal_q;
-    const bool noseed = noseed_m > 0.f && compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k) &&
-                        !(n_targets < n || sliced);
+    const bool noseed = noseed_m > 0.f && compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k);
     SPH_CK(ctx->seeds.ensure(ns));
     PassArgs sa = a;
     sa.list = ctx->seeds.p;
@@ -756,6 +756,16 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       launch_select(ctx->stream, ctx->iota.p, n, ctx->state.p, ST_NEED_HIST, ctx->tlist.p, ctx->qints.p + 28,
                     ctx->cub_temp.p, ctx->cub_bytes);
       const int nt_eff = sliced ? shi - slo : n_targets;  // targets in the compacted list
+      if (noseed) {
+        // the calibration sample along the compacted target order
+        const int ncal = (nt_eff + cal_stride - 1) / cal_stride;
+        SPH_CK(ctx->calbuf.ensure(ncal + 128));
+        k_seed_list_from<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->tlist.p, ctx->seeds.p,
+                                                              ctx->qints.p + 14);
+        k_cal_save<<<nblk(std::max(ncal, 64)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
+        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+        k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
+      } else {
       const int nst = (nt_eff + ctx->seed_stride - 1) / ctx->seed_stride;
       k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
                                                            ctx->qints.p + 14);
@@ -763,6 +773,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       k_seed_radius_from<<<nblk(nt_eff), kTB, 0, ctx->stream>>>(nt_eff, ctx->seed_stride, ctx->tlist.p,
                                                                    ctx->state.p, ctx->d2k.p, ctx->seed_margin, rmax,
                                                                    ctx->r0.p);
+      }
       launches += 5;
       a.list = ctx->tlist.p;  // walk the compacted targets, not every position
       a.list_count = ctx->qints.p + 28;
@@ -770,11 +781,11 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       // no dense seeds: the lane kernel starts every target from the tree's radius estimate, scaled by the
       // geometric mean of h / R0 over a sparse sample (every cal_stride-th target through the per-target kernel)
       const int ncal = (n + cal_stride - 1) / cal_stride;
-      SPH_CK(ctx->calbuf.ensure(ncal + 64 + (n < 64 ? 64 : 0)));
+      SPH_CK(ctx->calbuf.ensure(ncal + 128));
       k_seed_list<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->seeds.p, ctx->qints.p + 14);
-      k_cal_save<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->r0.p, ctx->calbuf.p);
+      k_cal_save<<<nblk(std::max(ncal, 64)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
       launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-      k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
+      k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
       launches += 4;
     } else {
       k_seed_list<<<nblk(ns), kTB, 0, ctx->stream>>>(ns, ctx->seed_stride, ctx->seeds.p, ctx->qints.p + 14);
