@@ -52,7 +52,10 @@ constexpr int kLWarps = 2;
 #endif
 constexpr int kTile = SPH_LANE_TILE;    // candidates per staged tile (>= the largest search cell)
 constexpr int kCells = SPH_LANE_CELLS;   // runs of cells per bundle
-constexpr int kBins = 64;     // histogram bins over [0, R^2)
+#ifndef SPH_LANE_BINS
+#define SPH_LANE_BINS 64
+#endif
+constexpr int kBins = SPH_LANE_BINS;     // histogram bins over [0, R^2)
 constexpr int kLStack = 96;   // traversal stack (internal node ids)
 constexpr int kInb = kTile / 8;  // in-bracket entries per lane (doubles; alias the tile buffers)
 constexpr float kEps = 9.5367431640625e-07f;  // 2^-20 relative guard (as sph_warp.cu)

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kBins) k_digit_scan(const unsigned *__restrict
 struct SortSmem {
   unsigned long long keys[kTile];
   uint32_t vals[kTile];
-  unsigned whist[kSortWarps][kBins + 1];  // per-warp counters, then per-warp exclusive offsets
+  unsigned short whist[kSortWarps][kBins + 1];  // per-warp counters, then per-warp exclusive offsets (<= 4096: 16 bits keep three tiles per SM)
   unsigned dstart[kBins];                 // tile-local start of each digit's run
   unsigned gbase[kBins];                  // global position of each digit's run of this tile
   unsigned wsum[kSortWarps];
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(int n, int shift, con
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const unsigned lt = (1u << lane) - 1u;
   if (t == 0) S.tile = atomicAdd(counter, 1);
-  for (int i = t; i < kSortWarps * (kBins + 1); i += kSortThreads) (&S.whist[0][0])[i] = 0u;
+  for (int i = t; i < kSortWarps * (kBins + 1); i += kSortThreads) (&S.whist[0][0])[i] = 0;
   __syncthreads();
   const int tile = S.tile;
   const int64_t base = (int64_t)tile * kTile;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(int n, int shift, con
     const unsigned old = S.whist[w][d];
     rank[j] = old + __popc(peers & lt);
     __syncwarp();
-    if (lane == 31 - __clz(peers)) S.whist[w][d] = old + __popc(peers);
+    if (lane == 31 - __clz(peers)) S.whist[w][d] = (unsigned short)(old + __popc(peers));
     __syncwarp();
   }
   __syncthreads();
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(int n, int shift, con
   unsigned cnt = 0;
   for (int ww = 0; ww < kSortWarps; ++ww) {
     const unsigned c = S.whist[ww][t];
-    S.whist[ww][t] = cnt;
+    S.whist[ww][t] = (unsigned short)cnt;
     cnt += c;
   }
   // tile-local start of each digit's run: exclusive scan over digits
