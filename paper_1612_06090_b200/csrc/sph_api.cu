@@ -500,7 +500,9 @@ PassArgs base_args(sph_ctx *ctx, int n, int k, int n_nodes, const sph_params *pr
   a.tree.n_nodes = n_nodes;
   a.pos = ctx->pos_sorted.p;
   a.mass64 = ctx->mass_s.p;
-  a.dens64 = prm ? (prm->precision != SPH_PRECISION_F32) : 0;
+  // fp32 per-pair density sums stay within rel 1e-4 up to a few thousand terms; beyond that (K near n) the
+  // terms are summed in fp64 like the fp64 / auto paths (tools/fuzz.py: K = 39,143 gave 1.2e-4 in fp32)
+  a.dens64 = prm ? (prm->precision != SPH_PRECISION_F32 || k > 2048) : 0;
   a.radius = ctx->r0.p;
   a.t_lo = ctx->t_lo.p;
   a.t_hi = ctx->t_hi.p;

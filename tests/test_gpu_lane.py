@@ -63,3 +63,20 @@ def test_lane_kernel_ignores_ghosts_as_targets():
 def test_lane_kernel_periodic_box():
     pos, _, _ = workload.nfw_halos(50000, 12.0, 30, seed=9)
     _check(pos.astype(np.float32), np.ones(50000), 64, box=12.0)
+
+
+def test_k_near_n_periodic_fp32_density_within_tolerance():
+    """K beyond n in a periodic box (the images supply the neighbours): tens of thousands of density terms per
+    particle, summed in fp64 above K = 2048 so rho stays within the fp32 path's rel 1e-4 (tools/fuzz.py case)."""
+    rng = np.random.default_rng(108)
+    n = 9000
+    pos = (rng.random((n, 3))).astype(np.float32)
+    pos[pos >= 1.0] = np.nextafter(np.float32(1.0), np.float32(0.0))
+    k = n + 5
+    p64 = pos.astype(np.float64)
+    mass = rng.random(n) + 0.5
+    h0 = np.full(n, sph.initial_smoothing_length(1.0, n, k))
+    want = oracle.density_pass_periodic(p64[:, 0], p64[:, 1], p64[:, 2], mass, h0, k, 1.0)
+    h, rho, _, st = sph.density_pass_soa(pos[:, 0], pos[:, 1], pos[:, 2], mass, h0, k, periodic=True, box=1.0)
+    assert np.array_equal(h, want.h)
+    assert float(np.max(np.abs(rho - want.rho) / want.rho)) <= 1e-5
