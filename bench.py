@@ -484,7 +484,7 @@ def run_ours(args):
     total_particles = float(n_total.item())
     value = total_particles * k / (ms_max * 1e-3)
 
-    # ---- roofline of the search launches (k_target seeds + k_lane + k_target leftovers: 92 % of the pass) ----
+    # ---- roofline of the search launches (k_target calibration sample + k_lane + k_target leftovers: 92 % of the pass) ----
     peak_ffma = float(L.sph_fp32_peak(ctx))
     t_k = kern["search"] + kern["select"] + kern["density"]
     ops = 6.0 * tests + 10.0 * accepted
@@ -510,7 +510,7 @@ def run_ours(args):
             "converged_particles_per_s": total_particles / (ms_max * 1e-3),
             "gpu_launches": launches // args.steps,
             "clocks": clk,
-            "roofline": {"bound": "fp32", "kernel": "search launches: k_lane (one lane per target over bundles of 32 sorted neighbours) + k_target (seeds and what k_lane leaves)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "fp32", "kernel": "search launches: k_lane (one lane per target over bundles of 32 sorted neighbours) + k_target (the calibration sample and what k_lane leaves)", "achieved": achieved, "peak": peak,
                          "unit": "Tops/s (fp32-pipe ops)", "frac": achieved / peak if peak else None,
                          "traffic": traffic,
                          "peak_source": "measured FFMA issue rate on this B200 (sph_fp32_peak); MEASURED_PEAKS.json "

@@ -739,10 +739,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
   bool known_run = false;
   const bool seeded = ctx->seed_stride > 1 && n >= 64 * ctx->seed_stride;
   if (seeded) {
-    // seeds first (every seed_stride-th sorted position, the general kernel
-    // from the tree's radius estimate), then every other target starts from
-    // its neighbouring seeds' converged h (sorted neighbours are spatial
-    // neighbours): the known-radius kernel takes them
+    // a sparse calibration sample (or, SPH_LANE_NOSEED=0 / fp64 sets, seeds at every seed_stride-th sorted
+    // position) through the general kernel from the tree's radius estimate; every other target then starts
+    // from that estimate scaled by the sample's h / R0 quantile (or from its neighbouring seeds' converged h)
     const int ns = (n + ctx->seed_stride - 1) / ctx->seed_stride;
     const float noseed_m = ctx->lane_noseed;
     const int cal_stride = ctx->lane_cal_stride;
@@ -768,13 +767,13 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
         launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
         k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
       } else {
-      const int nst = (nt_eff + ctx->seed_stride - 1) / ctx->seed_stride;
-      k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
-                                                           ctx->qints.p + 14);
-      launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
-      k_seed_radius_from<<<nblk(nt_eff), kTB, 0, ctx->stream>>>(nt_eff, ctx->seed_stride, ctx->tlist.p,
-                                                                   ctx->state.p, ctx->d2k.p, ctx->seed_margin, rmax,
-                                                                   ctx->r0.p);
+        const int nst = (nt_eff + ctx->seed_stride - 1) / ctx->seed_stride;
+        k_seed_list_from<<<nblk(nst), kTB, 0, ctx->stream>>>(nst, ctx->seed_stride, ctx->tlist.p, ctx->seeds.p,
+                                                             ctx->qints.p + 14);
+        launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
+        k_seed_radius_from<<<nblk(nt_eff), kTB, 0, ctx->stream>>>(nt_eff, ctx->seed_stride, ctx->tlist.p,
+                                                                     ctx->state.p, ctx->d2k.p, ctx->seed_margin, rmax,
+                                                                     ctx->r0.p);
       }
       launches += 5;
       a.list = ctx->tlist.p;  // walk the compacted targets, not every position

@@ -1,4 +1,5 @@
-# full ncu captures of the search launches on C3 (the bench config): k_target seeds, k_lane, k_target leftovers
+# full ncu captures of the search launches on C3 (the bench config): k_target over the calibration sample,
+# k_lane, k_target over what k_lane leaves
 # usage: bash tools/gpu_ncu_c3.sh TAG
 cd $GRAFT_REPO_ROOT
 TAG=${1:-rXX}
@@ -9,7 +10,7 @@ cap() {  # name regex skip
   echo "$1 rc=$?"
   ncu -i gpurun_out/${TAG}_$1_c3.ncu-rep --page details > gpurun_out/${TAG}_$1_c3_details.txt 2>&1
 }
-cap k_target_seed "^k_target$" 0
+cap k_target_sample "^k_target$" 0
 cap k_lane "^k_lane$" 0
 cap k_target_rest "^k_target$" 1
 python tools/traffic_json.py $TAG 3
