@@ -746,7 +746,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     const float noseed_m = ctx->lane_noseed;
     const int cal_stride = ctx->lane_cal_stride;
     const float cal_q = ctx->lane_cal_q;
-    const bool noseed = noseed_m > 0.f && compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k);
+    const bool noseed = noseed_m > 0.f && compute_f32 && ctx->known == 5 && lane_supported(k);
     SPH_CK(ctx->seeds.ensure(ns));
     PassArgs sa = a;
     sa.list = ctx->seeds.p;
@@ -800,7 +800,7 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
     const int cap = ctx->cell_lists;
     const int ncell = ctx->last_ncell;  // counted with the tree (stage_tree)
     bool lane_ran = false;
-    if (compute_f32 && ctx->known == 5 && !a.dens64 && lane_supported(k) && ctx->kn_list.ensure(n) == cudaSuccess) {
+    if (compute_f32 && ctx->known == 5 && lane_supported(k) && ctx->kn_list.ensure(n) == cudaSuccess) {
       // one lane per target over bundles of 32 sorted neighbours (sph_lane.cu);
       // what it leaves, the per-target kernel takes
       cudaEventRecord(ctx->kev_known[0], ctx->stream);

@@ -565,6 +565,32 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
                 if (q < 1.f) accf = fmaf(c.w, wv, accf);
               }
             };
+            if (a.dens64) {
+              // fp64 positions that are fp32 values (precision "auto"): every term as the reference computes it
+              // (density.py:160-171: exact d2, sqrt, W, mass in fp64); only the order of the sum differs
+              double accd = 0.0;
+              for (int e = 0; e < cnt; ++e) {
+                const int j = entry(e * 32 + lane);
+                const float4 c = pos[j];
+                const float dx = c.x - t.x, dy = c.y - t.y, dz = c.z - t.z;
+                if (!(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < d2k_f)) continue;
+                const double ex = exact_d2(__dsub_rn((double)c.x, (double)t.x), __dsub_rn((double)c.y, (double)t.y),
+                                           __dsub_rn((double)c.z, (double)t.z));
+                if (ex < d2k) {
+                  ++accepted;
+                  const double r_ = __dsqrt_rn(ex);
+                  double wv;
+                  if (a.kernel_kind == 0) {
+                    wv = wc6_lowered(r_, hh, norm_h3);
+                  } else {
+                    const double q = __ddiv_rn(r_, hh);
+                    wv = q < 1.0 ? norm_h3 * m4_profile(q) : 0.0;
+                  }
+                  accd = __dadd_rn(accd, __dmul_rn(a.mass64[j], wv));
+                }
+              }
+              rho = accd;
+            } else {
             int e = 0;
             for (; e + 4 <= cnt; e += 4) {
               float4 c[4];
@@ -575,6 +601,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
             }
             for (; e < cnt; ++e) term(pos[entry(e * 32 + lane)]);
             rho = __dmul_rn(norm_h3, (double)accf);
+            }
           }
           if (ok) {
             a.d2k[p] = d2k;
