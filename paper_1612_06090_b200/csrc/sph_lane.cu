@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
           ++c_few;
           // the per-target kernel starts from the radius the count within R suggests (its own growth rule)
           const int others = cum - 1;
-          const float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.15f : 2.f;
+          const float f = others > 0 ? cbrtf((float)(K + 8) / (float)others) * 1.1f : 2.f;
           a.radius[p] = fminf(R * fminf(fmaxf(f, 1.1f), 2.5f), a.rmax);
         }
         // a lane that does not finish below still knows the K-th lies in bin bsel: a tight radius for the
