@@ -89,7 +89,7 @@ struct sph_ctx {
   float lane_margin = 1.15f;  // SPH_LANEM: lane kernel radius = this x the neighbouring seeds' h
   float lane_noseed = 1.0f;   // SPH_LANE_NOSEED: > 0: no dense seeds, lane radius = this x the calibrated tree estimate (0: seeds every seed_stride-th target)
   int lane_cal_stride = 256;  // SPH_LANE_CAL: calibration sample = every this-th sorted target
-  float lane_cal_q = 0.88f;   // SPH_LANE_CALQ: quantile of h / R0 over the sample that scales the tree estimate
+  float lane_cal_q = 0.92f;   // SPH_LANE_CALQ: quantile of h / R0 (per class of R0) over the sample that scales the tree estimate
   int lane_stream = 2400;     // SPH_LANE_STREAM: bundles streaming more candidates than this go to the per-target kernel
   float lane_exc = 2.0f;      // SPH_LANEX: lanes reaching beyond this x the bundle's median reach are left out (0: none)
   bool known_ran = false;
@@ -179,13 +179,14 @@ __global__ void k_state_map(int n, uint8_t *state, uint8_t from, uint8_t to) {
 }
 
 // calibration sample of the tree's radius estimate (the lane kernel without dense seeds): R0 of every
-// stride-th target saved before the per-target kernel overwrites it, then a 64-bin histogram of
-// log(h / R0) over [-1.5, 1.5) in the first 64 words
+// sampled target saved before the per-target kernel overwrites it, then 64-bin histograms of log(h / R0)
+// over [-1.5, 1.5), one per class of R0 (half octaves, 16 classes), in the first 1024 words
+constexpr int kCalWords = 16 * 64;
 __global__ void k_cal_save(int ns, const uint32_t *__restrict__ sample, const float *__restrict__ r0,
                            float *__restrict__ cal) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < 64) reinterpret_cast<int *>(cal)[i] = 0;
-  if (i < ns) cal[64 + i] = r0[sample[i]];
+  if (i < kCalWords) reinterpret_cast<int *>(cal)[i] = 0;
+  if (i < ns) cal[kCalWords + i] = r0[sample[i]];
 }
 __global__ void k_cal_reduce(int ns, const uint32_t *__restrict__ sample, const uint8_t *__restrict__ state,
                              const double *__restrict__ d2k, float *__restrict__ cal) {
@@ -193,11 +194,12 @@ __global__ void k_cal_reduce(int ns, const uint32_t *__restrict__ sample, const 
   if (i >= ns) return;
   const size_t p = sample[i];
   const double d = d2k[p];
-  const float r = cal[64 + i];
+  const float r = cal[kCalWords + i];
   if (state[p] == ST_FINAL && d > 0.0 && d < 1e300 && r > 0.f) {
     const float v = 0.5f * logf((float)d) - logf(r);
     const int b = min(max((int)((v + 1.5f) * (64.0f / 3.0f)), 0), 63);
-    atomicAdd(reinterpret_cast<int *>(cal) + b, 1);
+    const int cls = (__float_as_int(r) >> 22) & 15;
+    atomicAdd(reinterpret_cast<int *>(cal) + cls * 64 + b, 1);
   }
 }
 
@@ -760,10 +762,10 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       if (noseed) {
         // the calibration sample along the compacted target order
         const int ncal = (nt_eff + cal_stride - 1) / cal_stride;
-        SPH_CK(ctx->calbuf.ensure(ncal + 128));
+        SPH_CK(ctx->calbuf.ensure(ncal + kCalWords + 64));
         k_seed_list_from<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->tlist.p, ctx->seeds.p,
                                                               ctx->qints.p + 14);
-        k_cal_save<<<nblk(std::max(ncal, 64)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
+        k_cal_save<<<nblk(std::max(ncal, kCalWords)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
         launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
         k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
       } else {
@@ -782,9 +784,9 @@ int density_pass_dev(sph_ctx *ctx, const sph_params *prm, const void *x, const v
       // no dense seeds: the lane kernel starts every target from the tree's radius estimate, scaled by the
       // geometric mean of h / R0 over a sparse sample (every cal_stride-th target through the per-target kernel)
       const int ncal = (n + cal_stride - 1) / cal_stride;
-      SPH_CK(ctx->calbuf.ensure(ncal + 128));
+      SPH_CK(ctx->calbuf.ensure(ncal + kCalWords + 64));
       k_seed_list<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, cal_stride, ctx->seeds.p, ctx->qints.p + 14);
-      k_cal_save<<<nblk(std::max(ncal, 64)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
+      k_cal_save<<<nblk(std::max(ncal, kCalWords)), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->r0.p, ctx->calbuf.p);
       launch_target(ctx->stream, compute_f32, sa, target_list_cap(k), ctx->qints.p + 5, ctx->num_sms);
       k_cal_reduce<<<nblk(ncal), kTB, 0, ctx->stream>>>(ncal, ctx->seeds.p, ctx->state.p, ctx->d2k.p, ctx->calbuf.p);
       launches += 4;

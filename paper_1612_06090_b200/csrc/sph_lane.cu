@@ -146,30 +146,36 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
   unsigned long long tests = 0, accepted = 0;
   int c_bail = 0, c_few = 0, c_full = 0, c_rank = 0, c_out = 0;
   // calibration of the tree's radius estimate: the calq quantile of log(h / R0) over a sparse sample of
-  // converged targets (64 bins over [-1.5, 1.5))
+  // converged targets, per class of R0 (half octaves, 16 classes: the estimate's bias depends on the local
+  // scale), 64 bins over [-1.5, 1.5) each; lane c < 16 holds class c's log-quantile, classes with fewer than
+  // 64 samples use the quantile over all classes
+  float qcls = 0.f;
   if (cal) {
     const int *cb = reinterpret_cast<const int *>(cal);
-    const int c0 = cb[2 * lane], c1 = cb[2 * lane + 1];
-    int incl = c0 + c1;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(FULL, incl, 31);
-    if (total > 0) {
+    auto quantile = [&](auto count_of) {  // count_of(bin) -> samples in that bin
+      int total = 0;
+      for (int bb = 0; bb < 64; ++bb) total += count_of(bb);
+      if (total < 64) return make_float2(0.f, (float)total);
       const float want = calq * (float)total;
-      const int excl = incl - c0 - c1;
-      const bool here = (float)incl >= want && (float)excl < want;
-      float lg = 0.f;
-      if (here) {
-        const float pos = (float)excl + (float)c0 >= want ? (float)(2 * lane) + (want - (float)excl) / fmaxf((float)c0, 1.f)
-                                                           : (float)(2 * lane + 1) + (want - (float)(excl + c0)) / fmaxf((float)c1, 1.f);
-        lg = -1.5f + pos * (3.0f / 64.0f);
+      int cum = 0, bb = 0;
+      for (; bb < 63; ++bb) {
+        const int c = count_of(bb);
+        if ((float)(cum + c) >= want) break;
+        cum += c;
       }
-      const unsigned hm = __ballot_sync(FULL, here);
-      if (hm) rscale *= expf(__shfl_sync(FULL, lg, __ffs(hm) - 1));
-    }
+      const float frac = (want - (float)cum) / fmaxf((float)count_of(bb), 1.f);
+      return make_float2(-1.5f + ((float)bb + fminf(frac, 1.f)) * (3.0f / 64.0f), (float)total);
+    };
+    const float2 all = quantile([&](int bb) {
+      int c = 0;
+      for (int k = 0; k < 16; ++k) c += cb[k * 64 + bb];
+      return c;
+    });
+    const int mycls = lane & 15;
+    const float2 mine = quantile([&](int bb) { return cb[mycls * 64 + bb]; });
+    qcls = mine.y >= 64.f ? mine.x : all.x;
   }
+  auto r0_class = [](float r0) { return (__float_as_int(r0) >> 22) & 15; };
 
   const int nb = (n + 31) >> 5;
   for (;;) {
@@ -182,9 +188,11 @@ __global__ void __launch_bounds__(kLWarps * 32) k_lane(const PassArgs a, int lca
     bool act = want;
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     float R = 0.f;
+    const float r0v = want ? a.radius[p] : 1.f;
+    const float qf = cal ? expf(__shfl_sync(FULL, qcls, r0_class(r0v))) : 1.f;  // the class's h / R0 quantile
     if (want) {
       t = pos[p];
-      R = a.radius[p] * rscale;
+      R = r0v * rscale * qf;
       R = fminf(R, a.rmax);
       if (!(R > 0.f)) act = false;
       // spheres crossing a periodic face are searched with image shifts: the per-target kernel
