@@ -12,9 +12,13 @@
 // loops crosses lanes.  Per bundle (reference compute_density_pass,
 // density.py:286-413; the radius search of density.py:215-246 replaced by an
 // exact K-th selection):
-//   radius  R_i = margin x the larger converged h of the two seeds around the
-//           target (k_seed_radius); lanes far from the bundle's bulk or whose
-//           sphere crosses a periodic face are left to the per-target kernel;
+//   radius  R_i = the tree's estimate R0 of the target's cell x the calq
+//           quantile of h / R0 over a sparse calibration sample run through the
+//           per-target kernel first, per half-octave class of R0 (cal != null);
+//           or margin x the larger converged h of the two dense seeds around
+//           the target (k_seed_radius, cal == null); lanes far from the
+//           bundle's bulk or whose sphere crosses a periodic face are left to
+//           the per-target kernel;
 //   walk    the search tree once with the bundle box grown by max R (and the
 //           bundle's bounding sphere); each hit cell is kept if it meets at
 //           least one lane's own sphere; memory-adjacent cells merge into runs;
@@ -32,7 +36,7 @@
 //           (density.py:160-171, 249-261; kernel.py:30-45).
 // Lanes the bundle cannot finish (fewer than K within R_i, list or bracket too
 // crowded, table overflow) keep ST_NEED_HIST and are appended to fb_list for
-// the per-target kernel.
+// the per-target kernel, with a radius hint where the histogram gives one.
 #include "sph_internal.cuh"
 #include <climits>
 #include <cstdio>
